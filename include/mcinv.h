@@ -1,0 +1,175 @@
+/*
+ * mcinv.h -- C99 ABI of the B200-native correlated-chains (CC) Monte Carlo
+ * matrix inverter (Garcia-Cortes & Cabrillo, arXiv cs/0412107).
+ *
+ * The method (PAPER.md, "P:<line>"): many independent chains each update two
+ * coupled vectors z and w row by row in Gauss-Seidel order with a shared
+ * noise draw phi (Eq. 4 and Eq. 5; Eq. 5a/5b). After a
+ * burn-in of N sweeps the products z w^dagger average to C^-1 (Eq. 1/C,
+ * P:173-176), and w^dagger Q z to tr(Q C^-1) (Eq. tr; see
+ * DESIGN.md reading R2 for the conjugation). This library estimates, for a
+ * sparse real (f64) or complex (c128) C given in CSR form:
+ *   MCINV_DIAG    diag(C^-1)                     (n values)
+ *   MCINV_PATTERN selected elements (C^-1)_{ij}  (default: the pattern of C)
+ *   MCINV_FULL    the dense C^-1                 (n*n values, row-major)
+ *   MCINV_TRACE   tr(Q C^-1) for a sparse Q      (1 value)
+ * each with a Monte Carlo standard error from disjoint chain groups.
+ *
+ * Conventions
+ *  - Every call returns mcinv_status; no C++ exception crosses the ABI.
+ *  - Indices are 0-based. CSR: row_ptr[0] = 0, non-decreasing, row_ptr[n] =
+ *    nnz; col_idx in [0, n). Duplicates are summed; explicit zeros are kept.
+ *  - c128 values are interleaved double pairs (re, im); estimates and standard
+ *    errors of complex outputs are interleaved too (the standard error pair
+ *    holds the SE of the real and of the imaginary part).
+ *  - Host inputs are copied during the call; the caller may free them on
+ *    return. All device memory of C and Q is owned by the context.
+ *  - The hot path (mcinv_run) is asynchronous on the caller's CUDA stream.
+ *  - Thread safety: one context per host thread and stream.
+ *  - There is no CPU fallback: without a usable CUDA device every call that
+ *    needs one returns MCINV_E_CUDA.
+ */
+#ifndef MCINV_H
+#define MCINV_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct mcinv_ctx mcinv_ctx;   /* opaque; owns device copies of C and Q */
+
+typedef enum {
+    MCINV_OK = 0,
+    MCINV_E_INVALID = 1,      /* bad argument, bad CSR, non-finite value */
+    MCINV_E_ZERO_DIAG = 2,    /* missing or zero c_ii: D must be non-singular */
+    MCINV_E_DIAG_DOMAIN = 3,  /* real path with c_ii <= 0 (1/sqrt(c_ii) not real; use C128) */
+    MCINV_E_DIVERGED = 4,     /* non-finite or |z|,|w| > 1e12 at the end of a run: sp(T) or sp(S) >= 1 */
+    MCINV_E_NOMEM = 5,        /* device or host allocation failed */
+    MCINV_E_CUDA = 6,         /* CUDA runtime error (message via mcinv_error_detail) */
+    MCINV_E_BUFFER = 7,       /* caller buffer too small; required size via mcinv_error_detail */
+    MCINV_E_STATE = 8         /* call out of order (e.g. result before run, resume without state) */
+} mcinv_status;
+
+typedef enum { MCINV_F64 = 1, MCINV_C128 = 2 } mcinv_dtype;
+
+enum { MCINV_DIAG = 1u, MCINV_PATTERN = 2u, MCINV_FULL = 4u, MCINV_TRACE = 8u };
+
+/* Noise source for Eq. (4)/(5): Gaussian (production), or the constants 0 and
+ * 1 (test modes: zero noise reduces CC to Gauss-Seidel, Eq. 12). */
+enum { MCINV_NOISE_GAUSS = 0, MCINV_NOISE_ZERO = 1, MCINV_NOISE_ONE = 2 };
+
+/* Build a context for C on CUDA device `device`: validates the CSR, splits
+ * C = L + D + U, builds the row lists of Eq. (4) and the
+ * conjugated column lists of Eq. (5), 1/c_ii and 1/sqrt(c_ii) (principal
+ * branch; Eq. 5 uses their conjugates, reading R1), and uploads
+ * them. values: nnz doubles (F64) or 2*nnz doubles (C128).
+ * Errors: E_INVALID, E_ZERO_DIAG, E_DIAG_DOMAIN, E_NOMEM, E_CUDA. On any
+ * error *out receives a context that holds only the error detail (offending
+ * row via mcinv_error_detail); it must still be destroyed. */
+mcinv_status mcinv_create(mcinv_ctx **out, int device, mcinv_dtype dtype, int64_t n,
+                          const int64_t *row_ptr, const int32_t *col_idx, const void *values);
+
+/* Weighting matrix Q of Eq. (tr), same dtype and order as C.
+ * Needed for MCINV_TRACE. The estimator is w^dagger Q z (reading R2). */
+mcinv_status mcinv_set_trace_q(mcinv_ctx *ctx, const int64_t *row_ptr, const int32_t *col_idx,
+                               const void *values);
+
+/* Elements (rows[p], cols[p]) of C^-1 estimated by MCINV_PATTERN, in this
+ * order. Default (never called): the structural pattern of C in CSR order,
+ * diagonal included. */
+mcinv_status mcinv_set_pattern(mcinv_ctx *ctx, int64_t count, const int32_t *rows, const int32_t *cols);
+
+/* Number of pattern elements currently configured (for sizing results). */
+mcinv_status mcinv_pattern_size(const mcinv_ctx *ctx, int64_t *count);
+
+typedef struct {
+    uint64_t seed;          /* Philox key (noise phi(c,k,i) keyed by (seed, chain, sweep, row)) */
+    int64_t chain_begin;    /* global index of the first chain of this call (multiple of group_size) */
+    int64_t chains;         /* chains in this call (multiple of group_size, >= 1) */
+    int64_t burn_in;        /* N: sweeps discarded */
+    int64_t cycles;         /* M - N: sampling sweeps accumulated */
+    int64_t sweep_begin;    /* absolute index of the first sweep (resume keeps the noise stream) */
+    unsigned outputs;       /* OR of MCINV_DIAG | MCINV_PATTERN | MCINV_FULL | MCINV_TRACE */
+    int noise;              /* MCINV_NOISE_* */
+    int group_size;         /* chains per standard-error group: 1, 2, 4, 8, 16 or 32 */
+    int resume;             /* 0: z = w = 0 (Alg. 1 step 1), accumulators zeroed;
+                               1: continue from the state and accumulators in `workspace` */
+    int snapshot_sweeps;    /* MCINV_FULL: sweeps per X Y^dagger contraction chunk (0 = auto) */
+    void *workspace;        /* device memory of >= mcinv_workspace_size bytes, 256-B aligned, or
+                               NULL to let the library allocate (and own) it */
+    size_t workspace_bytes;
+    void *stream;           /* cudaStream_t; NULL = legacy default stream */
+} mcinv_run_args;
+
+/* Device workspace needed by mcinv_run with these arguments (state Z/W,
+ * per-group accumulators, contraction snapshots, moments). */
+mcinv_status mcinv_workspace_size(const mcinv_ctx *ctx, const mcinv_run_args *args, size_t *bytes);
+
+/* Run chains [chain_begin, chain_begin + chains) for burn_in + cycles sweeps
+ * (Alg. 1 with a fixed burn-in), asynchronously on args->stream.
+ * On return the per-output moment vectors (see mcinv_accumulators) are being
+ * produced on the stream. Errors detected on the device (divergence) are
+ * reported by mcinv_result. */
+mcinv_status mcinv_run(mcinv_ctx *ctx, const mcinv_run_args *args);
+
+/* Borrowed device pointer to the moment vector of the last run, for an
+ * all-reduce (SUM, float64) across GPUs that ran disjoint chain ranges:
+ *   for each output in the order DIAG, PATTERN, FULL, TRACE present:
+ *       S1[count*e], S2[count*e]   (e = 1 real, 2 complex: re and im parts)
+ *   then one double: number of diverged chains.
+ * S1 = sum over groups of the group sums, S2 = sum of their squares.
+ * Valid until the next run or destroy. */
+mcinv_status mcinv_accumulators(mcinv_ctx *ctx, double **dev_ptr, size_t *count);
+
+/* Estimate and standard error of one output from the (possibly all-reduced)
+ * moments: estimate = S1 / (total_chains * cycles) (Eq. 1/C); SE =
+ * sd(group means)/sqrt(G), G = total_chains / group_size (R15).
+ * estimate / std_error receive count*e doubles each (std_error may be NULL);
+ * capacity is in doubles. on_device != 0: both are device pointers, written
+ * asynchronously on the run's stream; otherwise host pointers and the call
+ * synchronizes. Returns E_DIVERGED if any chain diverged, E_BUFFER (required
+ * capacity via mcinv_error_detail's index) if capacity is too small. */
+mcinv_status mcinv_result(mcinv_ctx *ctx, unsigned output, int64_t total_chains,
+                          double *estimate, double *std_error, size_t capacity, int on_device);
+
+const char *mcinv_status_string(mcinv_status st);
+
+/* Last error of this context: index (row, required capacity, ...) and text. */
+mcinv_status mcinv_error_detail(const mcinv_ctx *ctx, int64_t *index, const char **msg);
+
+void mcinv_destroy(mcinv_ctx *ctx);
+
+/* Instrumentation. With timing enabled, every sweep-kernel (K1) and
+ * contraction-kernel (K3) launch is bracketed by CUDA events on the launch
+ * stream. mcinv_stats returns, since the previous mcinv_stats call: the
+ * number of kernels this library launched, and the summed device time (ms)
+ * and launch count of K1 and K3 (synchronizes on pending events). */
+mcinv_status mcinv_set_timing(mcinv_ctx *ctx, int enable);
+mcinv_status mcinv_stats(mcinv_ctx *ctx, int64_t *launches, double *sweep_ms, int64_t *sweep_launches,
+                         double *contract_ms, int64_t *contract_launches);
+
+/* ------------------------------------------------------------ test-only */
+
+/* Philox4x32-10 words on the device for `count` counters ctr4[4*count]
+ * (host), key = seed; out4[4*count] host. */
+mcinv_status mcinv_debug_philox(int device, uint64_t seed, int64_t count, const uint32_t *ctr4,
+                                uint32_t *out4);
+/* Box-Muller Gaussian of Philox(ctr, seed) for each counter (host arrays). */
+mcinv_status mcinv_debug_gaussian(int device, uint64_t seed, int64_t count, const uint32_t *ctr4,
+                                  double *out);
+/* Copy the state of chains [chain_begin, chain_begin+chains) (relative to the
+ * last run's chain_begin) to host arrays z, w of shape [chains][n] (x2 doubles
+ * for C128). Synchronizes. */
+mcinv_status mcinv_debug_get_state(mcinv_ctx *ctx, int64_t chain_begin, int64_t chains, void *z, void *w);
+/* Overwrite that state from host arrays (same layout); a following run with
+ * resume = 1 continues from it. The run's workspace must still be valid. */
+mcinv_status mcinv_debug_set_state(mcinv_ctx *ctx, int64_t chain_begin, int64_t chains, const void *z,
+                                   const void *w);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MCINV_H */

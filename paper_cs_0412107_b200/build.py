@@ -1,0 +1,53 @@
+"""Build libmcinv.so (the C-ABI library) in-tree with nvcc for sm_100a.
+
+The library is the product: kernels (sweep.cu, contract.cu, reduce.cu) and
+the C ABI / host preprocessing (mcinv_host.cu). ``--fmad=false`` so that
+only explicit fma() calls fuse (reading R10); cudart is linked
+statically so the library does not depend on the CUDA runtime torch ships.
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+CSRC = os.path.join(HERE, "csrc")
+SO = os.path.join(HERE, "libmcinv.so")
+SOURCES = ["mcinv_host.cu", "sweep.cu", "contract.cu", "reduce.cu"]
+HEADERS = ["mcinv_internal.cuh", "noise.cuh", "scalar.cuh"]
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+FLAGS = ["-O3", "-std=c++17", "-lineinfo", "--fmad=false", "-Xcompiler", "-fPIC,-O2",
+         "-Xptxas", "-v", "-cudart", "static", "-I", os.path.join(ROOT, "include")]
+
+
+def _stale() -> bool:
+    if not os.path.exists(SO):
+        return True
+    t = os.path.getmtime(SO)
+    deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS] + [os.path.join(ROOT, "include", "mcinv.h")]
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    if not force and not _stale():
+        return SO
+    tmp = SO + ".tmp"
+    cmd = [NVCC, *ARCH, *FLAGS, "-shared", "-o", tmp] + [os.path.join(CSRC, f) for f in SOURCES]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    log = os.path.join(HERE, "build.log")
+    with open(log, "w") as f:
+        f.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError(f"nvcc failed (see {log})")
+    if verbose:
+        sys.stderr.write(r.stderr)
+    os.replace(tmp, SO)
+    return SO
+
+
+if __name__ == "__main__":
+    print(build(force="--force" in sys.argv, verbose=True))

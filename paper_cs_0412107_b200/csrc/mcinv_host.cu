@@ -1,0 +1,771 @@
+// mcinv_host.cu -- the C ABI of include/mcinv.h: H1 host preprocessing,
+// workspace layout, and the launch sequence of the hot path.
+//
+// Everything numeric on the hot path runs in the kernels of sweep.cu,
+// contract.cu and reduce.cu. This file validates inputs, builds the device
+// form of C (row/column union lists, 1/c_ii, 1/sqrt(c_ii)), lays out the
+// workspace and enqueues kernels on the caller's stream.
+#include <algorithm>
+#include <complex>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/mcinv.h"
+#include "mcinv_internal.cuh"
+
+using mcinv::cd;
+using mcinv::ZW;
+
+namespace {
+
+struct DevBuf {
+    void *p = nullptr;
+    size_t bytes = 0;
+    ~DevBuf() { release(); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+};
+
+struct Entry {
+    int j;
+    std::complex<double> v;
+};
+
+struct Layout {
+    int ld = 0, G = 0, T = 0;
+    int e = 1;              // doubles per scalar
+    size_t zw = 0, slot_diag = 0, slot_pat = 0, slot_full = 0, slot_trace = 0, snap_x = 0, snap_y = 0, mom = 0;
+    size_t mom_count = 0;   // doubles in the moment vector
+    size_t mom_diag = 0, mom_pat = 0, mom_full = 0, mom_trace = 0;  // offsets (doubles) of S1 in moments
+    size_t total = 0;
+};
+
+}  // namespace
+
+struct mcinv_ctx {
+    int device = 0;
+    int dtype = MCINV_F64;
+    int64_t n = 0;
+    std::string err;
+    int64_t err_index = -1;
+    bool valid = false;
+
+    // host canonical C (rows sorted, duplicates summed), kept for the default pattern
+    std::vector<int64_t> h_rp;
+    std::vector<int> h_col;
+    // device C
+    DevBuf u_ptr, u_col, u_a, u_b, delta, sigma;
+    // pattern
+    bool pattern_custom = false;
+    int64_t pcount = 0;
+    DevBuf p_ptr, p_idx, p_other;
+    // Q
+    bool have_q = false;
+    DevBuf qr_ptr, qr_col, qr_val, qc_ptr, qc_row, qc_val;
+    // last run
+    bool have_run = false;
+    mcinv_run_args last{};
+    Layout lay;
+    DevBuf own_ws;
+    char *ws = nullptr;
+    cudaStream_t stream = nullptr;
+    DevBuf tmp;  // staging for host-side results
+    // instrumentation
+    bool timing = false;
+    int64_t launches = 0;
+    struct Timed {
+        cudaEvent_t a, b;
+        int kind;  // 0 sweep, 1 contract
+    };
+    std::vector<Timed> pending;
+    std::vector<cudaEvent_t> event_pool;
+    ~mcinv_ctx() {
+        for (auto &t : pending) {
+            cudaEventDestroy(t.a);
+            cudaEventDestroy(t.b);
+        }
+        for (auto e : event_pool) cudaEventDestroy(e);
+    }
+};
+
+namespace {
+
+mcinv_status fail(mcinv_ctx *c, mcinv_status st, const std::string &msg, int64_t idx = -1) {
+    if (c) {
+        c->err = msg;
+        c->err_index = idx;
+    }
+    return st;
+}
+
+#define CK(call)                                                                              \
+    do {                                                                                      \
+        cudaError_t e_ = (call);                                                              \
+        if (e_ != cudaSuccess)                                                                \
+            return fail(ctx, MCINV_E_CUDA, std::string(#call ": ") + cudaGetErrorString(e_)); \
+    } while (0)
+
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+template <typename T>
+mcinv_status upload(mcinv_ctx *ctx, DevBuf &b, const std::vector<T> &h) {
+    b.release();
+    const size_t bytes = std::max<size_t>(sizeof(T), h.size() * sizeof(T));
+    if (cudaMalloc(&b.p, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        b.p = nullptr;
+        return fail(ctx, MCINV_E_NOMEM, "cudaMalloc failed");
+    }
+    b.bytes = bytes;
+    if (!h.empty()) CK(cudaMemcpy(b.p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice));
+    return MCINV_OK;
+}
+
+#define TRY(x)                                  \
+    do {                                        \
+        mcinv_status s_ = (x);                  \
+        if (s_ != MCINV_OK) return s_;          \
+    } while (0)
+
+// Validate a CSR and return canonical rows: sorted by column, duplicates summed.
+mcinv_status read_csr(mcinv_ctx *ctx, int64_t n, const int64_t *rp, const int32_t *col, const double *val, bool cplx,
+                      std::vector<std::vector<Entry>> &rows) {
+    if (!rp || !col || !val) return fail(ctx, MCINV_E_INVALID, "null CSR pointer");
+    if (rp[0] != 0) return fail(ctx, MCINV_E_INVALID, "row_ptr[0] != 0");
+    for (int64_t i = 0; i < n; ++i)
+        if (rp[i + 1] < rp[i]) return fail(ctx, MCINV_E_INVALID, "row_ptr decreasing", i);
+    if (rp[n] >= (int64_t(1) << 31)) return fail(ctx, MCINV_E_INVALID, "nnz >= 2^31");
+    rows.assign(n, {});
+    for (int64_t i = 0; i < n; ++i) {
+        auto &r = rows[i];
+        r.reserve(rp[i + 1] - rp[i]);
+        for (int64_t e = rp[i]; e < rp[i + 1]; ++e) {
+            if (col[e] < 0 || col[e] >= n) return fail(ctx, MCINV_E_INVALID, "column out of range", i);
+            const double re = cplx ? val[2 * e] : val[e], im = cplx ? val[2 * e + 1] : 0.0;
+            if (!std::isfinite(re) || !std::isfinite(im)) return fail(ctx, MCINV_E_INVALID, "non-finite value", i);
+            r.push_back(Entry{col[e], std::complex<double>(re, im)});
+        }
+        std::stable_sort(r.begin(), r.end(), [](const Entry &a, const Entry &b) { return a.j < b.j; });
+        size_t o = 0;
+        for (size_t q = 0; q < r.size(); ++q) {
+            if (o > 0 && r[o - 1].j == r[q].j) r[o - 1].v += r[q].v;
+            else r[o++] = r[q];
+        }
+        r.resize(o);
+    }
+    return MCINV_OK;
+}
+
+template <typename S> S to_s(std::complex<double> v);
+template <> double to_s<double>(std::complex<double> v) { return v.real(); }
+template <> cd to_s<cd>(std::complex<double> v) { return cd{v.real(), v.imag()}; }
+
+// H1: C = L + D + U; union row/column lists; delta, sigma.
+template <typename S>
+mcinv_status build_matrix(mcinv_ctx *ctx, const std::vector<std::vector<Entry>> &rows) {
+    const int64_t n = ctx->n;
+    std::vector<std::complex<double>> diag(n);
+    std::vector<std::vector<Entry>> colv(n);  // colv[i]: (j, c_ji) for j != i
+    ctx->h_rp.assign(n + 1, 0);
+    ctx->h_col.clear();
+    for (int64_t i = 0; i < n; ++i) {
+        bool have = false;
+        for (const Entry &e : rows[i]) {
+            ctx->h_col.push_back(e.j);
+            if (e.j == i) {
+                diag[i] = e.v;
+                have = true;
+            } else {
+                colv[e.j].push_back(Entry{(int)i, e.v});  // rows ascend -> sorted
+            }
+        }
+        ctx->h_rp[i + 1] = (int64_t)ctx->h_col.size();
+        if (!have || diag[i] == std::complex<double>(0.0, 0.0))
+            return fail(ctx, MCINV_E_ZERO_DIAG, "zero or missing diagonal", i);
+        if (ctx->dtype == MCINV_F64 && !(diag[i].real() > 0.0))
+            return fail(ctx, MCINV_E_DIAG_DOMAIN, "real path needs c_ii > 0", i);
+    }
+    std::vector<int> u_ptr(n + 1, 0), u_col;
+    std::vector<S> u_a, u_b, dl(n), sg(n);
+    u_col.reserve(2 * ctx->h_col.size());
+    for (int64_t i = 0; i < n; ++i) {
+        const auto &r = rows[i];
+        const auto &c = colv[i];
+        size_t p = 0, q = 0;
+        while (p < r.size() || q < c.size()) {
+            if (p < r.size() && r[p].j == i) {  // skip the diagonal
+                ++p;
+                continue;
+            }
+            const int jr = p < r.size() ? r[p].j : INT32_MAX;
+            const int jc = q < c.size() ? c[q].j : INT32_MAX;
+            const int j = std::min(jr, jc);
+            std::complex<double> a(0.0, 0.0), b(0.0, 0.0);
+            if (jr == j) a = r[p++].v;
+            if (jc == j) b = std::conj(c[q++].v);
+            u_col.push_back(j);
+            u_a.push_back(to_s<S>(a));
+            u_b.push_back(to_s<S>(b));
+        }
+        u_ptr[i + 1] = (int)u_col.size();
+        // delta_i = 1/c_ii, sigma_i = 1/sqrt(c_ii), principal branch (reading R1)
+        if (ctx->dtype == MCINV_F64) {
+            const double d = diag[i].real();
+            dl[i] = to_s<S>(std::complex<double>(1.0 / d, 0.0));
+            sg[i] = to_s<S>(std::complex<double>(1.0 / std::sqrt(d), 0.0));
+        } else {
+            dl[i] = to_s<S>(1.0 / diag[i]);
+            sg[i] = to_s<S>(1.0 / std::sqrt(diag[i]));
+        }
+    }
+    TRY(upload(ctx, ctx->u_ptr, u_ptr));
+    TRY(upload(ctx, ctx->u_col, u_col));
+    TRY(upload(ctx, ctx->u_a, u_a));
+    TRY(upload(ctx, ctx->u_b, u_b));
+    TRY(upload(ctx, ctx->delta, dl));
+    TRY(upload(ctx, ctx->sigma, sg));
+    return MCINV_OK;
+}
+
+// Pattern lists keyed by r = max(i, j) (see DevPattern).
+mcinv_status build_pattern(mcinv_ctx *ctx, int64_t count, const int32_t *rows, const int32_t *cols) {
+    const int64_t n = ctx->n;
+    std::vector<int> cnt(n + 1, 0), idx(std::max<int64_t>(count, 1)), other(std::max<int64_t>(count, 1));
+    for (int64_t p = 0; p < count; ++p) {
+        if (rows[p] < 0 || rows[p] >= n || cols[p] < 0 || cols[p] >= n)
+            return fail(ctx, MCINV_E_INVALID, "pattern index out of range", p);
+        cnt[std::max(rows[p], cols[p]) + 1]++;
+    }
+    for (int64_t i = 0; i < n; ++i) cnt[i + 1] += cnt[i];
+    std::vector<int> ptr(cnt.begin(), cnt.end()), fillp(cnt.begin(), cnt.end() - 1);
+    for (int64_t p = 0; p < count; ++p) {
+        const int r = rows[p], c = cols[p];
+        const int at = fillp[std::max(r, c)]++;
+        idx[at] = (int)p;
+        // r >= c: z_r (current) conj(w_c); r < c: z_r (gathered) conj(w_c) at row c
+        other[at] = (r >= c) ? c : (int)((unsigned)r | 0x80000000u);
+    }
+    idx.resize(std::max<int64_t>(count, 1));
+    TRY(upload(ctx, ctx->p_ptr, ptr));
+    TRY(upload(ctx, ctx->p_idx, idx));
+    TRY(upload(ctx, ctx->p_other, other));
+    ctx->pcount = count;
+    return MCINV_OK;
+}
+
+mcinv_status default_pattern(mcinv_ctx *ctx) {
+    const int64_t n = ctx->n;
+    std::vector<int32_t> r(ctx->h_col.size()), c(ctx->h_col.begin(), ctx->h_col.end());
+    for (int64_t i = 0; i < n; ++i)
+        for (int64_t e = ctx->h_rp[i]; e < ctx->h_rp[i + 1]; ++e) r[e] = (int32_t)i;
+    return build_pattern(ctx, (int64_t)r.size(), r.data(), c.data());
+}
+
+template <typename S>
+mcinv_status build_q(mcinv_ctx *ctx, const std::vector<std::vector<Entry>> &rows) {
+    const int64_t n = ctx->n;
+    std::vector<int> rptr(n + 1, 0), rcol, cptr(n + 1, 0), crow;
+    std::vector<S> rval, cval;
+    std::vector<std::vector<Entry>> colpart(n);
+    for (int64_t i = 0; i < n; ++i) {
+        for (const Entry &e : rows[i]) {
+            if (e.j <= i) {
+                rcol.push_back(e.j);
+                rval.push_back(to_s<S>(e.v));
+            } else {
+                colpart[e.j].push_back(Entry{(int)i, e.v});
+            }
+        }
+        rptr[i + 1] = (int)rcol.size();
+    }
+    for (int64_t j = 0; j < n; ++j) {
+        for (const Entry &e : colpart[j]) {
+            crow.push_back(e.j);
+            cval.push_back(to_s<S>(e.v));
+        }
+        cptr[j + 1] = (int)crow.size();
+    }
+    TRY(upload(ctx, ctx->qr_ptr, rptr));
+    TRY(upload(ctx, ctx->qr_col, rcol));
+    TRY(upload(ctx, ctx->qr_val, rval));
+    TRY(upload(ctx, ctx->qc_ptr, cptr));
+    TRY(upload(ctx, ctx->qc_row, crow));
+    TRY(upload(ctx, ctx->qc_val, cval));
+    ctx->have_q = true;
+    return MCINV_OK;
+}
+
+cudaEvent_t get_event(mcinv_ctx *ctx) {
+    if (!ctx->event_pool.empty()) {
+        cudaEvent_t e = ctx->event_pool.back();
+        ctx->event_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+// Launch a kernel-enqueueing callable, bracketing it with events when timing.
+template <typename F>
+void timed(mcinv_ctx *ctx, int kind, cudaStream_t st, F &&f) {
+    ctx->launches++;
+    if (!ctx->timing) {
+        f();
+        return;
+    }
+    mcinv_ctx::Timed t{get_event(ctx), get_event(ctx), kind};
+    cudaEventRecord(t.a, st);
+    f();
+    cudaEventRecord(t.b, st);
+    ctx->pending.push_back(t);
+}
+
+bool pow2_le32(int g) { return g == 1 || g == 2 || g == 4 || g == 8 || g == 16 || g == 32; }
+
+mcinv_status check_args(const mcinv_ctx *ctx_c, const mcinv_run_args *a) {
+    mcinv_ctx *ctx = const_cast<mcinv_ctx *>(ctx_c);
+    if (!a) return fail(ctx, MCINV_E_INVALID, "null args");
+    if (a->chains < 1 || a->chain_begin < 0 || a->burn_in < 0 || a->cycles < 0 || a->sweep_begin < 0)
+        return fail(ctx, MCINV_E_INVALID, "negative or empty run dimensions");
+    if (!pow2_le32(a->group_size)) return fail(ctx, MCINV_E_INVALID, "group_size must be 1,2,4,8,16 or 32");
+    if (a->chains % a->group_size || a->chain_begin % a->group_size)
+        return fail(ctx, MCINV_E_INVALID, "chains and chain_begin must be multiples of group_size");
+    if (a->chain_begin + a->chains > (int64_t(1) << 32) ||
+        a->sweep_begin + a->burn_in + a->cycles > (int64_t(1) << 32))
+        return fail(ctx, MCINV_E_INVALID, "chain or sweep index exceeds the 32-bit noise counter");
+    if (a->outputs & ~15u) return fail(ctx, MCINV_E_INVALID, "unknown output bit");
+    if ((a->outputs & MCINV_TRACE) && !ctx->have_q) return fail(ctx, MCINV_E_STATE, "TRACE needs mcinv_set_trace_q");
+    if (a->noise < 0 || a->noise > 2) return fail(ctx, MCINV_E_INVALID, "noise mode");
+    if (a->chains > (int64_t(1) << 30)) return fail(ctx, MCINV_E_INVALID, "too many chains for one call");
+    return MCINV_OK;
+}
+
+Layout make_layout(const mcinv_ctx *ctx, const mcinv_run_args *a) {
+    Layout L;
+    const int64_t n = ctx->n;
+    const bool cplx = ctx->dtype == MCINV_C128;
+    L.e = cplx ? 2 : 1;
+    const size_t sz = 8 * L.e;
+    L.ld = (int)((a->chains + 31) / 32 * 32);
+    L.G = (int)(a->chains / a->group_size);
+    L.T = 0;
+    if (a->outputs & MCINV_FULL) {
+        int T = a->snapshot_sweeps;
+        if (T <= 0) {
+            // K = T * gs >= 256 per contraction, bounded by cycles
+            T = (int)std::max<int64_t>(1, 256 / a->group_size);
+            if (T > 64) T = 64;
+        }
+        if (a->cycles > 0 && T > a->cycles) T = (int)a->cycles;
+        L.T = std::max(T, 1);
+    }
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        const size_t o = off;
+        off = align256(off + bytes);
+        return o;
+    };
+    L.zw = take((size_t)n * L.ld * 2 * sz);
+    if (a->outputs & MCINV_DIAG) L.slot_diag = take((size_t)L.G * n * sz);
+    if (a->outputs & MCINV_PATTERN) L.slot_pat = take((size_t)L.G * std::max<int64_t>(ctx->pcount, 1) * sz);
+    if (a->outputs & MCINV_FULL) {
+        L.slot_full = take((size_t)L.G * n * n * sz);
+        L.snap_x = take((size_t)L.T * n * L.ld * sz);
+        L.snap_y = take((size_t)L.T * n * L.ld * sz);
+    }
+    if (a->outputs & MCINV_TRACE) L.slot_trace = take((size_t)L.G * sz);
+    size_t m = 0;
+    if (a->outputs & MCINV_DIAG) { L.mom_diag = m; m += 2 * (size_t)n * L.e; }
+    if (a->outputs & MCINV_PATTERN) { L.mom_pat = m; m += 2 * (size_t)ctx->pcount * L.e; }
+    if (a->outputs & MCINV_FULL) { L.mom_full = m; m += 2 * (size_t)n * n * L.e; }
+    if (a->outputs & MCINV_TRACE) { L.mom_trace = m; m += 2 * (size_t)L.e; }
+    L.mom_count = m + 1;
+    L.mom = take(L.mom_count * 8);
+    L.total = off;
+    return L;
+}
+
+template <typename S>
+mcinv_status run_typed(mcinv_ctx *ctx, const mcinv_run_args *a, const Layout &L, char *ws, cudaStream_t st) {
+    using namespace mcinv;
+    const int64_t n = ctx->n;
+    SweepParams<S> p{};
+    p.A = DevMatrix<S>{(int)n, (const int *)ctx->u_ptr.p, (const int *)ctx->u_col.p, (const S *)ctx->u_a.p,
+                       (const S *)ctx->u_b.p, (const S *)ctx->delta.p, (const S *)ctx->sigma.p};
+    p.P = DevPattern{(int)ctx->pcount, (const int *)ctx->p_ptr.p, (const int *)ctx->p_idx.p,
+                     (const int *)ctx->p_other.p};
+    if (ctx->have_q)
+        p.Q = DevQ<S>{(const int *)ctx->qr_ptr.p, (const int *)ctx->qr_col.p, (const S *)ctx->qr_val.p,
+                      (const int *)ctx->qc_ptr.p, (const int *)ctx->qc_row.p, (const S *)ctx->qc_val.p};
+    p.zw = reinterpret_cast<ZW<S> *>(ws + L.zw);
+    p.ld = L.ld;
+    p.chains = (int)a->chains;
+    p.chain0 = (uint32_t)a->chain_begin;
+    p.key0 = (uint32_t)a->seed;
+    p.key1 = (uint32_t)(a->seed >> 32);
+    p.noise = a->noise;
+    p.sweep_abs0 = (uint32_t)a->sweep_begin;
+    p.burn_in = (int)a->burn_in;
+    p.outputs = a->outputs & ~(unsigned)MCINV_FULL;
+    p.gs = a->group_size;
+    p.G = L.G;
+    p.slot_diag = (double *)(ws + L.slot_diag);
+    p.slot_pat = (double *)(ws + L.slot_pat);
+    p.slot_trace = (double *)(ws + L.slot_trace);
+    const int total = (int)(a->burn_in + a->cycles);
+
+    if (!a->resume) {
+        CK(cudaMemsetAsync(ws + L.zw, 0, (size_t)n * L.ld * sizeof(ZW<S>), st));
+        if (a->outputs & MCINV_DIAG) CK(cudaMemsetAsync(p.slot_diag, 0, (size_t)L.G * n * sizeof(S), st));
+        if (a->outputs & MCINV_PATTERN)
+            CK(cudaMemsetAsync(p.slot_pat, 0, (size_t)L.G * std::max<int64_t>(ctx->pcount, 1) * sizeof(S), st));
+        if (a->outputs & MCINV_FULL) CK(cudaMemsetAsync(ws + L.slot_full, 0, (size_t)L.G * n * n * sizeof(S), st));
+        if (a->outputs & MCINV_TRACE) CK(cudaMemsetAsync(p.slot_trace, 0, (size_t)L.G * sizeof(S), st));
+    }
+    if (!(a->outputs & MCINV_FULL)) {
+        p.s_begin = 0;
+        p.s_end = total;
+        if (total > 0) timed(ctx, 0, st, [&] { launch_sweep<S>(p, st); });
+    } else {
+        // burn-in (and nothing else) in one launch, then T-sweep chunks each
+        // followed by the X Y^dagger contraction of its snapshots
+        p.snap_x = (S *)(ws + L.snap_x);
+        p.snap_y = (S *)(ws + L.snap_y);
+        if (a->burn_in > 0) {
+            p.s_begin = 0;
+            p.s_end = (int)a->burn_in;
+            p.snap_s0 = 0;
+            SweepParams<S> q = p;
+            timed(ctx, 0, st, [&] { launch_sweep<S>(q, st); });
+        }
+        for (int s0 = (int)a->burn_in; s0 < total; s0 += L.T) {
+            const int s1 = std::min(total, s0 + L.T);
+            SweepParams<S> q = p;
+            q.s_begin = s0;
+            q.s_end = s1;
+            q.snap_s0 = s0;
+            q.outputs = a->outputs;
+            timed(ctx, 0, st, [&] { launch_sweep<S>(q, st); });
+            timed(ctx, 1, st, [&] {
+                launch_contract<S>((const S *)(ws + L.snap_x), (const S *)(ws + L.snap_y),
+                                   (double *)(ws + L.slot_full), (int)n, L.ld, (int)a->chains, a->group_size,
+                                   s1 - s0, st);
+            });
+        }
+    }
+    CK(cudaGetLastError());
+    // moments and divergence flag
+    double *mom = (double *)(ws + L.mom);
+    CK(cudaMemsetAsync(mom + L.mom_count - 1, 0, sizeof(double), st));
+    launch_check<S>(p.zw, (int)n, L.ld, (int)a->chains, mom + L.mom_count - 1, st);
+    ctx->launches++;
+    const int e = L.e;
+    ctx->launches += __builtin_popcount(a->outputs);  // one moments kernel per output
+    if (a->outputs & MCINV_DIAG)
+        launch_moments(p.slot_diag, L.G, n * e, mom + L.mom_diag, mom + L.mom_diag + n * e, st);
+    if (a->outputs & MCINV_PATTERN)
+        launch_moments(p.slot_pat, L.G, ctx->pcount * e, mom + L.mom_pat, mom + L.mom_pat + ctx->pcount * e, st);
+    if (a->outputs & MCINV_FULL)
+        launch_moments((const double *)(ws + L.slot_full), L.G, n * n * e, mom + L.mom_full,
+                       mom + L.mom_full + n * n * e, st);
+    if (a->outputs & MCINV_TRACE) launch_moments(p.slot_trace, L.G, e, mom + L.mom_trace, mom + L.mom_trace + e, st);
+    CK(cudaGetLastError());
+    return MCINV_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *mcinv_status_string(mcinv_status st) {
+    switch (st) {
+        case MCINV_OK: return "ok";
+        case MCINV_E_INVALID: return "invalid argument";
+        case MCINV_E_ZERO_DIAG: return "zero or missing diagonal element";
+        case MCINV_E_DIAG_DOMAIN: return "real path requires a positive diagonal";
+        case MCINV_E_DIVERGED: return "chains diverged (sp(T) or sp(S) >= 1)";
+        case MCINV_E_NOMEM: return "out of memory";
+        case MCINV_E_CUDA: return "CUDA error";
+        case MCINV_E_BUFFER: return "buffer too small";
+        case MCINV_E_STATE: return "call out of order";
+    }
+    return "unknown status";
+}
+
+mcinv_status mcinv_error_detail(const mcinv_ctx *ctx, int64_t *index, const char **msg) {
+    if (!ctx) return MCINV_E_INVALID;
+    if (index) *index = ctx->err_index;
+    if (msg) *msg = ctx->err.c_str();
+    return MCINV_OK;
+}
+
+mcinv_status mcinv_create(mcinv_ctx **out, int device, mcinv_dtype dtype, int64_t n, const int64_t *row_ptr,
+                          const int32_t *col_idx, const void *values) {
+    if (!out) return MCINV_E_INVALID;
+    *out = nullptr;
+    mcinv_ctx *ctx = new (std::nothrow) mcinv_ctx();
+    if (!ctx) return MCINV_E_NOMEM;
+    *out = ctx;
+    ctx->device = device;
+    ctx->dtype = dtype;
+    ctx->n = n;
+    if (dtype != MCINV_F64 && dtype != MCINV_C128) return fail(ctx, MCINV_E_INVALID, "dtype");
+    if (n < 1 || n >= (int64_t(1) << 31)) return fail(ctx, MCINV_E_INVALID, "n out of range");
+    CK(cudaSetDevice(device));
+    std::vector<std::vector<Entry>> rows;
+    TRY(read_csr(ctx, n, row_ptr, col_idx, (const double *)values, dtype == MCINV_C128, rows));
+    TRY(dtype == MCINV_C128 ? build_matrix<cd>(ctx, rows) : build_matrix<double>(ctx, rows));
+    TRY(default_pattern(ctx));
+    ctx->valid = true;
+    ctx->err.clear();
+    return MCINV_OK;
+}
+
+mcinv_status mcinv_set_trace_q(mcinv_ctx *ctx, const int64_t *row_ptr, const int32_t *col_idx, const void *values) {
+    if (!ctx || !ctx->valid) return MCINV_E_STATE;
+    CK(cudaSetDevice(ctx->device));
+    std::vector<std::vector<Entry>> rows;
+    TRY(read_csr(ctx, ctx->n, row_ptr, col_idx, (const double *)values, ctx->dtype == MCINV_C128, rows));
+    return ctx->dtype == MCINV_C128 ? build_q<cd>(ctx, rows) : build_q<double>(ctx, rows);
+}
+
+mcinv_status mcinv_set_pattern(mcinv_ctx *ctx, int64_t count, const int32_t *rows, const int32_t *cols) {
+    if (!ctx || !ctx->valid) return MCINV_E_STATE;
+    if (count < 0 || count >= (int64_t(1) << 31) || (count > 0 && (!rows || !cols)))
+        return fail(ctx, MCINV_E_INVALID, "pattern");
+    CK(cudaSetDevice(ctx->device));
+    ctx->pattern_custom = true;
+    return build_pattern(ctx, count, rows, cols);
+}
+
+mcinv_status mcinv_pattern_size(const mcinv_ctx *ctx, int64_t *count) {
+    if (!ctx || !ctx->valid || !count) return MCINV_E_STATE;
+    *count = ctx->pcount;
+    return MCINV_OK;
+}
+
+mcinv_status mcinv_workspace_size(const mcinv_ctx *ctx, const mcinv_run_args *args, size_t *bytes) {
+    if (!ctx || !ctx->valid || !bytes) return MCINV_E_STATE;
+    TRY(check_args(ctx, args));
+    *bytes = make_layout(ctx, args).total;
+    return MCINV_OK;
+}
+
+mcinv_status mcinv_run(mcinv_ctx *ctx, const mcinv_run_args *args) {
+    if (!ctx || !ctx->valid) return MCINV_E_STATE;
+    TRY(check_args(ctx, args));
+    CK(cudaSetDevice(ctx->device));
+    const Layout L = make_layout(ctx, args);
+    char *ws = (char *)args->workspace;
+    if (args->resume) {
+        if (!ctx->have_run || ctx->last.chains != args->chains || ctx->last.outputs != args->outputs ||
+            ctx->last.group_size != args->group_size || (ws && ws != ctx->ws))
+            return fail(ctx, MCINV_E_STATE, "resume needs the previous run's shape and workspace");
+        if (!ws) ws = ctx->ws;
+    }
+    if (ws) {
+        if (args->workspace_bytes < L.total || ((uintptr_t)ws & 255))
+            return fail(ctx, MCINV_E_BUFFER, "workspace too small or misaligned", (int64_t)L.total);
+    } else {
+        if (ctx->own_ws.bytes < L.total) {
+            ctx->own_ws.release();
+            if (cudaMalloc(&ctx->own_ws.p, L.total) != cudaSuccess) {
+                cudaGetLastError();
+                ctx->own_ws.p = nullptr;
+                return fail(ctx, MCINV_E_NOMEM, "workspace allocation", (int64_t)L.total);
+            }
+            ctx->own_ws.bytes = L.total;
+        }
+        ws = (char *)ctx->own_ws.p;
+    }
+    cudaStream_t st = (cudaStream_t)args->stream;
+    ctx->have_run = false;
+    TRY(ctx->dtype == MCINV_C128 ? run_typed<cd>(ctx, args, L, ws, st) : run_typed<double>(ctx, args, L, ws, st));
+    ctx->have_run = true;
+    ctx->last = *args;
+    ctx->lay = L;
+    ctx->ws = ws;
+    ctx->stream = st;
+    return MCINV_OK;
+}
+
+mcinv_status mcinv_accumulators(mcinv_ctx *ctx, double **dev_ptr, size_t *count) {
+    if (!ctx || !ctx->have_run || !dev_ptr || !count) return MCINV_E_STATE;
+    *dev_ptr = (double *)(ctx->ws + ctx->lay.mom);
+    *count = ctx->lay.mom_count;
+    return MCINV_OK;
+}
+
+mcinv_status mcinv_result(mcinv_ctx *ctx, unsigned output, int64_t total_chains, double *estimate,
+                          double *std_error, size_t capacity, int on_device) {
+    if (!ctx || !ctx->have_run) return MCINV_E_STATE;
+    const Layout &L = ctx->lay;
+    const mcinv_run_args &a = ctx->last;
+    if (!(a.outputs & output) || (output & (output - 1)) || !estimate)
+        return fail(ctx, MCINV_E_INVALID, "output not computed by the last run");
+    if (total_chains < a.chains || total_chains % a.group_size)
+        return fail(ctx, MCINV_E_INVALID, "total_chains");
+    CK(cudaSetDevice(ctx->device));
+    const int64_t n = ctx->n;
+    int64_t count = 0;
+    size_t off = 0;
+    switch (output) {
+        case MCINV_DIAG: count = n; off = L.mom_diag; break;
+        case MCINV_PATTERN: count = ctx->pcount; off = L.mom_pat; break;
+        case MCINV_FULL: count = n * n; off = L.mom_full; break;
+        case MCINV_TRACE: count = 1; off = L.mom_trace; break;
+        default: return fail(ctx, MCINV_E_INVALID, "output");
+    }
+    const int64_t comps = count * L.e;
+    if (capacity < (size_t)comps) return fail(ctx, MCINV_E_BUFFER, "result buffer too small", comps);
+    const double *mom = (const double *)(ctx->ws + L.mom);
+    const double cyc = (double)a.cycles;
+    const double G = (double)(total_chains / a.group_size);
+    cudaStream_t st = ctx->stream;
+    if (on_device) {
+        mcinv::launch_finalize(mom + off, mom + off + comps, comps, (double)total_chains * cyc, a.group_size * cyc, G,
+                               estimate, std_error, st);
+        ctx->launches++;
+        CK(cudaGetLastError());
+    } else {
+        const size_t need = 2 * comps * sizeof(double);
+        if (ctx->tmp.bytes < need) {
+            ctx->tmp.release();
+            if (cudaMalloc(&ctx->tmp.p, need) != cudaSuccess) {
+                cudaGetLastError();
+                ctx->tmp.p = nullptr;
+                return fail(ctx, MCINV_E_NOMEM, "result staging");
+            }
+            ctx->tmp.bytes = need;
+        }
+        double *de = (double *)ctx->tmp.p, *ds = de + comps;
+        mcinv::launch_finalize(mom + off, mom + off + comps, comps, (double)total_chains * cyc, a.group_size * cyc, G,
+                               de, ds, st);
+        ctx->launches++;
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(estimate, de, comps * sizeof(double), cudaMemcpyDeviceToHost, st));
+        if (std_error) CK(cudaMemcpyAsync(std_error, ds, comps * sizeof(double), cudaMemcpyDeviceToHost, st));
+    }
+    double bad = 0.0;
+    CK(cudaMemcpyAsync(&bad, mom + L.mom_count - 1, sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (bad > 0.0) return fail(ctx, MCINV_E_DIVERGED, "state non-finite or above 1e12", (int64_t)bad);
+    return MCINV_OK;
+}
+
+void mcinv_destroy(mcinv_ctx *ctx) {
+    if (!ctx) return;
+    if (ctx->valid || ctx->own_ws.p) cudaSetDevice(ctx->device);
+    delete ctx;
+}
+
+mcinv_status mcinv_set_timing(mcinv_ctx *ctx, int enable) {
+    if (!ctx || !ctx->valid) return MCINV_E_STATE;
+    ctx->timing = enable != 0;
+    return MCINV_OK;
+}
+
+mcinv_status mcinv_stats(mcinv_ctx *ctx, int64_t *launches, double *sweep_ms, int64_t *sweep_launches,
+                         double *contract_ms, int64_t *contract_launches) {
+    if (!ctx || !ctx->valid) return MCINV_E_STATE;
+    CK(cudaSetDevice(ctx->device));
+    double ms[2] = {0.0, 0.0};
+    int64_t cnt[2] = {0, 0};
+    for (auto &t : ctx->pending) {
+        CK(cudaEventSynchronize(t.b));
+        float f = 0.f;
+        CK(cudaEventElapsedTime(&f, t.a, t.b));
+        ms[t.kind] += f;
+        cnt[t.kind]++;
+        ctx->event_pool.push_back(t.a);
+        ctx->event_pool.push_back(t.b);
+    }
+    ctx->pending.clear();
+    if (launches) *launches = ctx->launches;
+    if (sweep_ms) *sweep_ms = ms[0];
+    if (sweep_launches) *sweep_launches = cnt[0];
+    if (contract_ms) *contract_ms = ms[1];
+    if (contract_launches) *contract_launches = cnt[1];
+    ctx->launches = 0;
+    return MCINV_OK;
+}
+
+mcinv_status mcinv_debug_philox(int device, uint64_t seed, int64_t count, const uint32_t *ctr4, uint32_t *out4) {
+    mcinv_ctx *ctx = nullptr;
+    if (count < 0 || (count > 0 && (!ctr4 || !out4))) return MCINV_E_INVALID;
+    if (count == 0) return MCINV_OK;
+    CK(cudaSetDevice(device));
+    uint32_t *dc = nullptr, *dout = nullptr;
+    CK(cudaMalloc(&dc, count * 16));
+    CK(cudaMalloc(&dout, count * 16));
+    CK(cudaMemcpy(dc, ctr4, count * 16, cudaMemcpyHostToDevice));
+    mcinv::launch_philox(dc, count, (uint32_t)seed, (uint32_t)(seed >> 32), dout, nullptr, 0);
+    CK(cudaGetLastError());
+    CK(cudaMemcpy(out4, dout, count * 16, cudaMemcpyDeviceToHost));
+    cudaFree(dc);
+    cudaFree(dout);
+    return MCINV_OK;
+}
+
+mcinv_status mcinv_debug_gaussian(int device, uint64_t seed, int64_t count, const uint32_t *ctr4, double *out) {
+    mcinv_ctx *ctx = nullptr;
+    if (count < 0 || (count > 0 && (!ctr4 || !out))) return MCINV_E_INVALID;
+    if (count == 0) return MCINV_OK;
+    CK(cudaSetDevice(device));
+    uint32_t *dc = nullptr;
+    double *dout = nullptr;
+    CK(cudaMalloc(&dc, count * 16));
+    CK(cudaMalloc(&dout, count * 8));
+    CK(cudaMemcpy(dc, ctr4, count * 16, cudaMemcpyHostToDevice));
+    mcinv::launch_philox(dc, count, (uint32_t)seed, (uint32_t)(seed >> 32), nullptr, dout, 0);
+    CK(cudaGetLastError());
+    CK(cudaMemcpy(out, dout, count * 8, cudaMemcpyDeviceToHost));
+    cudaFree(dc);
+    cudaFree(dout);
+    return MCINV_OK;
+}
+
+static mcinv_status state_io(mcinv_ctx *ctx, int64_t chain_begin, int64_t chains, void *z, void *w, bool get) {
+    if (!ctx || !ctx->have_run) return MCINV_E_STATE;
+    if (chain_begin < 0 || chains < 0 || chain_begin + chains > ctx->last.chains || !z || !w)
+        return fail(ctx, MCINV_E_INVALID, "state range");
+    CK(cudaSetDevice(ctx->device));
+    const int64_t n = ctx->n, ld = ctx->lay.ld, e = ctx->lay.e;
+    std::vector<double> buf((size_t)n * ld * 2 * e);
+    CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaMemcpy(buf.data(), ctx->ws + ctx->lay.zw, buf.size() * 8, cudaMemcpyDeviceToHost));
+    double *zd = (double *)z, *wd = (double *)w;
+    for (int64_t c = 0; c < chains; ++c)
+        for (int64_t i = 0; i < n; ++i)
+            for (int64_t q = 0; q < e; ++q) {
+                double *src = &buf[((i * ld + chain_begin + c) * 2) * e + q];
+                double *hz = &zd[(c * n + i) * e + q], *hw = &wd[(c * n + i) * e + q];
+                if (get) {
+                    *hz = src[0];
+                    *hw = src[e];
+                } else {
+                    src[0] = *hz;
+                    src[e] = *hw;
+                }
+            }
+    if (!get) CK(cudaMemcpy(ctx->ws + ctx->lay.zw, buf.data(), buf.size() * 8, cudaMemcpyHostToDevice));
+    return MCINV_OK;
+}
+
+mcinv_status mcinv_debug_get_state(mcinv_ctx *ctx, int64_t chain_begin, int64_t chains, void *z, void *w) {
+    return state_io(ctx, chain_begin, chains, z, w, true);
+}
+
+mcinv_status mcinv_debug_set_state(mcinv_ctx *ctx, int64_t chain_begin, int64_t chains, const void *z,
+                                   const void *w) {
+    return state_io(ctx, chain_begin, chains, const_cast<void *>(z), const_cast<void *>(w), false);
+}
+
+}  // extern "C"

@@ -1,0 +1,101 @@
+// mcinv_internal.cuh -- types shared by the host library (mcinv_host.cu) and
+// the device kernels (sweep.cu, contract.cu, reduce.cu). Product code only;
+// nothing here is shared with oracle/.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace mcinv {
+
+// Complex double, interleaved (re, im) as in the ABI.
+struct __align__(16) cd {
+    double re, im;
+};
+
+// One (row, chain) state element: z_i and w_i of Eq. (4)/(5) side by side,
+// so that one coalesced load serves both updates when row i and column i of
+// C share their pattern (every BASELINE config).
+template <typename S> struct __align__(2 * sizeof(S)) ZW {
+    S z, w;
+};
+
+// Device copy of C (built by mcinv_create):
+//  u_ptr/u_col: per row i the sorted UNION of {j : c_ij != 0} and
+//               {j : c_ji != 0}, j != i (structural, explicit zeros kept);
+//  u_a[e] = c_ij        (0 if absent)  -> Eq. (4) term
+//  u_b[e] = conj(c_ji)  (0 if absent)  -> Eq. (5) term
+//  delta = 1/c_ii, sigma = 1/sqrt(c_ii) (principal branch).
+template <typename S> struct DevMatrix {
+    int n;
+    const int *u_ptr;
+    const int *u_col;
+    const S *u_a;
+    const S *u_b;
+    const S *delta;
+    const S *sigma;
+};
+
+// Pattern lists, by the row r = max(i, j) at which both z_i and w_j are
+// final within a sweep: p_other encodes the partner index and, in bit 31,
+// which side is the current row (0: z_r conj(w_other); 1: z_other conj(w_r)).
+struct DevPattern {
+    int count;
+    const int *p_ptr;
+    const int *p_idx;
+    const int *p_other;
+};
+
+// Q lists of the trace w^dagger Q z split by r = max(i, j):
+//  row part  qr: entries (j, Q_rj), j <= r   -> conj(w_r) * sum Q_rj z_j
+//  col part  qc: entries (i, Q_ir), i <  r   -> z_r * sum Q_ir conj(w_i)
+template <typename S> struct DevQ {
+    const int *qr_ptr;
+    const int *qr_col;
+    const S *qr_val;
+    const int *qc_ptr;
+    const int *qc_row;
+    const S *qc_val;
+};
+
+enum : unsigned { OUT_DIAG = 1u, OUT_PATTERN = 2u, OUT_FULL = 4u, OUT_TRACE = 8u };
+
+template <typename S> struct SweepParams {
+    DevMatrix<S> A;
+    DevPattern P;
+    DevQ<S> Q;
+    ZW<S> *zw;          // [n][ld]
+    int ld;             // chains padded to a multiple of 32
+    int chains;         // active chains
+    uint32_t chain0;    // global index of local chain 0
+    uint32_t key0, key1;
+    int noise;
+    uint32_t sweep_abs0;  // absolute sweep index of local sweep 0
+    int s_begin, s_end;   // local sweep range of this launch
+    int burn_in;
+    unsigned outputs;
+    int gs;               // group size
+    int G;                // groups in this run
+    double *slot_diag;    // [G][n] * e
+    double *slot_pat;     // [G][pcount] * e
+    double *slot_trace;   // [G] * e
+    S *snap_x, *snap_y;   // [T][n][ld]
+    int snap_s0;          // local sweep stored at snapshot slot 0
+};
+
+template <typename S>
+void launch_sweep(const SweepParams<S> &p, cudaStream_t st);
+
+// A_g[i][j] += sum_{t < T, c in group g} X[t][i][c] conj(Y[t][j][c]).
+template <typename S>
+void launch_contract(const S *x, const S *y, double *acc, int n, int ld, int chains, int gs, int T,
+                     cudaStream_t st);
+
+void launch_moments(const double *slot, int G, int64_t comps, double *s1, double *s2, cudaStream_t st);
+void launch_finalize(const double *s1, const double *s2, int64_t comps, double m_cycles, double gs_cycles,
+                     double G, double *est, double *se, cudaStream_t st);
+template <typename S>
+void launch_check(const ZW<S> *zw, int n, int ld, int chains, double *flag, cudaStream_t st);
+void launch_philox(const uint32_t *ctr, int64_t count, uint32_t k0, uint32_t k1, uint32_t *out,
+                   double *gauss, cudaStream_t st);
+
+}  // namespace mcinv

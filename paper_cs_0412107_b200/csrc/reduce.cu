@@ -1,0 +1,103 @@
+// reduce.cu -- K4: group moments, finalize (estimate + standard error),
+// divergence check, and the test-only Philox/Gaussian dump kernels.
+//
+// Estimate (Eq. 1/C):  est = S1 / (m (M-N)).
+// Standard error (reading R15, replacing the Geyer error of
+// P:354-360): group means mu_g = S_g / (gs (M-N)); SE = sd(mu_g) / sqrt(G).
+#include "mcinv_internal.cuh"
+#include "noise.cuh"
+#include "scalar.cuh"
+
+namespace mcinv {
+
+// slot layout [G][comps]; s1[c] = sum_g slot, s2[c] = sum_g slot^2.
+__global__ void moments_kernel(const double *__restrict__ slot, int G, int64_t comps, double *__restrict__ s1,
+                               double *__restrict__ s2) {
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < comps;
+         c += (int64_t)gridDim.x * blockDim.x) {
+        double a = 0.0, b = 0.0;
+        for (int g = 0; g < G; ++g) {
+            const double v = slot[(int64_t)g * comps + c];
+            a += v;
+            b = fma(v, v, b);
+        }
+        s1[c] = a;
+        s2[c] = b;
+    }
+}
+
+__global__ void finalize_kernel(const double *__restrict__ s1, const double *__restrict__ s2, int64_t comps,
+                                double m_cycles, double gs_cycles, double G, double *__restrict__ est,
+                                double *__restrict__ se) {
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < comps;
+         c += (int64_t)gridDim.x * blockDim.x) {
+        est[c] = s1[c] / m_cycles;
+        if (se) {
+            // sum of squared group means minus G * (mean of group means)^2
+            const double mean = s1[c] / (G * gs_cycles);
+            const double sq = s2[c] / (gs_cycles * gs_cycles);
+            const double var = G > 1.0 ? (sq - G * mean * mean) / (G - 1.0) : NAN;
+            se[c] = var > 0.0 ? sqrt(var / G) : (var == var ? 0.0 : NAN);
+        }
+    }
+}
+
+// Count state values that are non-finite or exceed 1e12 in magnitude
+// (SPEC S:234 divergence rule; sp(T) >= 1 or sp(S) >= 1).
+template <typename S>
+__global__ void check_kernel(const ZW<S> *__restrict__ zw, int n, int ld, int chains, double *flag) {
+    int bad = 0;
+    const int64_t total = (int64_t)n * ld;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        if ((int)(e % ld) >= chains) continue;
+        const ZW<S> v = zw[e];
+        bad += bad_s(v.z) || bad_s(v.w);
+    }
+    bad = __reduce_add_sync(0xffffffffu, bad);
+    if ((threadIdx.x & 31) == 0 && bad) atomicAdd(flag, (double)bad);
+}
+
+__global__ void philox_kernel(const uint32_t *__restrict__ ctr, int64_t count, uint32_t k0, uint32_t k1,
+                              uint32_t *__restrict__ out, double *__restrict__ gauss) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < count;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const PhiloxOut r = philox4x32_10(ctr[4 * t], ctr[4 * t + 1], ctr[4 * t + 2], ctr[4 * t + 3], k0, k1);
+        if (out) {
+            out[4 * t] = r.x;
+            out[4 * t + 1] = r.y;
+            out[4 * t + 2] = r.z;
+            out[4 * t + 3] = r.w;
+        }
+        if (gauss) gauss[t] = box_muller(r);
+    }
+}
+
+static int grid_for(int64_t work, int threads) {
+    int64_t b = (work + threads - 1) / threads;
+    if (b > 148 * 16) b = 148 * 16;
+    return b < 1 ? 1 : (int)b;
+}
+
+void launch_moments(const double *slot, int G, int64_t comps, double *s1, double *s2, cudaStream_t st) {
+    moments_kernel<<<grid_for(comps, 256), 256, 0, st>>>(slot, G, comps, s1, s2);
+}
+
+void launch_finalize(const double *s1, const double *s2, int64_t comps, double m_cycles, double gs_cycles, double G,
+                     double *est, double *se, cudaStream_t st) {
+    finalize_kernel<<<grid_for(comps, 256), 256, 0, st>>>(s1, s2, comps, m_cycles, gs_cycles, G, est, se);
+}
+
+template <typename S>
+void launch_check(const ZW<S> *zw, int n, int ld, int chains, double *flag, cudaStream_t st) {
+    check_kernel<S><<<grid_for((int64_t)n * ld, 256), 256, 0, st>>>(zw, n, ld, chains, flag);
+}
+template void launch_check<double>(const ZW<double> *, int, int, int, double *, cudaStream_t);
+template void launch_check<cd>(const ZW<cd> *, int, int, int, double *, cudaStream_t);
+
+void launch_philox(const uint32_t *ctr, int64_t count, uint32_t k0, uint32_t k1, uint32_t *out, double *gauss,
+                   cudaStream_t st) {
+    philox_kernel<<<grid_for(count, 256), 256, 0, st>>>(ctr, count, k0, k1, out, gauss);
+}
+
+}  // namespace mcinv

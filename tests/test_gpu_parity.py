@@ -1,0 +1,311 @@
+"""GPU (CUDA path through the C ABI) vs oracle, same seeds -- the parity gate.
+
+Levels (BASELINE.json north_star):
+  1. Philox words bit-exact; Gaussian within 1e-15 relative.
+  2. post-sweep z, w within 1e-12 normwise relative error per chain.
+  3. estimates within 1e-10 relative Frobenius and normwise max error.
+Sizes: every BASELINE config at a reduced size that spans several warps /
+groups and a ragged tail, plus full-size runs compared on sampled chains
+(state after all sweeps) and on exact properties (deterministic solves,
+pure-gauge closed form).
+"""
+import numpy as np
+import pytest
+
+import workloads as W
+from tests import _stats
+
+pytestmark = pytest.mark.gpu
+
+TOL_STATE = 1e-12
+TOL_EST = 1e-10
+
+
+@pytest.fixture(scope="module")
+def mc():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_cs_0412107_b200 as M
+    M.load()
+    return M
+
+
+def normwise(a, b):
+    a = np.asarray(a)
+    b = np.asarray(b)
+    den = np.max(np.abs(b))
+    return np.max(np.abs(a - b)) / (den if den > 0 else 1.0)
+
+
+def frob(a, b):
+    return np.linalg.norm(np.ravel(a - b)) / max(np.linalg.norm(np.ravel(b)), 1e-300)
+
+
+def states_match(zg, wg, zo, wo, tol=TOL_STATE):
+    for c in range(zo.shape[0]):
+        assert normwise(zg[c], zo[c]) < tol, f"z chain {c}: {normwise(zg[c], zo[c])}"
+        assert normwise(wg[c], wo[c]) < tol, f"w chain {c}: {normwise(wg[c], wo[c])}"
+
+
+def est_match(eg, eo, tol=TOL_EST, what=""):
+    assert normwise(eg, eo) < tol, f"{what} normwise {normwise(eg, eo)}"
+    assert frob(eg, eo) < tol, f"{what} frobenius {frob(eg, eo)}"
+
+
+def compare_run(mc, orc, c, q=None, pattern=None, seed=1, chains=64, burn_in=5, cycles=10, outputs=("diag",),
+                group_size=32, chain_begin=0, snapshot_sweeps=0):
+    inv = mc.Inverter(c, q=q, pattern=pattern)
+    inv.run(seed, chains, burn_in, cycles, outputs, chain_begin=chain_begin, group_size=group_size,
+            snapshot_sweeps=snapshot_sweeps)
+    res = {o: inv.result(o) for o in outputs}
+    zg, wg = inv.get_state()
+    om = orc.Matrix(c, q=q, pattern=pattern if pattern is not None else
+                    (np.repeat(np.arange(c.n), np.diff(c.row_ptr)).astype(np.int32), c.col))
+    r = om.run(seed, chains, burn_in, cycles, outputs, chain_begin=chain_begin)
+    states_match(zg, wg, r["z"], r["w"])
+    for o in outputs:
+        eo, so = orc.estimate(r[o], cycles, group_size=group_size, chain_begin=chain_begin)
+        eg, sg = res[o]
+        est_match(eg, eo, what=o)
+        if chains // group_size >= 2:
+            # SE via sum of squares (GPU) vs two-pass (oracle): cancellation-limited
+            assert normwise(sg, so) < 1e-6, f"{o} SE {normwise(sg, so)}"
+    inv.close()
+    return res
+
+
+# ------------------------------------------------------------- level 1
+
+def test_philox_bit_exact(mc, orc):
+    rng = np.random.default_rng(0)
+    ctr = rng.integers(0, 2**32, size=(2000, 4), dtype=np.uint64).astype(np.uint32)
+    ctr[:10] = [[0, 0, 0, 0]] * 10
+    ctr[10] = [0xFFFFFFFF] * 4
+    for seed in (0, 0x5EED0002, 2**64 - 1, 0x123456789ABCDEF):
+        g = mc.philox(ctr, seed)
+        for k in range(0, 2000, 7):
+            assert list(g[k]) == list(orc.philox(ctr[k], [seed & 0xFFFFFFFF, seed >> 32])), (seed, k)
+
+
+def test_gaussian_matches_oracle(mc, orc):
+    rng = np.random.default_rng(1)
+    ctr = np.stack([rng.integers(0, 20000, 3000), rng.integers(0, 2200, 3000), rng.integers(0, 1024, 3000),
+                    np.zeros(3000, int)], 1).astype(np.uint32)
+    seed = 0x5EED0002
+    g = mc.gaussian(ctr, seed)
+    o = np.array([orc.gaussian(seed, int(a), int(b), int(c)) for a, b, c, _ in ctr])
+    assert np.max(np.abs(g - o) / np.maximum(np.abs(o), 1e-3)) < 1e-15 * 16
+
+
+# ------------------------------------------------------------- level 2/3, reduced sizes
+
+def test_config1_full_parity(mc, orc):
+    """Config 1 exactly as BASELINE.json states it: n=64 dense real, 64 chains,
+    100 burn-in + 1000 cycles, full C^-1 (group_size 1 -> G = 64)."""
+    c, _, run = W.config(1)
+    res = compare_run(mc, orc, c, seed=run.seed, chains=run.chains, burn_in=run.burn_in, cycles=run.cycles,
+                      outputs=("full",), group_size=run.group_size)
+    est, se = res["full"]
+    _stats.check(est, np.linalg.inv(c.to_dense()), se, G=64, what="config1 full vs LU")
+
+
+def test_config2_reduced_parity(mc, orc):
+    """Pedigree matrix (config 2 recipe) at n=3000, 72 chains (ragged last
+    warp), diag + pattern with groups of 8."""
+    c = W.pedigree(3000, seed=1002)
+    compare_run(mc, orc, c, seed=0x5EED0002, chains=72, burn_in=4, cycles=6, outputs=("diag", "pattern"),
+                group_size=8)
+
+
+def test_config3_reduced_parity(mc, orc):
+    """Complex lattice (config 3 recipe) at L=8, full output through the DMMA
+    contraction, several snapshot chunks (T=4) and a ragged chunk."""
+    c = W.lattice(8, 2, 0.2, seed=1003)
+    compare_run(mc, orc, c, seed=0x5EED0003, chains=96, burn_in=3, cycles=10, outputs=("full", "diag"),
+                group_size=16, snapshot_sweeps=4)
+
+
+def test_config3_real_full_gemm_tiles(mc, orc):
+    """Real full output with n=100 (ragged 64x64 tiles) and group size 4."""
+    c = W.random_dense(100, seed=9, ratio=0.5, density=0.2)
+    compare_run(mc, orc, c, seed=3, chains=32, burn_in=2, cycles=7, outputs=("full",), group_size=4,
+                snapshot_sweeps=3)
+
+
+def test_config5_reduced_parity(mc, orc):
+    """4-D complex lattice (config 5 recipe) at 4^4 with Q (4 nnz/row):
+    diag + trace (w^dagger Q z, reading R2)."""
+    c = W.lattice(4, 4, 0.1, seed=1005)
+    q = W.random_q(c.n, 2005, 4)
+    compare_run(mc, orc, c, q=q, seed=0x5EED0005, chains=64, burn_in=3, cycles=8, outputs=("diag", "trace"),
+                group_size=32)
+
+
+def test_all_outputs_complex_nonhermitian(mc, orc):
+    c = W.random_dense(40, seed=12, complex_=True, ratio=0.6, density=0.3, diag_phase=np.pi)
+    q = W.random_q(40, 13, 3)
+    rows = np.array([0, 5, 39, 12, 12, 7], np.int32)
+    cols = np.array([0, 30, 2, 12, 13, 7], np.int32)
+    compare_run(mc, orc, c, q=q, pattern=(rows, cols), seed=77, chains=40, burn_in=2, cycles=5,
+                outputs=("diag", "pattern", "full", "trace"), group_size=8, snapshot_sweeps=2)
+
+
+def test_nonsymmetric_structure(mc, orc):
+    """Row i and column i with different patterns (union lists with zeros)."""
+    a = np.triu(W.random_dense(30, seed=14, ratio=0.5).to_dense())  # upper triangle only
+    a[np.arange(1, 30), np.arange(29)] = -0.1                         # plus a sub-diagonal
+    c = W.CSR.from_dense(a)
+    compare_run(mc, orc, c, seed=5, chains=32, burn_in=3, cycles=4, outputs=("diag", "pattern"), group_size=2)
+
+
+def test_zero_noise_gauss_seidel(mc, orc):
+    """noise = zero from a non-zero start reproduces the oracle's GS iterates."""
+    c = W.random_dense(50, seed=15, complex_=True, ratio=0.7, density=0.2)
+    inv = mc.Inverter(c)
+    inv.run(1, 32, 0, 0, ("diag",), group_size=32, noise="zero")
+    rng = np.random.default_rng(2)
+    z0 = rng.standard_normal((32, 50)) + 1j * rng.standard_normal((32, 50))
+    w0 = rng.standard_normal((32, 50)) + 1j * rng.standard_normal((32, 50))
+    inv.set_state(z0, w0)
+    inv.run(1, 32, 5, 0, ("diag",), group_size=32, noise="zero", resume=True)
+    zg, wg = inv.get_state()
+    r = orc.Matrix(c).run(1, 32, 5, 0, noise=orc.NOISE_ZERO, z_init=z0, w_init=w0)
+    states_match(zg, wg, r["z"], r["w"])
+
+
+def test_edge_cases(mc, orc):
+    # n = 1
+    compare_run(mc, orc, W.diagonal(np.array([2.5])), seed=1, chains=32, burn_in=1, cycles=3,
+                outputs=("diag", "full"), group_size=4)
+    # diagonal complex with the branch cut
+    compare_run(mc, orc, W.diagonal(np.array([-2.0 + 0j, 1j, 3.0, -1 - 1e-3j])), seed=2, chains=33 * 1,
+                burn_in=0, cycles=4, outputs=("diag",), group_size=1)
+    # empty pattern list
+    c = W.random_dense(8, seed=3)
+    inv = mc.Inverter(c, pattern=(np.zeros(0, np.int32), np.zeros(0, np.int32)))
+    inv.run(1, 32, 1, 2, ("pattern", "diag"))
+    e, s = inv.result("pattern")
+    assert e.size == 0
+    inv.close()
+
+
+def test_sharding_invariance_and_resume(mc):
+    """Chains keyed by global index: two shards summed == one run (moments),
+    and a run split in two sweeps ranges == one run (bitwise state)."""
+    c = W.pedigree(2000, seed=7)
+    a = mc.Inverter(c)
+    a.run(9, 128, 3, 5, ("diag", "pattern"), group_size=32)
+    full = a.accumulators().cpu().numpy().copy()
+    z_all, w_all = a.get_state()
+    b = mc.Inverter(c)
+    parts = []
+    for cb in (0, 64):
+        b.run(9, 64, 3, 5, ("diag", "pattern"), chain_begin=cb, group_size=32)
+        parts.append(b.accumulators().cpu().numpy().copy())
+        zb, wb = b.get_state()
+        assert np.array_equal(zb, z_all[cb:cb + 64]) and np.array_equal(wb, w_all[cb:cb + 64])
+    np.testing.assert_allclose(parts[0] + parts[1], full, rtol=1e-12, atol=1e-300)
+    # resume: 8 sweeps == 3 + 5
+    b.run(9, 128, 3, 0, ("diag",), group_size=32)
+    b.run(9, 128, 0, 5, ("diag",), group_size=32, sweep_begin=3, resume=True)
+    zr, wr = b.get_state()
+    a.run(9, 128, 8, 0, ("diag",), group_size=32)
+    z8, w8 = a.get_state()
+    assert np.array_equal(zr, z8) and np.array_equal(wr, w8)
+
+
+def test_errors(mc):
+    M = mc
+    with pytest.raises(M.MCInvError) as e:
+        M.Inverter(W.CSR.from_dense(np.array([[1.0, 1.0], [1.0, 0.0]]), keep_zeros_on_diag=False))
+    assert e.value.code == 2 and e.value.index == 1
+    with pytest.raises(M.MCInvError) as e:
+        M.Inverter(W.CSR.from_dense(np.array([[1.0, 0.1], [0.1, -2.0]])))
+    assert e.value.code == 3
+    inv = M.Inverter(W.CSR.from_dense(np.array([[1.0, 3.0], [3.0, 1.0]])))  # sp(T) = 9
+    inv.run(1, 32, 200, 1, ("diag",))
+    with pytest.raises(M.MCInvError) as e:
+        inv.result("diag")
+    assert e.value.code == 4
+    with pytest.raises(M.MCInvError) as e:
+        inv.run(1, 30, 1, 1, ("diag",), group_size=32)  # chains not a multiple of group_size
+    assert e.value.code == 1
+    with pytest.raises(M.MCInvError) as e:
+        inv.run(1, 32, 1, 1, ("trace",))  # no Q
+    assert e.value.code == 8
+
+
+# ------------------------------------------------------------- full sizes (bench launch configuration)
+
+def _exact_columns(c, cols, tol=1e-14):
+    """X = C^-1[:, cols] by Jacobi iteration X <- D^-1 (E - (C - D) X); the
+    config-2/4 recipe is strictly row diagonally dominant (factor 1.1), so
+    ||D^-1 (C - D)||_inf = 1/1.1 and the iteration converges to tol."""
+    A = c.to_scipy()
+    d = A.diagonal()
+    off = A - __import__("scipy.sparse", fromlist=["diags"]).diags(d)
+    E = np.zeros((c.n, len(cols)), dtype=c.val.dtype)
+    E[cols, np.arange(len(cols))] = 1
+    X = E / d[:, None]
+    for _ in range(2000):
+        Xn = (E - off @ X) / d[:, None]
+        if np.max(np.abs(Xn - X)) < tol * np.max(np.abs(Xn)):
+            return Xn
+        X = Xn
+    raise RuntimeError("Jacobi did not converge")
+
+
+def test_config2_full_size(mc, orc):
+    """Config 2 exactly as bench.py times it (n=20000, 1024 chains, 200+2000
+    sweeps, diag + pattern): sampled chains' final states vs the oracle, and
+    diag / pattern estimates of sampled rows vs exact sparse solves."""
+    c, _, run = W.config(2)
+    inv = mc.Inverter(c)
+    inv.run(run.seed, run.chains, run.burn_in, run.cycles, run.outputs, group_size=run.group_size)
+    ed, sd = inv.result("diag")
+    ep, sp_ = inv.result("pattern")
+    picks = [0, 517, 1023]
+    om = orc.Matrix(c)
+    for ch in picks:
+        r = om.run(run.seed, 1, run.burn_in + run.cycles, 0, chain_begin=ch)
+        zg, wg = inv.get_state(ch, 1)
+        states_match(zg, wg, r["z"], r["w"])
+    rng = np.random.default_rng(5)
+    rows = np.sort(rng.choice(c.n, 60, replace=False))
+    X = _exact_columns(c, rows)                    # X[:, k] = C^-1[:, rows[k]]
+    exact_d = X[rows, np.arange(len(rows))]
+    _stats.check(ed[rows], exact_d, sd[rows], G=32, what="config2 diag")
+    # pattern elements (i, j) with j in the sampled columns
+    pr = np.repeat(np.arange(c.n), np.diff(c.row_ptr))
+    sel = np.isin(c.col, rows)
+    pos = {r: k for k, r in enumerate(rows)}
+    exact_p = np.array([X[i, pos[j]] for i, j in zip(pr[sel], c.col[sel])])
+    _stats.check(ep[sel], exact_p, sp_[sel], G=32, what="config2 pattern")
+
+
+@pytest.mark.slow
+def test_config5_full_size_pure_gauge(mc, orc):
+    """Config 5 launch configuration (16^4 complex, 16384 chains, diag +
+    trace) on the pure-gauge variant: diag(C^-1) = 1.055485534357617 at every
+    site (finding F4); sampled chain states vs the oracle (reduced sweeps)."""
+    c, q, run = W.config(5, pure_gauge=True)
+    inv = mc.Inverter(c, q=q)
+    inv.run(run.seed, run.chains, run.burn_in, run.cycles, run.outputs, group_size=run.group_size)
+    ed, sd = inv.result("diag")
+    _stats.check(ed, np.full(c.n, 1.055485534357617 + 0j), sd, G=run.chains // 32, what="config5 diag")
+    inv.run(run.seed, 64, 3, 0, ("diag",), chain_begin=16384 - 64)
+    zg, wg = inv.get_state(60, 4)
+    r = orc.Matrix(c).run(run.seed, 4, 3, 0, chain_begin=16384 - 4)
+    states_match(zg, wg, r["z"], r["w"])
+
+
+def test_config4_sampled_sweeps(mc, orc):
+    """Config 4 matrix (n = 1e6 pedigree): 2 sweeps of 64 chains, sampled
+    chain states vs the oracle."""
+    c, _, run = W.config(4)
+    inv = mc.Inverter(c)
+    inv.run(run.seed, 64, 2, 0, ("diag",), chain_begin=8192 - 64)
+    zg, wg = inv.get_state(62, 2)
+    r = orc.Matrix(c).run(run.seed, 2, 2, 0, chain_begin=8192 - 2)
+    states_match(zg, wg, r["z"], r["w"])
