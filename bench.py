@@ -250,6 +250,7 @@ def ours_arm(args):
     ms = t0.elapsed_time(t1) / args.steps
     st = inv.stats()
     inv.set_timing(False)
+    kinfo = inv.kernel_info()
     if world > 1:
         x = torch.tensor([ms], device="cuda", dtype=torch.float64)
         dist.all_reduce(x, op=dist.ReduceOp.MAX)
@@ -318,7 +319,7 @@ def ours_arm(args):
                            "total_chains": total_chains, "burn_in": run.burn_in, "cycles": run.cycles,
                            "outputs": list(outputs), "group_size": run.group_size,
                            "l2": f"inputs larger than L2 (state {c.n * chains * (32 if np.iscomplexobj(c.val) else 16) / 1e6:.0f} MB > 126 MB)",
-                           "matrix_sha256": c.sha256()[:16]},
+                           "matrix_sha256": c.sha256()[:16], "kernel": kinfo},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": st["launches"], "clocks": clk}
         print(json.dumps(line), flush=True)

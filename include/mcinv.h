@@ -151,6 +151,12 @@ mcinv_status mcinv_set_timing(mcinv_ctx *ctx, int enable);
 mcinv_status mcinv_stats(mcinv_ctx *ctx, int64_t *launches, double *sweep_ms, int64_t *sweep_launches,
                          double *contract_ms, int64_t *contract_launches);
 
+/* Which sweep kernel the last mcinv_run used: version 2 = step-scheduled
+ * kernel (sweep2.cu) with chains_per_warp C and steps_per_sweep steps;
+ * version 1 = row-by-row kernel (sweep.cu; used when the v2 plan does not fit
+ * shared memory, or with MCINV_KERNEL=v1 in the environment). */
+mcinv_status mcinv_kernel_info(const mcinv_ctx *ctx, int *version, int *chains_per_warp, int64_t *steps_per_sweep);
+
 /* ------------------------------------------------------------ test-only */
 
 /* Philox4x32-10 words on the device for `count` counters ctr4[4*count]
@@ -160,6 +166,16 @@ mcinv_status mcinv_debug_philox(int device, uint64_t seed, int64_t count, const 
 /* Box-Muller Gaussian of Philox(ctr, seed) for each counter (host arrays). */
 mcinv_status mcinv_debug_gaussian(int device, uint64_t seed, int64_t count, const uint32_t *ctr4,
                                   double *out);
+/* Host-only (no GPU needed): run mcinv_create's preprocessing and the v2
+ * step planner for C (and optional Q / pattern;
+ * p_rows == NULL selects the default pattern) and copy the record tiles of
+ * one sweep into `tiles` (NULL: size query). info[8] = {steps per sweep,
+ * tile slot bytes, max items per step, tile bytes, segments, entries, near
+ * entries, items}. For CPU tests of the planner. */
+mcinv_status mcinv_debug_plan(mcinv_dtype dtype, int64_t n, const int64_t *row_ptr, const int32_t *col_idx,
+                              const void *values, const int64_t *q_row_ptr, const int32_t *q_col_idx,
+                              const void *q_values, int64_t pcount, const int32_t *p_rows, const int32_t *p_cols,
+                              unsigned outputs, int chains_per_warp, void *tiles, size_t capacity, int64_t *info);
 /* Copy the state of chains [chain_begin, chain_begin+chains) (relative to the
  * last run's chain_begin) to host arrays z, w of shape [chains][n] (x2 doubles
  * for C128). Synchronizes. */

@@ -13,8 +13,14 @@
 #include <string>
 #include <vector>
 
+#include <cstdlib>
+#include <map>
+#include <memory>
+#include <tuple>
+
 #include "../../include/mcinv.h"
 #include "mcinv_internal.cuh"
+#include "plan.h"
 
 using mcinv::cd;
 using mcinv::ZW;
@@ -37,6 +43,13 @@ struct Entry {
     std::complex<double> v;
 };
 
+struct PlanDev {
+    DevBuf tiles, tile_off;
+    int steps = 0, tile_slot = 0, max_items = 0, C = 32;
+    std::string error;  // non-empty: plan not usable, v1 kernel is used
+    mcinv::HostPlan stats;
+};
+
 struct Layout {
     int ld = 0, G = 0, T = 0;
     int e = 1;              // doubles per scalar
@@ -55,10 +68,22 @@ struct mcinv_ctx {
     std::string err;
     int64_t err_index = -1;
     bool valid = false;
+    bool host_only = false;  // mcinv_debug_plan: no device allocations
 
     // host canonical C (rows sorted, duplicates summed), kept for the default pattern
     std::vector<int64_t> h_rp;
     std::vector<int> h_col;
+    // host copies for the v2 planner (plan.h)
+    std::vector<int> h_u_ptr, h_u_col;
+    std::vector<std::complex<double>> h_u_a, h_u_b, h_delta, h_sigma;
+    std::vector<int> h_prow, h_pcol;
+    std::vector<int64_t> h_q_ptr;
+    std::vector<int> h_q_col;
+    std::vector<std::complex<double>> h_q_val;
+    std::map<std::tuple<int, unsigned>, std::unique_ptr<PlanDev>> plans;  // (C, outputs) -> plan
+    int last_kernel = 0;  // 1 = v1, 2 = v2
+    int last_C = 0;
+    int64_t last_steps = 0;
     // device C
     DevBuf u_ptr, u_col, u_a, u_b, delta, sigma;
     // pattern
@@ -116,6 +141,7 @@ size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 template <typename T>
 mcinv_status upload(mcinv_ctx *ctx, DevBuf &b, const std::vector<T> &h) {
     b.release();
+    if (ctx->host_only) return MCINV_OK;
     const size_t bytes = std::max<size_t>(sizeof(T), h.size() * sizeof(T));
     if (cudaMalloc(&b.p, bytes) != cudaSuccess) {
         cudaGetLastError();
@@ -212,6 +238,8 @@ mcinv_status build_matrix(mcinv_ctx *ctx, const std::vector<std::vector<Entry>> 
             u_col.push_back(j);
             u_a.push_back(to_s<S>(a));
             u_b.push_back(to_s<S>(b));
+            ctx->h_u_a.push_back(a);
+            ctx->h_u_b.push_back(b);
         }
         u_ptr[i + 1] = (int)u_col.size();
         // delta_i = 1/c_ii, sigma_i = 1/sqrt(c_ii), principal branch (reading R1)
@@ -222,6 +250,19 @@ mcinv_status build_matrix(mcinv_ctx *ctx, const std::vector<std::vector<Entry>> 
         } else {
             dl[i] = to_s<S>(1.0 / diag[i]);
             sg[i] = to_s<S>(1.0 / std::sqrt(diag[i]));
+        }
+    }
+    ctx->h_u_ptr = u_ptr;
+    ctx->h_u_col = u_col;
+    ctx->h_delta.resize(n);
+    ctx->h_sigma.resize(n);
+    for (int64_t i = 0; i < n; ++i) {
+        if (ctx->dtype == MCINV_F64) {
+            ctx->h_delta[i] = 1.0 / diag[i].real();
+            ctx->h_sigma[i] = 1.0 / std::sqrt(diag[i].real());
+        } else {
+            ctx->h_delta[i] = 1.0 / diag[i];
+            ctx->h_sigma[i] = 1.0 / std::sqrt(diag[i]);
         }
     }
     TRY(upload(ctx, ctx->u_ptr, u_ptr));
@@ -252,6 +293,9 @@ mcinv_status build_pattern(mcinv_ctx *ctx, int64_t count, const int32_t *rows, c
         other[at] = (r >= c) ? c : (int)((unsigned)r | 0x80000000u);
     }
     idx.resize(std::max<int64_t>(count, 1));
+    ctx->h_prow.assign(rows, rows + count);
+    ctx->h_pcol.assign(cols, cols + count);
+    ctx->plans.clear();
     TRY(upload(ctx, ctx->p_ptr, ptr));
     TRY(upload(ctx, ctx->p_idx, idx));
     TRY(upload(ctx, ctx->p_other, other));
@@ -273,6 +317,17 @@ mcinv_status build_q(mcinv_ctx *ctx, const std::vector<std::vector<Entry>> &rows
     std::vector<int> rptr(n + 1, 0), rcol, cptr(n + 1, 0), crow;
     std::vector<S> rval, cval;
     std::vector<std::vector<Entry>> colpart(n);
+    ctx->h_q_ptr.assign(n + 1, 0);
+    ctx->h_q_col.clear();
+    ctx->h_q_val.clear();
+    for (int64_t i = 0; i < n; ++i) {
+        for (const Entry &e : rows[i]) {
+            ctx->h_q_col.push_back(e.j);
+            ctx->h_q_val.push_back(e.v);
+        }
+        ctx->h_q_ptr[i + 1] = (int64_t)ctx->h_q_col.size();
+    }
+    ctx->plans.clear();
     for (int64_t i = 0; i < n; ++i) {
         for (const Entry &e : rows[i]) {
             if (e.j <= i) {
@@ -392,6 +447,71 @@ Layout make_layout(const mcinv_ctx *ctx, const mcinv_run_args *a) {
     return L;
 }
 
+int choose_C(int64_t ld) {
+    // rows of a step (R = 32 / C) give intra-chain parallelism when chains are
+    // few; many chains fill the GPU by themselves (C = 32, fully coalesced)
+    if (const char *e = std::getenv("MCINV_C")) return std::atoi(e);
+    if (ld >= 32 * 148) return 32;
+    if (ld >= 16 * 148) return 16;
+    return 8;
+}
+
+int kernel_pref() {  // 0 auto, 1 force v1, 2 force v2
+    const char *e = std::getenv("MCINV_KERNEL");
+    if (!e) return 0;
+    if (!std::strcmp(e, "v1")) return 1;
+    if (!std::strcmp(e, "v2")) return 2;
+    return 0;
+}
+
+template <typename S>
+PlanDev *get_plan(mcinv_ctx *ctx, int C, unsigned outputs) {
+    const unsigned key_out = outputs & (MCINV_DIAG | MCINV_PATTERN | MCINV_TRACE);
+    auto key = std::make_tuple(C, key_out);
+    auto it = ctx->plans.find(key);
+    if (it != ctx->plans.end()) return it->second.get();
+    std::unique_ptr<PlanDev> pd(new PlanDev());
+    pd->C = C;
+    mcinv::PlanInput in;
+    in.n = ctx->n;
+    in.cplx = ctx->dtype == MCINV_C128;
+    in.u_ptr = &ctx->h_u_ptr;
+    in.u_col = &ctx->h_u_col;
+    in.u_a = &ctx->h_u_a;
+    in.u_b = &ctx->h_u_b;
+    in.delta = &ctx->h_delta;
+    in.sigma = &ctx->h_sigma;
+    in.want_diag = key_out & MCINV_DIAG;
+    in.want_pattern = key_out & MCINV_PATTERN;
+    in.want_trace = key_out & MCINV_TRACE;
+    in.p_row = &ctx->h_prow;
+    in.p_col = &ctx->h_pcol;
+    in.q_ptr = &ctx->h_q_ptr;
+    in.q_col = &ctx->h_q_col;
+    in.q_val = &ctx->h_q_val;
+    mcinv::HostPlan hp;
+    pd->error = mcinv::build_plan(in, 32 / C, C, hp);
+    if (pd->error.empty()) {
+        const size_t smem = mcinv::sweep2_smem<S>(hp.tile_slot_bytes, hp.max_items);
+        if (smem > 227 * 1024) pd->error = "plan needs " + std::to_string(smem) + " B of shared memory";
+    }
+    if (pd->error.empty()) {
+        if (upload(ctx, pd->tiles, hp.tiles) != MCINV_OK || upload(ctx, pd->tile_off, hp.tile_off) != MCINV_OK)
+            pd->error = "plan upload failed";
+        pd->steps = hp.steps;
+        pd->tile_slot = hp.tile_slot_bytes;
+        pd->max_items = hp.max_items;
+        if (!ctx->host_only) {
+            hp.tiles.clear();
+            hp.tiles.shrink_to_fit();
+        }
+        pd->stats = std::move(hp);
+    }
+    PlanDev *raw = pd.get();
+    ctx->plans[key] = std::move(pd);
+    return raw;
+}
+
 template <typename S>
 mcinv_status run_typed(mcinv_ctx *ctx, const mcinv_run_args *a, const Layout &L, char *ws, cudaStream_t st) {
     using namespace mcinv;
@@ -429,30 +549,72 @@ mcinv_status run_typed(mcinv_ctx *ctx, const mcinv_run_args *a, const Layout &L,
         if (a->outputs & MCINV_FULL) CK(cudaMemsetAsync(ws + L.slot_full, 0, (size_t)L.G * n * n * sizeof(S), st));
         if (a->outputs & MCINV_TRACE) CK(cudaMemsetAsync(p.slot_trace, 0, (size_t)L.G * sizeof(S), st));
     }
-    if (!(a->outputs & MCINV_FULL)) {
-        p.s_begin = 0;
-        p.s_end = total;
-        if (total > 0) timed(ctx, 0, st, [&] { launch_sweep<S>(p, st); });
-    } else {
-        // burn-in (and nothing else) in one launch, then T-sweep chunks each
-        // followed by the X Y^dagger contraction of its snapshots
-        p.snap_x = (S *)(ws + L.snap_x);
-        p.snap_y = (S *)(ws + L.snap_y);
-        if (a->burn_in > 0) {
-            p.s_begin = 0;
-            p.s_end = (int)a->burn_in;
-            p.snap_s0 = 0;
-            SweepParams<S> q = p;
-            timed(ctx, 0, st, [&] { launch_sweep<S>(q, st); });
-        }
-        for (int s0 = (int)a->burn_in; s0 < total; s0 += L.T) {
-            const int s1 = std::min(total, s0 + L.T);
+    // kernel choice: v2 (step schedule, sweep2.cu) unless its plan does not fit
+    const int pref = kernel_pref();
+    const int C = choose_C(L.ld);
+    PlanDev *plan = pref == 1 ? nullptr : get_plan<S>(ctx, C, a->outputs);
+    const bool v2 = plan && plan->error.empty();
+    if (pref == 2 && !v2) return fail(ctx, MCINV_E_INVALID, "v2 kernel unavailable: " + plan->error);
+    ctx->last_kernel = v2 ? 2 : 1;
+    ctx->last_C = v2 ? plan->C : 32;
+    ctx->last_steps = v2 ? plan->steps : n;
+    Sweep2Params<S> q2{};
+    if (v2) {
+        q2.tiles = (const unsigned char *)plan->tiles.p;
+        q2.tile_off = (const int64_t *)plan->tile_off.p;
+        q2.steps = plan->steps;
+        q2.tile_slot = plan->tile_slot;
+        q2.max_items = plan->max_items;
+        q2.zw = p.zw;
+        q2.n = (int)n;
+        q2.ld = L.ld;
+        q2.chains = p.chains;
+        q2.chain0 = p.chain0;
+        q2.key0 = p.key0;
+        q2.key1 = p.key1;
+        q2.noise = p.noise;
+        q2.sweep_abs0 = p.sweep_abs0;
+        q2.burn_in = p.burn_in;
+        q2.gs = p.gs;
+        q2.pcount = (int)ctx->pcount;
+        q2.slot_diag = p.slot_diag;
+        q2.slot_pat = p.slot_pat;
+        q2.slot_trace = p.slot_trace;
+    }
+    cudaError_t lerr = cudaSuccess;
+    auto sweep = [&](int s0, int s1, int snap_s0, unsigned outs) {
+        if (v2) {
+            Sweep2Params<S> q = q2;
+            q.s_begin = s0;
+            q.s_end = s1;
+            q.snap_s0 = snap_s0;
+            q.outputs = outs;
+            q.snap_x = (S *)(ws + L.snap_x);
+            q.snap_y = (S *)(ws + L.snap_y);
+            timed(ctx, 0, st, [&] {
+                cudaError_t e = launch_sweep2<S>(q, plan->C, st);
+                if (e != cudaSuccess) lerr = e;
+            });
+        } else {
             SweepParams<S> q = p;
             q.s_begin = s0;
             q.s_end = s1;
-            q.snap_s0 = s0;
-            q.outputs = a->outputs;
+            q.snap_s0 = snap_s0;
+            q.outputs = outs;
+            q.snap_x = (S *)(ws + L.snap_x);
+            q.snap_y = (S *)(ws + L.snap_y);
             timed(ctx, 0, st, [&] { launch_sweep<S>(q, st); });
+        }
+    };
+    if (!(a->outputs & MCINV_FULL)) {
+        if (total > 0) sweep(0, total, 0, a->outputs);
+    } else {
+        // burn-in in one launch, then T-sweep chunks each followed by the
+        // X Y^dagger contraction of its snapshots
+        if (a->burn_in > 0) sweep(0, (int)a->burn_in, 0, a->outputs & ~(unsigned)MCINV_FULL);
+        for (int s0 = (int)a->burn_in; s0 < total; s0 += L.T) {
+            const int s1 = std::min(total, s0 + L.T);
+            sweep(s0, s1, s0, a->outputs);
             timed(ctx, 1, st, [&] {
                 launch_contract<S>((const S *)(ws + L.snap_x), (const S *)(ws + L.snap_y),
                                    (double *)(ws + L.slot_full), (int)n, L.ld, (int)a->chains, a->group_size,
@@ -460,6 +622,7 @@ mcinv_status run_typed(mcinv_ctx *ctx, const mcinv_run_args *a, const Layout &L,
             });
         }
     }
+    if (lerr != cudaSuccess) return fail(ctx, MCINV_E_CUDA, std::string("sweep2 launch: ") + cudaGetErrorString(lerr));
     CK(cudaGetLastError());
     // moments and divergence flag
     double *mom = (double *)(ws + L.mom);
@@ -666,6 +829,14 @@ void mcinv_destroy(mcinv_ctx *ctx) {
     delete ctx;
 }
 
+mcinv_status mcinv_kernel_info(const mcinv_ctx *ctx, int *version, int *chains_per_warp, int64_t *steps_per_sweep) {
+    if (!ctx || !ctx->have_run) return MCINV_E_STATE;
+    if (version) *version = ctx->last_kernel;
+    if (chains_per_warp) *chains_per_warp = ctx->last_C;
+    if (steps_per_sweep) *steps_per_sweep = ctx->last_steps;
+    return MCINV_OK;
+}
+
 mcinv_status mcinv_set_timing(mcinv_ctx *ctx, int enable) {
     if (!ctx || !ctx->valid) return MCINV_E_STATE;
     ctx->timing = enable != 0;
@@ -694,6 +865,48 @@ mcinv_status mcinv_stats(mcinv_ctx *ctx, int64_t *launches, double *sweep_ms, in
     if (contract_ms) *contract_ms = ms[1];
     if (contract_launches) *contract_launches = cnt[1];
     ctx->launches = 0;
+    return MCINV_OK;
+}
+
+mcinv_status mcinv_debug_plan(mcinv_dtype dtype, int64_t n, const int64_t *row_ptr, const int32_t *col_idx,
+                              const void *values, const int64_t *q_row_ptr, const int32_t *q_col_idx,
+                              const void *q_values, int64_t pcount, const int32_t *p_rows, const int32_t *p_cols,
+                              unsigned outputs, int chains_per_warp, void *tiles, size_t capacity, int64_t *info) {
+    if (!info) return MCINV_E_INVALID;
+    if (chains_per_warp != 8 && chains_per_warp != 16 && chains_per_warp != 32) return MCINV_E_INVALID;
+    mcinv_ctx c;
+    mcinv_ctx *ctx = &c;
+    ctx->host_only = true;
+    ctx->dtype = dtype;
+    ctx->n = n;
+    if (dtype != MCINV_F64 && dtype != MCINV_C128) return MCINV_E_INVALID;
+    if (n < 1 || n >= (int64_t(1) << 31)) return MCINV_E_INVALID;
+    std::vector<std::vector<Entry>> rows;
+    TRY(read_csr(ctx, n, row_ptr, col_idx, (const double *)values, dtype == MCINV_C128, rows));
+    TRY(dtype == MCINV_C128 ? build_matrix<cd>(ctx, rows) : build_matrix<double>(ctx, rows));
+    if (p_rows) TRY(build_pattern(ctx, pcount, p_rows, p_cols));
+    else TRY(default_pattern(ctx));
+    if (q_row_ptr) {
+        std::vector<std::vector<Entry>> qrows;
+        TRY(read_csr(ctx, n, q_row_ptr, q_col_idx, (const double *)q_values, dtype == MCINV_C128, qrows));
+        TRY(dtype == MCINV_C128 ? build_q<cd>(ctx, qrows) : build_q<double>(ctx, qrows));
+    }
+    PlanDev *pd = dtype == MCINV_C128 ? get_plan<cd>(ctx, chains_per_warp, outputs)
+                                      : get_plan<double>(ctx, chains_per_warp, outputs);
+    if (!pd->error.empty()) return fail(ctx, MCINV_E_INVALID, pd->error);
+    const mcinv::HostPlan &hp = pd->stats;
+    info[0] = hp.steps;
+    info[1] = hp.tile_slot_bytes;
+    info[2] = hp.max_items;
+    info[3] = (int64_t)hp.tiles.size();
+    info[4] = hp.segments;
+    info[5] = hp.entries;
+    info[6] = hp.near_entries;
+    info[7] = hp.items;
+    if (tiles) {
+        if (capacity < hp.tiles.size()) return MCINV_E_BUFFER;
+        std::memcpy(tiles, hp.tiles.data(), hp.tiles.size());
+    }
     return MCINV_OK;
 }
 

@@ -1,0 +1,266 @@
+// plan.cu -- host planner for the v2 sweep kernel; see plan.h.
+#include <algorithm>
+#include <cstring>
+#include <queue>
+
+#include "plan.h"
+
+namespace mcinv {
+
+namespace {
+
+struct Ent {
+    int j;
+    std::complex<double> a, b;
+};
+
+struct Item {
+    int op, partner;  // partner row (or -1 for self)
+    int slot;
+    std::complex<double> q;
+};
+
+struct Seg {
+    int row;
+    int first_entry, count;  // entries [first_entry, first_entry + count) of the row list
+    bool first, last;
+};
+
+void put_scalar(unsigned char *p, std::complex<double> v, bool cplx) {
+    double re = v.real(), im = v.imag();
+    std::memcpy(p, &re, 8);
+    if (cplx) std::memcpy(p + 8, &im, 8);
+}
+
+}  // namespace
+
+std::string build_plan(const PlanInput &in, int R, int C, HostPlan &out) {
+    const int64_t n = in.n;
+    const bool cplx = in.cplx;
+    const int esz = cplx ? 16 : 8;
+    const int zwsz = 2 * esz;
+    const int BLK = R * C * zwsz;
+    const int RING_OFF = 0;
+    const int GB_OFF = NRING * BLK;
+    const int ZERO_OFF = GB_OFF + NRING * KCAP * BLK;
+    if (R * C != 32) return "R * C must be 32";
+
+    // ---- items per row (Eq. 1/C pattern and diag, Eq. tr split by max(i,j))
+    std::vector<std::vector<Item>> items(n);
+    if (in.want_diag)
+        for (int64_t i = 0; i < n; ++i) items[i].push_back(Item{IT_DIAG, -1, (int)i, {}});
+    if (in.want_pattern) {
+        const auto &pr = *in.p_row, &pc = *in.p_col;
+        for (size_t p = 0; p < pr.size(); ++p) {
+            const int r = pr[p], c = pc[p];
+            if (r == c) items[r].push_back(Item{IT_PAT_SELF, -1, (int)p, {}});
+            else if (r > c) items[r].push_back(Item{IT_PAT_ZI, c, (int)p, {}});
+            else items[c].push_back(Item{IT_PAT_ZO, r, (int)p, {}});
+        }
+    }
+    if (in.want_trace) {
+        const auto &qp = *in.q_ptr;
+        const auto &qc = *in.q_col;
+        const auto &qv = *in.q_val;
+        for (int64_t i = 0; i < n; ++i)
+            for (int64_t e = qp[i]; e < qp[i + 1]; ++e) {
+                const int j = qc[e];
+                if (j == i) items[i].push_back(Item{IT_QROW_SELF, -1, 0, qv[e]});
+                else if (j < i) items[i].push_back(Item{IT_QROW, j, 0, qv[e]});
+                else items[j].push_back(Item{IT_QCOL, (int)i, 0, qv[e]});  // Q_ij, i < j: at row j
+            }
+    }
+
+    // ---- entry lists (union of row i and column i of C, H1)
+    std::vector<std::vector<Ent>> ent(n);
+    for (int64_t i = 0; i < n; ++i) {
+        const auto &up = *in.u_ptr;
+        for (int e = up[i]; e < up[i + 1]; ++e) ent[i].push_back(Ent{(*in.u_col)[e], (*in.u_a)[e], (*in.u_b)[e]});
+    }
+
+    // ---- dependency graph: every entry relation i~j orients min -> max
+    std::vector<std::vector<int>> succ(n);
+    std::vector<int> npred(n, 0);
+    {
+        std::vector<std::pair<int, int>> edges;
+        for (int64_t i = 0; i < n; ++i) {
+            for (const Ent &e : ent[i])
+                if (e.j != i) edges.emplace_back(std::min<int>(i, e.j), std::max<int>(i, e.j));
+            for (const Item &it : items[i])  // accumulation partners are lower rows: j -> i
+                if (it.partner >= 0 && it.partner != i)
+                    edges.emplace_back(std::min<int>(i, it.partner), std::max<int>(i, it.partner));
+        }
+        std::sort(edges.begin(), edges.end());
+        edges.erase(std::unique(edges.begin(), edges.end()), edges.end());
+        for (auto &e : edges) {
+            succ[e.first].push_back(e.second);
+            npred[e.second]++;
+        }
+    }
+
+    // ---- list scheduling: steps of R slots, segments of a row consecutive in one slot
+    std::vector<std::vector<Seg>> steps;  // steps[t][r]
+    std::vector<int> fin_step(n, -1), fin_slot(n, -1);
+    {
+        std::priority_queue<int, std::vector<int>, std::greater<int>> ready;
+        for (int64_t i = 0; i < n; ++i)
+            if (npred[i] == 0) ready.push((int)i);
+        struct Active {
+            int row = -1, next_seg = 0, nseg = 0;
+        };
+        std::vector<Active> act(R);
+        int64_t done = 0;
+        std::vector<int> newly;
+        while (done < n) {
+            std::vector<Seg> st(R, Seg{-1, 0, 0, false, false});
+            for (int r = 0; r < R; ++r) {
+                if (act[r].row < 0 && !ready.empty()) {
+                    const int i = ready.top();
+                    ready.pop();
+                    const int len = (int)ent[i].size();
+                    act[r].row = i;
+                    act[r].next_seg = 0;
+                    act[r].nseg = len == 0 ? 1 : (len + KCAP - 1) / KCAP;
+                }
+                if (act[r].row >= 0) {
+                    const int i = act[r].row;
+                    const int s = act[r].next_seg;
+                    const int len = (int)ent[i].size();
+                    Seg sg;
+                    sg.row = i;
+                    sg.first_entry = s * KCAP;
+                    sg.count = std::min(KCAP, len - s * KCAP);
+                    if (sg.count < 0) sg.count = 0;
+                    sg.first = s == 0;
+                    sg.last = s == act[r].nseg - 1;
+                    st[r] = sg;
+                }
+            }
+            const int t = (int)steps.size();
+            newly.clear();
+            bool any = false;
+            for (int r = 0; r < R; ++r) {
+                if (act[r].row < 0) continue;
+                any = true;
+                if (st[r].last) {
+                    const int i = act[r].row;
+                    fin_step[i] = t;
+                    fin_slot[i] = r;
+                    ++done;
+                    for (int s : succ[i])
+                        if (--npred[s] == 0) newly.push_back(s);
+                    act[r].row = -1;
+                } else {
+                    act[r].next_seg++;
+                }
+            }
+            if (!any) return "scheduler stalled (cyclic dependency?)";
+            steps.push_back(st);
+            for (int s : newly) ready.push(s);
+        }
+    }
+    while (steps.size() % NRING) steps.push_back(std::vector<Seg>(R, Seg{-1, 0, 0, false, false}));
+    const int S = (int)steps.size();
+
+    // ---- tiles
+    out = HostPlan();
+    out.R = R;
+    out.C = C;
+    out.steps = S;
+    out.tile_off.assign(S + 1, 0);
+    std::vector<TileLayout> lay(S);
+    for (int t = 0; t < S; ++t) {
+        int K = 0, I = 0;
+        for (int r = 0; r < R; ++r) {
+            const Seg &sg = steps[t][r];
+            if (sg.row < 0) continue;
+            K = std::max(K, sg.count);
+            if (sg.last) I = std::max(I, (int)items[sg.row].size());
+        }
+        lay[t] = TileLayout{K, I, R, esz};
+        out.tile_off[t + 1] = out.tile_off[t] + lay[t].total();
+        out.tile_slot_bytes = std::max(out.tile_slot_bytes, lay[t].total());
+        out.max_items = std::max(out.max_items, I);
+    }
+    out.tiles.assign(out.tile_off[S], 0);
+    for (int t = 0; t < S; ++t) {
+        const TileLayout &L = lay[t];
+        unsigned char *T = out.tiles.data() + out.tile_off[t];
+        const int nt = (t + NTILE - 1) % S;
+        int hdr[4] = {L.K, L.I, (int)(out.tile_off[nt + 1] - out.tile_off[nt]), 0};
+        int64_t noff = out.tile_off[nt];
+        std::memcpy(T, hdr, 16);
+        std::memcpy(T + 16, &noff, 8);
+        int *rows = (int *)(T + L.rows());
+        int *flags = rows + R;
+        for (int r = 0; r < R; ++r) {
+            const Seg &sg = steps[t][r];
+            rows[r] = sg.row;
+            flags[r] = sg.row < 0 ? 0 : (4 | (sg.first ? 1 : 0) | (sg.last ? 2 : 0));
+            if (sg.row >= 0 && sg.last) {
+                put_scalar(T + L.dsig() + r * esz, (*in.delta)[sg.row], cplx);
+                put_scalar(T + L.dsig() + (R + r) * esz, (*in.sigma)[sg.row], cplx);
+            }
+        }
+        for (int k = 0; k < L.K; ++k)
+            for (int r = 0; r < R; ++r) {
+                int *meta = (int *)(T + L.meta() + 8 * (k * R + r));
+                unsigned char *cf = T + L.coef() + 2 * esz * (k * R + r);
+                const Seg &sg = steps[t][r];
+                if (sg.row < 0 || k >= sg.count) {
+                    meta[0] = ZERO_OFF;
+                    meta[1] = -1;
+                    continue;
+                }
+                const int i = sg.row;
+                const Ent &e = ent[i][sg.first_entry + k];
+                const int j = e.j;
+                const int tj = fin_step[j];
+                const int d = (j < i) ? t - tj : S + t - tj;
+                if (d < 1 || d > S) return "internal: bad distance";
+                out.entries++;
+                if (d <= PDIST) {
+                    meta[0] = RING_OFF + ((((t - d) % NRING) + NRING) % NRING) * BLK + fin_slot[j] * C * zwsz;
+                    meta[1] = -1;
+                    out.near_entries++;
+                } else {
+                    meta[0] = GB_OFF + ((t % NRING) * KCAP + k) * BLK + r * C * zwsz;
+                    meta[1] = j;
+                }
+                put_scalar(cf, e.a, cplx);
+                put_scalar(cf + esz, e.b, cplx);
+            }
+        for (int q = 0; q < L.I; ++q)
+            for (int r = 0; r < R; ++r) {
+                unsigned char *it = T + L.items() + L.item_bytes() * (q * R + r);
+                int code = IT_NOP, slot = 0, prow = -1, voff = -1;
+                std::complex<double> qv = 0.0;
+                const Seg &sg = steps[t][r];
+                if (sg.row >= 0 && sg.last && q < (int)items[sg.row].size()) {
+                    const Item &m = items[sg.row][q];
+                    code = m.op;
+                    if (m.partner >= 0) {
+                        prow = m.partner;
+                        // partner among this segment's entries -> its value is in smem
+                        for (int k = 0; k < sg.count; ++k)
+                            if (ent[sg.row][sg.first_entry + k].j == m.partner) {
+                                voff = ((const int *)(T + L.meta() + 8 * (k * R + r)))[0];
+                                code |= 8;
+                                break;
+                            }
+                    }
+                    slot = m.slot;
+                    qv = m.q;
+                    out.items++;
+                }
+                int w4[4] = {code, slot, prow, voff};
+                std::memcpy(it, w4, 16);
+                put_scalar(it + 16, qv, cplx);
+            }
+        for (int r = 0; r < R; ++r)
+            if (steps[t][r].row >= 0) out.segments++;
+    }
+    return "";
+}
+
+}  // namespace mcinv

@@ -50,6 +50,12 @@ __device__ __forceinline__ cd shfl_xor_s(cd v, int off) {
 __device__ __forceinline__ void add_to(double *p, double v) { p[0] += v; }
 __device__ __forceinline__ void add_to(double *p, cd v) { p[0] += v.re; p[1] += v.im; }
 
+__device__ __forceinline__ void atomic_add_to(double *p, double v) { atomicAdd(p, v); }
+__device__ __forceinline__ void atomic_add_to(double *p, cd v) {
+    atomicAdd(p, v.re);
+    atomicAdd(p + 1, v.im);
+}
+
 __device__ __forceinline__ bool bad_s(double v) { return !(fabs(v) <= 1e12); }
 __device__ __forceinline__ bool bad_s(cd v) { return !(fabs(v.re) <= 1e12) || !(fabs(v.im) <= 1e12); }
 

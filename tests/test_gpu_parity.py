@@ -236,6 +236,30 @@ def test_errors(mc):
     assert e.value.code == 8
 
 
+@pytest.mark.parametrize("kernel", ["v1", "v2"])
+def test_both_kernels(mc, orc, kernel, monkeypatch):
+    """The row-by-row kernel (v1) and the step-scheduled kernel (v2) both
+    match the oracle; v2 is forced for every chains-per-warp layout."""
+    monkeypatch.setenv("MCINV_KERNEL", kernel)
+    for C in ((8, 16, 32) if kernel == "v2" else (32,)):
+        monkeypatch.setenv("MCINV_C", str(C))
+        compare_run(mc, orc, W.pedigree(500, seed=21), seed=4, chains=64, burn_in=2, cycles=4,
+                    outputs=("diag", "pattern"), group_size=8)
+        c = W.lattice(4, 3, 0.15, seed=22)
+        compare_run(mc, orc, c, q=W.random_q(c.n, 23, 3), seed=5, chains=40, burn_in=2, cycles=3,
+                    outputs=("diag", "trace", "full"), group_size=4, snapshot_sweeps=2)
+
+
+def test_bench_configs_use_v2(mc):
+    for k in (2, 3, 5):
+        c, q, run = W.config(k)
+        inv = mc.Inverter(c, q=q)
+        inv.run(run.seed, run.chains, 0, 1, tuple(o for o in run.outputs if o != "full") or ("diag",),
+                group_size=run.group_size)
+        assert inv.kernel_info()["version"] == 2, k
+        inv.close()
+
+
 # ------------------------------------------------------------- full sizes (bench launch configuration)
 
 def _exact_columns(c, cols, tol=1e-14):
