@@ -71,11 +71,38 @@ std::string build_plan(const PlanInput &in, int R, int C, HostPlan &out) {
             }
     }
 
-    // ---- entry lists (union of row i and column i of C, H1)
+    // ---- entry lists (union of row i and column i of C, H1). Accumulation
+    // partners must be operands of the row's FINAL segment so that their
+    // values are prefetched with the other operands; partners elsewhere get a
+    // zero-coefficient duplicate appended (an exact no-op in the fma chain).
     std::vector<std::vector<Ent>> ent(n);
+    int64_t dups = 0;
     for (int64_t i = 0; i < n; ++i) {
+        auto &L = ent[i];
         const auto &up = *in.u_ptr;
-        for (int e = up[i]; e < up[i + 1]; ++e) ent[i].push_back(Ent{(*in.u_col)[e], (*in.u_a)[e], (*in.u_b)[e]});
+        for (int e = up[i]; e < up[i + 1]; ++e) L.push_back(Ent{(*in.u_col)[e], (*in.u_a)[e], (*in.u_b)[e]});
+        std::vector<int> partners;
+        for (const Item &it : items[i])
+            if (it.partner >= 0) partners.push_back(it.partner);
+        std::sort(partners.begin(), partners.end());
+        partners.erase(std::unique(partners.begin(), partners.end()), partners.end());
+        if ((int)partners.size() > KCAP) continue;  // too many: the kernel reads them from HBM
+        for (int iter = 0; iter <= 4 * KCAP; ++iter) {
+            const int len = (int)L.size();
+            const int F = len == 0 ? 0 : ((len - 1) / KCAP) * KCAP;
+            int missing = -1;
+            for (int pj : partners) {
+                bool ok = false;
+                for (int k = F; k < len && !ok; ++k) ok = L[k].j == pj;
+                if (!ok) {
+                    missing = pj;
+                    break;
+                }
+            }
+            if (missing < 0) break;
+            L.push_back(Ent{missing, 0.0, 0.0});
+            ++dups;
+        }
     }
 
     // ---- dependency graph: every entry relation i~j orients min -> max
@@ -168,6 +195,7 @@ std::string build_plan(const PlanInput &in, int R, int C, HostPlan &out) {
     out.C = C;
     out.steps = S;
     out.tile_off.assign(S + 1, 0);
+    out.dup_entries = dups;
     std::vector<TileLayout> lay(S);
     for (int t = 0; t < S; ++t) {
         int K = 0, I = 0;
