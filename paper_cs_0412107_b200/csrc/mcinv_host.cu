@@ -492,7 +492,7 @@ PlanDev *get_plan(mcinv_ctx *ctx, int C, unsigned outputs) {
     mcinv::HostPlan hp;
     pd->error = mcinv::build_plan(in, 32 / C, C, hp);
     if (pd->error.empty()) {
-        const size_t smem = mcinv::sweep2_smem<S>(hp.tile_slot_bytes, hp.max_items);
+        const size_t smem = mcinv::sweep2_smem<S>(hp.tile_slot_bytes, hp.max_parts);
         if (smem > 227 * 1024) pd->error = "plan needs " + std::to_string(smem) + " B of shared memory";
     }
     if (pd->error.empty()) {
@@ -500,7 +500,7 @@ PlanDev *get_plan(mcinv_ctx *ctx, int C, unsigned outputs) {
             pd->error = "plan upload failed";
         pd->steps = hp.steps;
         pd->tile_slot = hp.tile_slot_bytes;
-        pd->max_items = hp.max_items;
+        pd->max_items = hp.max_parts;
         if (!ctx->host_only) {
             hp.tiles.clear();
             hp.tiles.shrink_to_fit();
@@ -897,12 +897,12 @@ mcinv_status mcinv_debug_plan(mcinv_dtype dtype, int64_t n, const int64_t *row_p
     const mcinv::HostPlan &hp = pd->stats;
     info[0] = hp.steps;
     info[1] = hp.tile_slot_bytes;
-    info[2] = hp.max_items;
+    info[2] = hp.max_parts;
     info[3] = (int64_t)hp.tiles.size();
     info[4] = hp.segments;
     info[5] = hp.entries;
     info[6] = hp.near_entries;
-    info[7] = hp.items;
+    info[7] = hp.parts;
     if (tiles) {
         if (capacity < hp.tiles.size()) return MCINV_E_BUFFER;
         std::memcpy(tiles, hp.tiles.data(), hp.tiles.size());

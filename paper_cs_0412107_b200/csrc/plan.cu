@@ -1,4 +1,4 @@
-// plan.cu -- host planner for the v2 sweep kernel; see plan.h.
+// plan.cu -- host planner for the step-scheduled sweep kernel; see plan.h.
 #include <algorithm>
 #include <cstring>
 #include <queue>
@@ -14,10 +14,18 @@ struct Ent {
     std::complex<double> a, b;
 };
 
-struct Item {
-    int op, partner;  // partner row (or -1 for self)
-    int slot;
-    std::complex<double> q;
+// accumulation record of one partner row j (lower than the row i)
+struct Part {
+    int j;
+    int pzi = -1, pzo = -1;
+    std::complex<double> qr = 0.0, qc = 0.0;
+    bool has_qr = false, has_qc = false;
+};
+
+struct RowAcc {
+    int dslot = -1, pslot = -1;
+    std::complex<double> qself = 0.0;
+    std::vector<Part> parts;
 };
 
 struct Seg {
@@ -32,6 +40,18 @@ void put_scalar(unsigned char *p, std::complex<double> v, bool cplx) {
     if (cplx) std::memcpy(p + 8, &im, 8);
 }
 
+Part &part_for(RowAcc &ra, int j, int role) {
+    // role 0 pzi, 1 pzo, 2 qr, 3 qc: first record of j with that role free
+    for (Part &p : ra.parts) {
+        if (p.j != j) continue;
+        if ((role == 0 && p.pzi < 0) || (role == 1 && p.pzo < 0) || (role == 2 && !p.has_qr) ||
+            (role == 3 && !p.has_qc))
+            return p;
+    }
+    ra.parts.push_back(Part{j});
+    return ra.parts.back();
+}
+
 }  // namespace
 
 std::string build_plan(const PlanInput &in, int R, int C, HostPlan &out) {
@@ -39,23 +59,27 @@ std::string build_plan(const PlanInput &in, int R, int C, HostPlan &out) {
     const bool cplx = in.cplx;
     const int esz = cplx ? 16 : 8;
     const int zwsz = 2 * esz;
-    const int BLK = R * C * zwsz;
-    const int RING_OFF = 0;
+    const int BLK = 32 * zwsz;
     const int GB_OFF = NRING * BLK;
-    const int ZERO_OFF = GB_OFF + NRING * KCAP * BLK;
+    const int ZERO_OFF = GB_OFF + NGBUF * KCAP * BLK;
     if (R * C != 32) return "R * C must be 32";
 
-    // ---- items per row (Eq. 1/C pattern and diag, Eq. tr split by max(i,j))
-    std::vector<std::vector<Item>> items(n);
+    // ---- accumulation requests per row, keyed by r = max(i, j) (Eq. 1/C, Eq. tr)
+    std::vector<RowAcc> acc(n);
     if (in.want_diag)
-        for (int64_t i = 0; i < n; ++i) items[i].push_back(Item{IT_DIAG, -1, (int)i, {}});
+        for (int64_t i = 0; i < n; ++i) acc[i].dslot = (int)i;
     if (in.want_pattern) {
         const auto &pr = *in.p_row, &pc = *in.p_col;
         for (size_t p = 0; p < pr.size(); ++p) {
             const int r = pr[p], c = pc[p];
-            if (r == c) items[r].push_back(Item{IT_PAT_SELF, -1, (int)p, {}});
-            else if (r > c) items[r].push_back(Item{IT_PAT_ZI, c, (int)p, {}});
-            else items[c].push_back(Item{IT_PAT_ZO, r, (int)p, {}});
+            if (r == c) {
+                if (acc[r].pslot >= 0) return "duplicate diagonal pattern element";
+                acc[r].pslot = (int)p;
+            } else if (r > c) {
+                part_for(acc[r], c, 0).pzi = (int)p;   // z_r conj(w_c) at row r
+            } else {
+                part_for(acc[c], r, 1).pzo = (int)p;   // z_r conj(w_c) at row c
+            }
         }
     }
     if (in.want_trace) {
@@ -65,16 +89,22 @@ std::string build_plan(const PlanInput &in, int R, int C, HostPlan &out) {
         for (int64_t i = 0; i < n; ++i)
             for (int64_t e = qp[i]; e < qp[i + 1]; ++e) {
                 const int j = qc[e];
-                if (j == i) items[i].push_back(Item{IT_QROW_SELF, -1, 0, qv[e]});
-                else if (j < i) items[i].push_back(Item{IT_QROW, j, 0, qv[e]});
-                else items[j].push_back(Item{IT_QCOL, (int)i, 0, qv[e]});  // Q_ij, i < j: at row j
+                if (j == i) {
+                    acc[i].qself += qv[e];
+                } else if (j < i) {
+                    Part &p = part_for(acc[i], j, 2);  // conj(w_i) Q_ij z_j at row i
+                    p.qr = qv[e];
+                    p.has_qr = true;
+                } else {
+                    Part &p = part_for(acc[j], (int)i, 3);  // conj(w_i) Q_ij z_j at row j
+                    p.qc = qv[e];
+                    p.has_qc = true;
+                }
             }
     }
 
-    // ---- entry lists (union of row i and column i of C, H1). Accumulation
-    // partners must be operands of the row's FINAL segment so that their
-    // values are prefetched with the other operands; partners elsewhere get a
-    // zero-coefficient duplicate appended (an exact no-op in the fma chain).
+    // ---- entry lists (union of row i and column i of C, H1); partners must be
+    // operands of the last two segments: append zero-coefficient duplicates
     std::vector<std::vector<Ent>> ent(n);
     int64_t dups = 0;
     for (int64_t i = 0; i < n; ++i) {
@@ -82,18 +112,20 @@ std::string build_plan(const PlanInput &in, int R, int C, HostPlan &out) {
         const auto &up = *in.u_ptr;
         for (int e = up[i]; e < up[i + 1]; ++e) L.push_back(Ent{(*in.u_col)[e], (*in.u_a)[e], (*in.u_b)[e]});
         std::vector<int> partners;
-        for (const Item &it : items[i])
-            if (it.partner >= 0) partners.push_back(it.partner);
+        for (const Part &p : acc[i].parts) partners.push_back(p.j);
         std::sort(partners.begin(), partners.end());
         partners.erase(std::unique(partners.begin(), partners.end()), partners.end());
-        if ((int)partners.size() > KCAP) continue;  // too many: the kernel reads them from HBM
-        for (int iter = 0; iter <= 4 * KCAP; ++iter) {
+        if ((int)partners.size() > MAXPART)
+            return "row " + std::to_string(i) + " has more than " + std::to_string(MAXPART) + " accumulation partners";
+        for (int iter = 0;; ++iter) {
+            if (iter > 4 * MAXPART) return "internal: partner placement did not converge";
             const int len = (int)L.size();
-            const int F = len == 0 ? 0 : ((len - 1) / KCAP) * KCAP;
+            const int nseg = len == 0 ? 1 : (len + KCAP - 1) / KCAP;
+            const int W = nseg >= 2 ? (nseg - 2) * KCAP : 0;
             int missing = -1;
             for (int pj : partners) {
                 bool ok = false;
-                for (int k = F; k < len && !ok; ++k) ok = L[k].j == pj;
+                for (int k = W; k < len && !ok; ++k) ok = L[k].j == pj;
                 if (!ok) {
                     missing = pj;
                     break;
@@ -105,18 +137,14 @@ std::string build_plan(const PlanInput &in, int R, int C, HostPlan &out) {
         }
     }
 
-    // ---- dependency graph: every entry relation i~j orients min -> max
+    // ---- dependency graph: every operand relation i~j orients min -> max
     std::vector<std::vector<int>> succ(n);
     std::vector<int> npred(n, 0);
     {
         std::vector<std::pair<int, int>> edges;
-        for (int64_t i = 0; i < n; ++i) {
+        for (int64_t i = 0; i < n; ++i)
             for (const Ent &e : ent[i])
                 if (e.j != i) edges.emplace_back(std::min<int>(i, e.j), std::max<int>(i, e.j));
-            for (const Item &it : items[i])  // accumulation partners are lower rows: j -> i
-                if (it.partner >= 0 && it.partner != i)
-                    edges.emplace_back(std::min<int>(i, it.partner), std::max<int>(i, it.partner));
-        }
         std::sort(edges.begin(), edges.end());
         edges.erase(std::unique(edges.begin(), edges.end()), edges.end());
         for (auto &e : edges) {
@@ -156,8 +184,7 @@ std::string build_plan(const PlanInput &in, int R, int C, HostPlan &out) {
                     Seg sg;
                     sg.row = i;
                     sg.first_entry = s * KCAP;
-                    sg.count = std::min(KCAP, len - s * KCAP);
-                    if (sg.count < 0) sg.count = 0;
+                    sg.count = std::max(0, std::min(KCAP, len - s * KCAP));
                     sg.first = s == 0;
                     sg.last = s == act[r].nseg - 1;
                     st[r] = sg;
@@ -189,6 +216,24 @@ std::string build_plan(const PlanInput &in, int R, int C, HostPlan &out) {
     while (steps.size() % NRING) steps.push_back(std::vector<Seg>(R, Seg{-1, 0, 0, false, false}));
     const int S = (int)steps.size();
 
+    // smem value offset of operand k of the segment in slot r at step t
+    auto value_off = [&](int t, int r, int k, int *col, bool *is_near) -> int {
+        const Seg &sg = steps[t][r];
+        const int i = sg.row;
+        const int j = ent[i][sg.first_entry + k].j;
+        const int tj = fin_step[j];
+        const int d = (j < i) ? t - tj : S + t - tj;
+        if (d < 1 || d > S) return -1;
+        if (d <= PDIST) {
+            *col = -1;
+            *is_near = true;
+            return ((((t - d) % NRING) + NRING) % NRING) * BLK + fin_slot[j] * C * zwsz;
+        }
+        *col = j;
+        *is_near = false;
+        return GB_OFF + ((t % NGBUF) * KCAP + k) * BLK + r * C * zwsz;
+    };
+
     // ---- tiles
     out = HostPlan();
     out.R = R;
@@ -198,36 +243,38 @@ std::string build_plan(const PlanInput &in, int R, int C, HostPlan &out) {
     out.dup_entries = dups;
     std::vector<TileLayout> lay(S);
     for (int t = 0; t < S; ++t) {
-        int K = 0, I = 0;
+        int K = 0, P = 0;
         for (int r = 0; r < R; ++r) {
             const Seg &sg = steps[t][r];
             if (sg.row < 0) continue;
             K = std::max(K, sg.count);
-            if (sg.last) I = std::max(I, (int)items[sg.row].size());
+            if (sg.last) P = std::max(P, (int)acc[sg.row].parts.size());
         }
-        lay[t] = TileLayout{K, I, R, esz};
+        lay[t] = TileLayout{K, P, R, esz};
         out.tile_off[t + 1] = out.tile_off[t] + lay[t].total();
         out.tile_slot_bytes = std::max(out.tile_slot_bytes, lay[t].total());
-        out.max_items = std::max(out.max_items, I);
+        out.max_parts = std::max(out.max_parts, P);
     }
     out.tiles.assign(out.tile_off[S], 0);
     for (int t = 0; t < S; ++t) {
         const TileLayout &L = lay[t];
         unsigned char *T = out.tiles.data() + out.tile_off[t];
-        const int nt = (t + NTILE - 1) % S;
-        int hdr[4] = {L.K, L.I, (int)(out.tile_off[nt + 1] - out.tile_off[nt]), 0};
+        const int nt = (t + 8) % S;  // the producer issues tile t+8 while gathering step t
+        int hdr[4] = {L.K, L.P, (int)(out.tile_off[nt + 1] - out.tile_off[nt]), in.want_trace ? 1 : 0};
         int64_t noff = out.tile_off[nt];
         std::memcpy(T, hdr, 16);
         std::memcpy(T + 16, &noff, 8);
         int *rows = (int *)(T + L.rows());
-        int *flags = rows + R;
         for (int r = 0; r < R; ++r) {
             const Seg &sg = steps[t][r];
             rows[r] = sg.row;
-            flags[r] = sg.row < 0 ? 0 : (4 | (sg.first ? 1 : 0) | (sg.last ? 2 : 0));
+            rows[R + r] = sg.row < 0 ? 0 : (4 | (sg.first ? 1 : 0) | (sg.last ? 2 : 0));
+            rows[2 * R + r] = (sg.row >= 0 && sg.last) ? acc[sg.row].dslot : -1;
+            rows[3 * R + r] = (sg.row >= 0 && sg.last) ? acc[sg.row].pslot : -1;
             if (sg.row >= 0 && sg.last) {
-                put_scalar(T + L.dsig() + r * esz, (*in.delta)[sg.row], cplx);
-                put_scalar(T + L.dsig() + (R + r) * esz, (*in.sigma)[sg.row], cplx);
+                put_scalar(T + L.dsq() + r * esz, (*in.delta)[sg.row], cplx);
+                put_scalar(T + L.dsq() + (R + r) * esz, (*in.sigma)[sg.row], cplx);
+                put_scalar(T + L.dsq() + (2 * R + r) * esz, acc[sg.row].qself, cplx);
             }
         }
         for (int k = 0; k < L.K; ++k)
@@ -240,53 +287,59 @@ std::string build_plan(const PlanInput &in, int R, int C, HostPlan &out) {
                     meta[1] = -1;
                     continue;
                 }
-                const int i = sg.row;
-                const Ent &e = ent[i][sg.first_entry + k];
-                const int j = e.j;
-                const int tj = fin_step[j];
-                const int d = (j < i) ? t - tj : S + t - tj;
-                if (d < 1 || d > S) return "internal: bad distance";
+                int col = -1;
+                bool nr = false;
+                const int off = value_off(t, r, k, &col, &nr);
+                if (off < 0) return "internal: bad operand distance";
+                meta[0] = off;
+                meta[1] = col;
                 out.entries++;
-                if (d <= PDIST) {
-                    meta[0] = RING_OFF + ((((t - d) % NRING) + NRING) % NRING) * BLK + fin_slot[j] * C * zwsz;
-                    meta[1] = -1;
-                    out.near_entries++;
-                } else {
-                    meta[0] = GB_OFF + ((t % NRING) * KCAP + k) * BLK + r * C * zwsz;
-                    meta[1] = j;
-                }
+                out.near_entries += nr;
+                const Ent &e = ent[sg.row][sg.first_entry + k];
                 put_scalar(cf, e.a, cplx);
                 put_scalar(cf + esz, e.b, cplx);
             }
-        for (int q = 0; q < L.I; ++q)
-            for (int r = 0; r < R; ++r) {
-                unsigned char *it = T + L.items() + L.item_bytes() * (q * R + r);
-                int code = IT_NOP, slot = 0, prow = -1, voff = -1;
-                std::complex<double> qv = 0.0;
-                const Seg &sg = steps[t][r];
-                if (sg.row >= 0 && sg.last && q < (int)items[sg.row].size()) {
-                    const Item &m = items[sg.row][q];
-                    code = m.op;
-                    if (m.partner >= 0) {
-                        prow = m.partner;
-                        // partner among this segment's entries -> its value is in smem
-                        for (int k = 0; k < sg.count; ++k)
-                            if (ent[sg.row][sg.first_entry + k].j == m.partner) {
-                                voff = ((const int *)(T + L.meta() + 8 * (k * R + r)))[0];
-                                code |= 8;
-                                break;
-                            }
-                    }
-                    slot = m.slot;
-                    qv = m.q;
-                    out.items++;
-                }
-                int w4[4] = {code, slot, prow, voff};
-                std::memcpy(it, w4, 16);
-                put_scalar(it + 16, qv, cplx);
-            }
         for (int r = 0; r < R; ++r)
             if (steps[t][r].row >= 0) out.segments++;
+        for (int q = 0; q < L.P; ++q)
+            for (int r = 0; r < R; ++r) {
+                unsigned char *pr = T + L.part() + L.part_bytes() * (q * R + r);
+                int w4[4] = {ZERO_OFF, -1, -1, 0};
+                std::complex<double> qr = 0.0, qc = 0.0;
+                const Seg &sg = steps[t][r];
+                if (sg.row >= 0 && sg.last && q < (int)acc[sg.row].parts.size()) {
+                    const int i = sg.row;
+                    const Part &pt = acc[i].parts[q];
+                    // operand of the final segment (step t) or of the previous one (t-1)
+                    int voff = -1;
+                    for (int k = 0; k < sg.count && voff < 0; ++k)
+                        if (ent[i][sg.first_entry + k].j == pt.j) {
+                            int col;
+                            bool nr;
+                            voff = value_off(t, r, k, &col, &nr);
+                        }
+                    if (voff < 0 && !sg.first) {
+                        const Seg &pv = steps[t - 1][r];
+                        if (pv.row != i) return "internal: previous segment not in t-1";
+                        for (int k = 0; k < pv.count && voff < 0; ++k)
+                            if (ent[i][pv.first_entry + k].j == pt.j) {
+                                int col;
+                                bool nr;
+                                voff = value_off(t - 1, r, k, &col, &nr);
+                            }
+                    }
+                    if (voff < 0) return "internal: partner operand not found";
+                    w4[0] = voff;
+                    w4[1] = pt.pzi;
+                    w4[2] = pt.pzo;
+                    qr = pt.qr;
+                    qc = pt.qc;
+                    out.parts++;
+                }
+                std::memcpy(pr, w4, 16);
+                put_scalar(pr + 16, qr, cplx);
+                put_scalar(pr + 16 + esz, qc, cplx);
+            }
     }
     return "";
 }

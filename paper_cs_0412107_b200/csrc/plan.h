@@ -1,4 +1,4 @@
-// plan.h -- host planner for the v2 sweep kernel (sweep2.cu).
+// plan.h -- host planner for the step-scheduled sweep kernel (sweep2.cu).
 //
 // The sweep of Eq. (4)/(5) visits rows in ascending order;
 // row i reads new values of its lower neighbours (j < i) and old values of
@@ -12,8 +12,11 @@
 //
 // Rows longer than KCAP entries are split into segments in consecutive steps
 // of the same row slot. Each entry is classified by the distance d (in steps)
-// from the step that produced its value: d <= P: read from the in-smem ring of
-// recent results; d > P: gathered from HBM P steps ahead with cp.async.
+// from the step that produced its value: d <= PDIST: read from the in-smem
+// ring of recent results; d > PDIST: gathered from HBM 8 steps ahead with
+// cp.async. Accumulation partners of a row (Eq. 1/C pattern elements, Eq. tr
+// Q terms) are operands of its last two segments (zero-coefficient duplicates
+// are appended when needed), so the accumulator warp finds them in smem.
 #pragma once
 #include <complex>
 #include <cstdint>
@@ -23,21 +26,11 @@
 namespace mcinv {
 
 constexpr int KCAP = 8;     // entries per row segment
-constexpr int PDIST = 7;    // gather prefetch distance (steps)
-constexpr int NRING = 8;    // ring / gbuf slots (PDIST + 1)
-constexpr int NTILE = 16;   // record tile slots (tile for step T+15 issued at step T)
-
-// item opcodes (accumulation at the final segment of a row; Eq. 1/C, Eq. tr)
-enum ItemOp : int {
-    IT_NOP = 0,
-    IT_DIAG = 1,       // diag slot  += z_i conj(w_i)
-    IT_PAT_ZI = 2,     // pat slot   += z_i conj(w_k)    (partner = entry k)
-    IT_PAT_ZO = 3,     // pat slot   += z_k conj(w_i)
-    IT_PAT_SELF = 4,   // pat slot   += z_i conj(w_i)
-    IT_QROW = 5,       // qz += q z_k
-    IT_QROW_SELF = 6,  // qz += q z_i
-    IT_QCOL = 7        // qw += q conj(w_k)
-};
+constexpr int PDIST = 7;    // near/far threshold (steps): far operands are >= 8 steps old
+constexpr int NGBUF = 8;    // gather-buffer step slots
+constexpr int NRING = 16;   // result-ring step slots (steps per sweep padded to a multiple)
+constexpr int NTILE = 16;   // record tile slots
+constexpr int MAXPART = 2 * KCAP;  // accumulation partners per row
 
 struct PlanInput {
     int64_t n = 0;
@@ -58,29 +51,45 @@ struct HostPlan {
     int R = 1, C = 32;
     int steps = 0;              // steps per sweep (padded to a multiple of NRING)
     int tile_slot_bytes = 0;    // max tile bytes (16-aligned)
-    int max_items = 0;
+    int max_parts = 0;          // max partner records per row slot in a step
     std::vector<unsigned char> tiles;   // concatenated tiles
     std::vector<int64_t> tile_off;      // steps + 1
     // statistics
-    int64_t segments = 0, entries = 0, near_entries = 0, items = 0, dup_entries = 0;
+    int64_t segments = 0, entries = 0, near_entries = 0, parts = 0, dup_entries = 0;
 };
 
 // Build the plan; returns "" on success or an error message.
 std::string build_plan(const PlanInput &in, int R, int C, HostPlan &out);
 
-// Tile layout, shared with the kernel. All section offsets are 16-aligned.
+// Tile layout, shared with the kernel; every section offset is 16-aligned.
+//   hdr   32 B : int K, int P, int next_bytes, int has_q; int64 next_off; pad
+//   rows  16R  : int row[R], int flags[R] (1 first seg, 2 last seg, 4 busy),
+//                int dslot[R] (diag slot or -1), int pslot[R] (pattern (i,i) slot or -1)
+//   dsq   3R S : delta[R], sigma[R], qself[R] (Q_ii)
+//   meta  K R  : int2 {smem value offset, gather column or -1}
+//   coef  K R  : S a (Eq. 4 coefficient), S b (Eq. 5 coefficient)
+//   part  P R  : {int voff, int pzi, int pzo, int pad, S qr, S qc}
+//                pzi: pattern slot of z_i conj(w_j); pzo: slot of z_j conj(w_i)
+//                qr = Q_ij (j < i), qc = Q_ji (j < i) for the trace w^dagger Q z
 struct TileLayout {
-    int K, I, R, esz;  // esz = sizeof(scalar) (8 or 16)
-    __host__ __device__ int hdr() const { return 0; }                       // 32 B
-    __host__ __device__ int rows() const { return 32; }                     // int rows[R], int flags[R]
-    __host__ __device__ int dsig() const { return 32 + r16(8 * R); }        // S delta[R], S sigma[R]
-    __host__ __device__ int meta() const { return dsig() + r16(2 * R * esz); }  // int2 meta[K][R]
-    __host__ __device__ int coef() const { return meta() + r16(8 * K * R); }    // S a,b [K][R]
-    __host__ __device__ int items() const { return coef() + r16(2 * esz * K * R); }  // item [I][R]
-    // item: {int code (op | 8 * has_voff), int slot, int partner_row, int voff, S q, pad}
-    __host__ __device__ int item_bytes() const { return 32; }
-    __host__ __device__ int total() const { return items() + r16(item_bytes() * I * R); }
+    int K, P, R, esz;
+    __host__ __device__ int rows() const { return 32; }
+    __host__ __device__ int dsq() const { return 32 + r16(16 * R); }
+    __host__ __device__ int meta() const { return dsq() + r16(3 * R * esz); }
+    __host__ __device__ int coef() const { return meta() + r16(8 * K * R); }
+    __host__ __device__ int part() const { return coef() + r16(2 * esz * K * R); }
+    __host__ __device__ int part_bytes() const { return 16 + 2 * esz; }
+    __host__ __device__ int total() const { return part() + r16(part_bytes() * P * R); }
     __host__ __device__ static int r16(int x) { return (x + 15) & ~15; }
+};
+
+// Shared-memory value area of the kernel (bytes): ring | gather buffer | zero block.
+template <int ESZ> struct ValueArea {
+    static constexpr int BLK = 32 * 2 * ESZ;  // one step slot: R rows x C chains x (z, w)
+    static constexpr int RING = 0;
+    static constexpr int GBUF = NRING * BLK;
+    static constexpr int ZERO = GBUF + NGBUF * KCAP * BLK;
+    static constexpr int BYTES = ZERO + BLK;
 };
 
 }  // namespace mcinv

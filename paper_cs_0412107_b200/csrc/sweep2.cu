@@ -1,25 +1,25 @@
-// sweep2.cu -- K1/K2 v2: the CC sweep kernel on a dependency-respecting step
-// schedule (plan.h), one warp per CTA.
+// sweep2.cu -- K1/K2 (v2): the CC sweep on a dependency-respecting step
+// schedule (plan.h), warp-specialized.
 //
-// Lanes = C chains x R row slots (C * R = 32). A step updates up to R rows of
-// the warp's C chains at once; the planner guarantees that the rows of a step
-// do not depend on each other and that every operand is exactly the one the
-// sequential sweep (Eq. 4/5) would read, so z and w are
-// bit-identical to the row-by-row order (checked against the oracle).
+// One CTA owns C chains; lanes = C chains x R row slots (C * R = 32). The
+// planner guarantees that the rows of a step do not depend on each other and
+// that every operand is exactly the one the sequential sweep (Eq. 4/5,
+// PAPER.md:157-160) reads, so z and w are bit-identical to row-by-row order.
 //
-// Per step T the warp
-//   1. issues the TMA bulk copy of the record tile of step T+15 (cols,
-//      coefficients, smem source offsets, accumulation items) into a 16-slot
-//      smem ring (mbarrier complete_tx),
-//   2. issues cp.async gathers of the z/w pairs of step T+7's far entries
-//      (produced >= 8 steps ago) from the [n][ld] state in HBM into smem,
-//   3. runs the serial fma chains of step T reading operands from smem (far
-//      entries: the gather buffer; near entries: a ring of the last 8 steps'
-//      results), draws phi (Philox4x32-10 + Box-Muller, noise.cuh), writes
-//      z_i, w_i to HBM and to the ring,
-//   4. in sampling sweeps accumulates diag / pattern via an smem transpose
-//      reduction over the chains of an SE group, and the trace w^dagger Q z in
-//      registers (Eq. 1/C, Eq. tr).
+// Warp roles (all synchronised with mbarriers, per step slot):
+//   A  (warp 0)   the serial part only: for each step, the fma chains of
+//                 Eq. (4)/(5) over smem operands, z_i, w_i to HBM and to the
+//                 16-step result ring, FULL-output snapshots.
+//   B  (warp 1)   producer: TMA bulk copy of the record tile of step U+8
+//                 (cols, coefficients, smem source offsets, accumulation
+//                 records) and cp.async gathers of step U's far operands
+//                 (>= 8 steps old) from the [n][ld] state in HBM.
+//   D  (warp 2)   accumulation (sampling sweeps): diag, pattern and trace
+//                 products of the rows finished in the step (Eq. 1/C, Eq. tr,
+//                 P:173-182), smem transpose-reduction over the chains of an
+//                 SE group, one RMW (or RED) per group slot.
+//   N  (warps 3+) noise: phi(row, sweep, chain) by Philox4x32-10 + Box-Muller
+//                 (noise.cuh) into an smem ring, NW warps round-robin.
 #include "mcinv_internal.cuh"
 #include "noise.cuh"
 #include "plan.h"
@@ -29,14 +29,14 @@ namespace mcinv {
 
 namespace {
 
+constexpr int NQ = 8;  // noise ring slots
+
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
-
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
 }
-
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred p;\n"
@@ -46,21 +46,21 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
-
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
 __device__ __forceinline__ void tma_load_1d(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
                  "l"(src), "r"(bytes), "r"(bar)
                  : "memory");
 }
-
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void *src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+// arrive on the mbarrier when all prior cp.async of this thread complete
+__device__ __forceinline__ void cp_async_arrive(uint32_t bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(bar) : "memory");
 }
 
 template <typename S>
@@ -68,247 +68,278 @@ __device__ __forceinline__ S lds_s(const unsigned char *p) {
     return *reinterpret_cast<const S *>(p);
 }
 
+// phase parity of the use of a step-indexed barrier slot (T relative to T0)
+__device__ __forceinline__ uint32_t par(int64_t T, int64_t T0, int nslots) {
+    return (uint32_t)(((T - T0) / nslots) & 1);
+}
+
 }  // namespace
 
-template <typename S, int C, int R>
-__global__ void __launch_bounds__(32) sweep2_kernel(const Sweep2Params<S> p) {
+template <typename S, int C, int R, int NW>
+__global__ void __launch_bounds__(32 * (3 + NW)) sweep2_kernel(const Sweep2Params<S> p) {
     constexpr int ESZ = sizeof(S);
     constexpr int ZWSZ = 2 * ESZ;
-    constexpr int BLK = 32 * ZWSZ;
-    constexpr int GB_OFF = NRING * BLK;
-    constexpr int ZERO_OFF = GB_OFF + NRING * KCAP * BLK;
-    constexpr int VAL_BYTES = ZERO_OFF + BLK;
+    using VA = ValueArea<ESZ>;
+    constexpr int BLK = VA::BLK;
 
     extern __shared__ __align__(128) unsigned char smem[];
     unsigned char *vals = smem;
-    unsigned char *tiles = smem + VAL_BYTES;
-    unsigned char *stage = tiles + NTILE * p.tile_slot;
-    uint64_t *bars = reinterpret_cast<uint64_t *>(stage + (size_t)p.max_items * 32 * ESZ);
+    unsigned char *tiles = smem + VA::BYTES;
+    double *noise = reinterpret_cast<double *>(tiles + NTILE * p.tile_slot);   // [NQ][32]
+    unsigned char *stage = reinterpret_cast<unsigned char *>(noise + NQ * 32);  // D products [2P+2][32]
+    uint64_t *bars = reinterpret_cast<uint64_t *>(stage + (size_t)(2 * p.max_items + 2) * 32 * ESZ);
+    uint64_t *b_tile = bars;                   // [NTILE] TMA complete_tx
+    uint64_t *b_gather = b_tile + NTILE;       // [NGBUF] 32 cp.async arrivals
+    uint64_t *b_adone = b_gather + NGBUF;      // [NGBUF] A finished step
+    uint64_t *b_ddone = b_adone + NGBUF;       // [NGBUF] D finished step
+    uint64_t *b_nfull = b_ddone + NGBUF;       // [NQ] noise ready
+    uint64_t *b_nempty = b_nfull + NQ;         // [NQ] noise consumed
 
-    const int lane = threadIdx.x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int c = lane % C, r = lane / C;
-    const int cb = blockIdx.x * C;        // first local chain of this CTA
-    const int chain = cb + c;             // local chain (< ld)
+    const int cb = blockIdx.x * C;
+    const int chain = cb + c;
     const bool active = chain < p.chains;
     const uint32_t gchain = p.chain0 + static_cast<uint32_t>(chain);
-    const int coff = c * ZWSZ;            // lane's chain offset inside a block row
+    const int coff = c * ZWSZ;
+    const int roff = r * C * ZWSZ;
     const int64_t T0 = (int64_t)p.s_begin * p.steps, T_end = (int64_t)p.s_end * p.steps;
     const int S_n = p.steps;
+    auto tile_of = [&](int64_t T) { return tiles + (T % NTILE) * p.tile_slot; };
 
-    // ---- init: barriers, zero block
-    for (int b = lane; b < BLK / 16; b += 32) reinterpret_cast<double2 *>(vals + ZERO_OFF)[b] = make_double2(0.0, 0.0);
-    if (lane == 0) {
-        for (int s = 0; s < NTILE; ++s) mbar_init(smem_u32(&bars[s]), 1);
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < NTILE; ++s) mbar_init(smem_u32(&b_tile[s]), 1);
+        for (int s = 0; s < NGBUF; ++s) {
+            mbar_init(smem_u32(&b_gather[s]), 32);
+            mbar_init(smem_u32(&b_adone[s]), 1);
+            mbar_init(smem_u32(&b_ddone[s]), 1);
+        }
+        for (int s = 0; s < NQ; ++s) {
+            mbar_init(smem_u32(&b_nfull[s]), 1);
+            mbar_init(smem_u32(&b_nempty[s]), 1);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    __syncwarp();
-
-    auto issue_tile = [&](int64_t T, int64_t goff, int bytes) {
-        if (lane == 0) {
-            const int s = (int)(T % NTILE);
-            tma_load_1d(smem_u32(tiles + s * p.tile_slot), p.tiles + goff, (uint32_t)bytes, smem_u32(&bars[s]));
+    if (warp == 0) {
+        // zero block and the ring of the 7 steps before T0 (from the state)
+        for (int b = lane; b < BLK / 16; b += 32)
+            reinterpret_cast<double2 *>(vals + VA::ZERO)[b] = make_double2(0.0, 0.0);
+        for (int q = 1; q <= PDIST; ++q) {
+            const int64_t T = T0 - q;
+            const int t = (int)(((T % S_n) + S_n) % S_n);
+            const int *g = reinterpret_cast<const int *>(p.tiles + p.tile_off[t] + 32);
+            const int row = g[r], flg = g[R + r];
+            if (row >= 0 && (flg & 2))
+                *reinterpret_cast<ZW<S> *>(vals + (((T % NRING) + NRING) % NRING) * BLK + roff + coff) =
+                    p.zw[(int64_t)row * p.ld + chain];
         }
-    };
-    auto wait_tile = [&](int64_t T) {
-        mbar_wait(smem_u32(&bars[T % NTILE]), (uint32_t)(((T - T0) / NTILE) & 1));
-    };
-    auto tile_of = [&](int64_t T) { return tiles + (T % NTILE) * p.tile_slot; };
-    // gathers of the far entries of step T (tile already landed)
-    auto gather = [&](int64_t T) {
-        const unsigned char *tl = tile_of(T);
-        const int K = reinterpret_cast<const int *>(tl)[0];
-        const TileLayout L{K, 0, R, ESZ};
-        for (int k = 0; k < K; ++k) {
-            const int2 m = *reinterpret_cast<const int2 *>(tl + L.meta() + 8 * (k * R + r));
-            if (m.y >= 0) {
-                const unsigned char *src = reinterpret_cast<const unsigned char *>(p.zw + (int64_t)m.y * p.ld + chain);
-                const uint32_t dst = smem_u32(vals + m.x + coff);
+    }
+    __syncthreads();
+
+    if (warp == 1) {
+        // ================= B: tiles and gathers
+        if (lane == 0)
+            for (int64_t T = T0; T < T0 + 8 && T < T_end; ++T) {
+                const int t = (int)(T % S_n);
+                tma_load_1d(smem_u32(tile_of(T)), p.tiles + p.tile_off[t], (uint32_t)(p.tile_off[t + 1] - p.tile_off[t]),
+                            smem_u32(&b_tile[T % NTILE]));
+            }
+        for (int64_t U = T0; U < T_end; ++U) {
+            if (U - 8 >= T0) mbar_wait(smem_u32(&b_adone[U % NGBUF]), par(U - 8, T0, NGBUF));
+            if (U - 7 >= T0) mbar_wait(smem_u32(&b_ddone[(U - 7) % NGBUF]), par(U - 7, T0, NGBUF));
+            mbar_wait(smem_u32(&b_tile[U % NTILE]), par(U, T0, NTILE));
+            const unsigned char *tl = tile_of(U);
+            const int *hdr = reinterpret_cast<const int *>(tl);
+            if (lane == 0 && U + 8 < T_end) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                tma_load_1d(smem_u32(tile_of(U + 8)), p.tiles + *reinterpret_cast<const int64_t *>(tl + 16),
+                            (uint32_t)hdr[2], smem_u32(&b_tile[(U + 8) % NTILE]));
+            }
+            const TileLayout L{hdr[0], hdr[1], R, ESZ};
+            for (int k = 0; k < L.K; ++k) {
+                const int2 m = *reinterpret_cast<const int2 *>(tl + L.meta() + 8 * (k * R + r));
+                if (m.y >= 0) {
+                    const unsigned char *src =
+                        reinterpret_cast<const unsigned char *>(p.zw + (int64_t)m.y * p.ld + chain);
+                    const uint32_t dst = smem_u32(vals + m.x + coff);
 #pragma unroll
-                for (int h = 0; h < ZWSZ / 16; ++h) cp_async16(dst + 16 * h, src + 16 * h);
-            }
-        }
-    };
-
-    // ---- prologue: tiles T0 .. T0+14, ring of the 7 steps before T0, gathers T0 .. T0+6
-    for (int64_t T = T0; T < T0 + NTILE - 1 && T < T_end; ++T) {
-        const int t = (int)(T % S_n);
-        issue_tile(T, p.tile_off[t], (int)(p.tile_off[t + 1] - p.tile_off[t]));
-    }
-    for (int q = 1; q <= PDIST; ++q) {
-        const int64_t T = T0 - q;
-        const int t = (int)(((T % S_n) + S_n) % S_n);
-        const unsigned char *g = p.tiles + p.tile_off[t];
-        const int row = reinterpret_cast<const int *>(g + 32)[r];
-        const int flg = reinterpret_cast<const int *>(g + 32)[R + r];
-        if (row >= 0 && (flg & 2)) {
-            const ZW<S> v = p.zw[(int64_t)row * p.ld + chain];
-            *reinterpret_cast<ZW<S> *>(vals + (((T % NRING) + NRING) % NRING) * BLK + r * C * ZWSZ + coff) = v;
-        }
-    }
-    for (int64_t T = T0; T < T0 + PDIST; ++T) {
-        if (T < T_end) {
-            wait_tile(T);
-            gather(T);
-        }
-        cp_async_commit();
-    }
-    __syncwarp();
-
-    S acc_z = zero_s<S>(), acc_w = zero_s<S>(), tr = zero_s<S>();
-    const bool want_tr = (p.outputs & OUT_TRACE) != 0;
-    for (int64_t T = T0; T < T_end; ++T) {
-        const unsigned char *tl = tile_of(T);
-        const int *hdr = reinterpret_cast<const int *>(tl);
-        const int K = hdr[0], I = hdr[1];
-        // 1. record tile of step T+15 into the slot of step T-1
-        if (T + NTILE - 1 < T_end) {
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            issue_tile(T + NTILE - 1, *reinterpret_cast<const int64_t *>(tl + 16), hdr[2]);
-        }
-        // 2. gathers for step T+7 (its far entries were produced at steps <= T-1)
-        if (T + PDIST < T_end) {
-            wait_tile(T + PDIST);
-            gather(T + PDIST);
-        }
-        cp_async_commit();
-        // 3. operands of step T have landed
-        cp_async_wait<PDIST>();
-
-        const TileLayout L{K, I, R, ESZ};
-        const int flags = reinterpret_cast<const int *>(tl + 32)[R + r];
-        if (flags & 1) {
-            acc_z = zero_s<S>();
-            acc_w = zero_s<S>();
-        }
-        for (int k = 0; k < K; ++k) {
-            const int off = reinterpret_cast<const int *>(tl + L.meta())[2 * (k * R + r)];
-            const S a = lds_s<S>(tl + L.coef() + 2 * ESZ * (k * R + r));
-            const S b = lds_s<S>(tl + L.coef() + 2 * ESZ * (k * R + r) + ESZ);
-            const ZW<S> v = *reinterpret_cast<const ZW<S> *>(vals + off + coff);
-            acc_z = fma_s(a, v.z, acc_z);
-            acc_w = fma_s(b, v.w, acc_w);
-        }
-        const bool last = (flags & 2) != 0;
-        const int64_t s_loc = T / S_n;  // local sweep index of this launch's sweep range
-        const bool sampling = s_loc >= p.burn_in;
-        S zi = zero_s<S>(), wi = zero_s<S>();
-        if (last) {
-            const int row = reinterpret_cast<const int *>(tl + 32)[r];
-            double phi;
-            if (p.noise == 0)
-                phi = gaussian(static_cast<uint32_t>(row), p.sweep_abs0 + static_cast<uint32_t>(s_loc), gchain, p.key0,
-                               p.key1);
-            else
-                phi = p.noise == 2 ? 1.0 : 0.0;
-            const S dl = lds_s<S>(tl + L.dsig() + r * ESZ);
-            const S sg = lds_s<S>(tl + L.dsig() + (R + r) * ESZ);
-            zi = fma_s(neg_s(dl), acc_z, scale_s(sg, phi));
-            wi = fma_s(neg_s(conj_s(dl)), acc_w, scale_s(conj_s(sg), phi));
-            p.zw[(int64_t)row * p.ld + chain] = ZW<S>{zi, wi};
-            *reinterpret_cast<ZW<S> *>(vals + (T % NRING) * BLK + r * C * ZWSZ + coff) = ZW<S>{zi, wi};
-            if ((p.outputs & OUT_FULL) && sampling) {
-                const int64_t t = s_loc - p.snap_s0;
-                p.snap_x[(t * p.n + row) * p.ld + chain] = zi;
-                p.snap_y[(t * p.n + row) * p.ld + chain] = wi;
-            }
-        }
-        if (sampling && I > 0) {
-            // 4. items: products (staged for the group reduction) and trace registers
-            S qz = zero_s<S>(), qw = zero_s<S>();
-            const bool live = last && active;
-            for (int q = 0; q < I; ++q) {
-                const unsigned char *it = tl + L.items() + L.item_bytes() * (q * R + r);
-                const int4 w4 = *reinterpret_cast<const int4 *>(it);
-                const int op = w4.x & 7;
-                ZW<S> pv{zero_s<S>(), zero_s<S>()};
-                if (op == IT_PAT_ZI || op == IT_PAT_ZO || op == IT_QROW || op == IT_QCOL) {
-                    if (w4.x & 8) pv = *reinterpret_cast<const ZW<S> *>(vals + w4.w + coff);
-                    else if (live) pv = p.zw[(int64_t)w4.z * p.ld + chain];
+                    for (int h = 0; h < ZWSZ / 16; ++h) cp_async16(dst + 16 * h, src + 16 * h);
                 }
-                S prod = zero_s<S>();
-                switch (op) {
-                    case IT_DIAG:
-                    case IT_PAT_SELF: prod = zwc_s(zi, wi); break;
-                    case IT_PAT_ZI: prod = zwc_s(zi, pv.w); break;
-                    case IT_PAT_ZO: prod = zwc_s(pv.z, wi); break;
-                    case IT_QROW: qz = add_s(qz, mul_s(lds_s<S>(it + 16), pv.z)); break;
-                    case IT_QROW_SELF: qz = add_s(qz, mul_s(lds_s<S>(it + 16), zi)); break;
-                    case IT_QCOL: qw = add_s(qw, mul_s(lds_s<S>(it + 16), conj_s(pv.w))); break;
-                    default: break;
-                }
-                *reinterpret_cast<S *>(stage + (q * 32 + lane) * ESZ) = live ? prod : zero_s<S>();
             }
-            if (want_tr && live) tr = add_s(tr, add_s(zwc_s(qz, wi), mul_s(zi, qw)));
+            cp_async_arrive(smem_u32(&b_gather[U % NGBUF]));
+        }
+    } else if (warp == 0) {
+        // ================= A: the serial fma chains
+        S acc_z = zero_s<S>(), acc_w = zero_s<S>();
+        for (int64_t T = T0; T < T_end; ++T) {
+            mbar_wait(smem_u32(&b_gather[T % NGBUF]), par(T, T0, NGBUF));
+            const unsigned char *tl = tile_of(T);
+            const int *hdr = reinterpret_cast<const int *>(tl);
+            const TileLayout L{hdr[0], hdr[1], R, ESZ};
+            const int flags = reinterpret_cast<const int *>(tl + 32)[R + r];
+            if (flags & 1) {
+                acc_z = zero_s<S>();
+                acc_w = zero_s<S>();
+            }
+            for (int k = 0; k < L.K; ++k) {
+                const int off = reinterpret_cast<const int *>(tl + L.meta())[2 * (k * R + r)];
+                const unsigned char *cf = tl + L.coef() + 2 * ESZ * (k * R + r);
+                const ZW<S> v = *reinterpret_cast<const ZW<S> *>(vals + off + coff);
+                acc_z = fma_s(lds_s<S>(cf), v.z, acc_z);
+                acc_w = fma_s(lds_s<S>(cf + ESZ), v.w, acc_w);
+            }
+            mbar_wait(smem_u32(&b_nfull[T % NQ]), par(T, T0, NQ));
+            if (flags & 2) {
+                const int row = reinterpret_cast<const int *>(tl + 32)[r];
+                const double phi = noise[(T % NQ) * 32 + lane];
+                const S dl = lds_s<S>(tl + L.dsq() + r * ESZ);
+                const S sg = lds_s<S>(tl + L.dsq() + (R + r) * ESZ);
+                const S zi = fma_s(neg_s(dl), acc_z, scale_s(sg, phi));
+                const S wi = fma_s(neg_s(conj_s(dl)), acc_w, scale_s(conj_s(sg), phi));
+                p.zw[(int64_t)row * p.ld + chain] = ZW<S>{zi, wi};
+                *reinterpret_cast<ZW<S> *>(vals + (T % NRING) * BLK + roff + coff) = ZW<S>{zi, wi};
+                const int64_t s_loc = T / S_n;
+                if ((p.outputs & OUT_FULL) && s_loc >= p.burn_in) {
+                    const int64_t t = s_loc - p.snap_s0;
+                    p.snap_x[(t * p.n + row) * p.ld + chain] = zi;
+                    p.snap_y[(t * p.n + row) * p.ld + chain] = wi;
+                }
+            }
             __syncwarp();
-            // group sums: one task per (item, row slot, SE group); groups wider
-            // than the CTA's C chains are completed with atomics across CTAs
-            const int gse = p.gs < C ? p.gs : C;
-            const int gpr = C / gse;  // groups (or group parts) per row slot
-            const int ntask = I * R * gpr;
-            for (int tk = lane; tk < ntask; tk += 32) {
-                const int q = tk / (R * gpr), rem = tk % (R * gpr);
-                const int r2 = rem / gpr, g2 = rem % gpr;
-                const unsigned char *it = tl + L.items() + L.item_bytes() * (q * R + r2);
-                const int2 w2 = *reinterpret_cast<const int2 *>(it);
-                const int op = w2.x & 7;
-                if (op < IT_DIAG || op > IT_PAT_SELF) continue;
-                const int c0 = g2 * gse;
-                if (cb + c0 >= p.chains) continue;
+            if (lane == 0) {
+                mbar_arrive(smem_u32(&b_nempty[T % NQ]));
+                mbar_arrive(smem_u32(&b_adone[T % NGBUF]));
+            }
+        }
+    } else if (warp == 2) {
+        // ================= D: accumulation
+        const bool want_tr = (p.outputs & OUT_TRACE) != 0;
+        const bool want_red = (p.outputs & (OUT_DIAG | OUT_PATTERN)) != 0;
+        const int gse = p.gs < C ? p.gs : C;
+        const int gpr = C / gse;
+        S tr = zero_s<S>();
+        S *st = reinterpret_cast<S *>(stage);
+        for (int64_t T = T0; T < T_end; ++T) {
+            mbar_wait(smem_u32(&b_adone[T % NGBUF]), par(T, T0, NGBUF));
+            const int64_t s_loc = T / S_n;
+            if (s_loc >= p.burn_in && (want_tr || want_red)) {
+                const unsigned char *tl = tile_of(T);
+                const int *hdr = reinterpret_cast<const int *>(tl);
+                const TileLayout L{hdr[0], hdr[1], R, ESZ};
+                const int *rs = reinterpret_cast<const int *>(tl + 32);
+                const bool live = (rs[R + r] & 2) && active;
+                const ZW<S> me = *reinterpret_cast<const ZW<S> *>(vals + (T % NRING) * BLK + roff + coff);
+                const S self = zwc_s(me.z, me.w);
+                st[(2 * L.P) * 32 + lane] = live ? self : zero_s<S>();      // diag
+                st[(2 * L.P + 1) * 32 + lane] = live ? self : zero_s<S>();  // pattern (i,i)
+                S qz = mul_s(lds_s<S>(tl + L.dsq() + (2 * R + r) * ESZ), me.z);
+                S qw = zero_s<S>();
+                for (int q = 0; q < L.P; ++q) {
+                    const unsigned char *pr = tl + L.part() + L.part_bytes() * (q * R + r);
+                    const int voff = reinterpret_cast<const int *>(pr)[0];
+                    const ZW<S> v = *reinterpret_cast<const ZW<S> *>(vals + voff + coff);
+                    st[(2 * q) * 32 + lane] = live ? zwc_s(me.z, v.w) : zero_s<S>();
+                    st[(2 * q + 1) * 32 + lane] = live ? zwc_s(v.z, me.w) : zero_s<S>();
+                    if (want_tr) {
+                        qz = add_s(qz, mul_s(lds_s<S>(pr + 16), v.z));
+                        qw = add_s(qw, mul_s(lds_s<S>(pr + 16 + ESZ), conj_s(v.w)));
+                    }
+                }
+                if (want_tr && live) tr = add_s(tr, add_s(zwc_s(qz, me.w), mul_s(me.z, qw)));
+                __syncwarp();
+                if (want_red) {
+                    // one task per (record, row slot, group part): sum the chains, one RMW/RED
+                    const int nt = (2 * L.P + 2) * R * gpr;
+                    for (int tk = lane; tk < nt; tk += 32) {
+                        const int q2 = tk / (R * gpr), rem = tk % (R * gpr);
+                        const int r2 = rem / gpr, g2 = rem % gpr;
+                        if (!(rs[R + r2] & 2)) continue;
+                        int slot;
+                        bool is_diag = false;
+                        if (q2 < 2 * L.P) {
+                            slot = reinterpret_cast<const int *>(tl + L.part() +
+                                                                 L.part_bytes() * ((q2 >> 1) * R + r2))[1 + (q2 & 1)];
+                        } else if (q2 == 2 * L.P) {
+                            slot = rs[2 * R + r2];
+                            is_diag = true;
+                        } else {
+                            slot = rs[3 * R + r2];
+                        }
+                        const int c0 = g2 * gse;
+                        if (slot < 0 || cb + c0 >= p.chains) continue;
+                        S sum = zero_s<S>();
+                        for (int cc = 0; cc < gse; ++cc) sum = add_s(sum, st[q2 * 32 + r2 * C + c0 + cc]);
+                        const int64_t grp = (cb + c0) / p.gs;
+                        double *dst = is_diag ? p.slot_diag + (grp * p.n + slot) * (ESZ / 8)
+                                              : p.slot_pat + (grp * p.pcount + slot) * (ESZ / 8);
+                        if (p.gs > C) atomic_add_to(dst, sum);
+                        else add_to(dst, sum);
+                    }
+                }
+                __syncwarp();
+            }
+            if (lane == 0) mbar_arrive(smem_u32(&b_ddone[T % NGBUF]));
+        }
+        if (want_tr) {
+            // trace: sum the lane registers over row slots and the chains of each group
+            __syncwarp();
+            st[lane] = active ? tr : zero_s<S>();
+            __syncwarp();
+            if (lane < gpr && cb + lane * gse < p.chains) {
                 S sum = zero_s<S>();
-                for (int cc = 0; cc < gse; ++cc)
-                    sum = add_s(sum, *reinterpret_cast<const S *>(stage + (q * 32 + r2 * C + c0 + cc) * ESZ));
-                const int64_t grp = (cb + c0) / p.gs;
-                double *dst = op == IT_DIAG ? p.slot_diag + (grp * p.n + w2.y) * (ESZ / 8)
-                                            : p.slot_pat + (grp * p.pcount + w2.y) * (ESZ / 8);
+                for (int r2 = 0; r2 < R; ++r2)
+                    for (int cc = 0; cc < gse; ++cc) sum = add_s(sum, st[r2 * C + lane * gse + cc]);
+                double *dst = p.slot_trace + (int64_t)((cb + lane * gse) / p.gs) * (ESZ / 8);
                 if (p.gs > C) atomic_add_to(dst, sum);
                 else add_to(dst, sum);
             }
         }
-        __syncwarp();
-    }
-    // trace: sum the lane registers over row slots and the chains of each group
-    if (want_tr) {
-        __syncwarp();
-        *reinterpret_cast<S *>(stage + lane * ESZ) = active ? tr : zero_s<S>();
-        __syncwarp();
-        const int gse = p.gs < C ? p.gs : C;
-        const int ngrp = C / gse;
-        if (lane < ngrp && cb + lane * gse < p.chains) {
-            S sum = zero_s<S>();
-            for (int r2 = 0; r2 < R; ++r2)
-                for (int cc = 0; cc < gse; ++cc)
-                    sum = add_s(sum, *reinterpret_cast<const S *>(stage + (r2 * C + lane * gse + cc) * ESZ));
-            double *dst = p.slot_trace + (int64_t)((cb + lane * gse) / p.gs) * (ESZ / 8);
-            if (p.gs > C) atomic_add_to(dst, sum);
-            else add_to(dst, sum);
+    } else {
+        // ================= N: noise, steps T0 + w, T0 + w + NW, ...
+        const int w = warp - 3;
+        for (int64_t T = T0 + w; T < T_end; T += NW) {
+            if (T - NQ >= T0) mbar_wait(smem_u32(&b_nempty[T % NQ]), par(T - NQ, T0, NQ));
+            mbar_wait(smem_u32(&b_tile[T % NTILE]), par(T, T0, NTILE));
+            const int *rs = reinterpret_cast<const int *>(tile_of(T) + 32);
+            double phi = 0.0;
+            if (rs[R + r] & 2) {
+                if (p.noise == 0)
+                    phi = gaussian(static_cast<uint32_t>(rs[r]), p.sweep_abs0 + static_cast<uint32_t>(T / S_n), gchain,
+                                   p.key0, p.key1);
+                else
+                    phi = p.noise == 2 ? 1.0 : 0.0;
+            }
+            noise[(T % NQ) * 32 + lane] = phi;
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(&b_nfull[T % NQ]));
         }
     }
 }
 
 template <typename S>
-size_t sweep2_smem(int tile_slot, int max_items) {
-    constexpr int BLK = 32 * 2 * sizeof(S);
-    const size_t vals = (size_t)(NRING + NRING * KCAP + 1) * BLK;
-    const int mi = max_items > 1 ? max_items : 1;
-    return vals + (size_t)NTILE * tile_slot + (size_t)mi * 32 * sizeof(S) + NTILE * 8;
+size_t sweep2_smem(int tile_slot, int max_parts) {
+    constexpr int ESZ = sizeof(S);
+    const size_t stage = (size_t)(2 * max_parts + 2) * 32 * ESZ;
+    const size_t nbars = NTILE + 3 * NGBUF + 2 * NQ;
+    return (size_t)ValueArea<ESZ>::BYTES + (size_t)NTILE * tile_slot + NQ * 32 * 8 + stage + nbars * 8;
 }
 
-template <typename S, int C, int R>
+template <typename S, int C, int R, int NW>
 static cudaError_t launch2(const Sweep2Params<S> &p, cudaStream_t st) {
     const size_t smem = sweep2_smem<S>(p.tile_slot, p.max_items);
-    cudaError_t e = cudaFuncSetAttribute(sweep2_kernel<S, C, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e =
+        cudaFuncSetAttribute(sweep2_kernel<S, C, R, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    const int blocks = p.ld / C;
-    sweep2_kernel<S, C, R><<<blocks, 32, smem, st>>>(p);
+    sweep2_kernel<S, C, R, NW><<<p.ld / C, 32 * (3 + NW), smem, st>>>(p);
     return cudaGetLastError();
 }
 
 template <typename S>
 cudaError_t launch_sweep2(const Sweep2Params<S> &p, int C, cudaStream_t st) {
     switch (C) {
-        case 8: return launch2<S, 8, 4>(p, st);
-        case 16: return launch2<S, 16, 2>(p, st);
-        default: return launch2<S, 32, 1>(p, st);
+        case 8: return launch2<S, 8, 4, 2>(p, st);
+        case 16: return launch2<S, 16, 2, 2>(p, st);
+        default: return launch2<S, 32, 1, 2>(p, st);
     }
 }
 

@@ -1,10 +1,11 @@
 """CPU check of the v2 step planner (plan.cu) without a GPU.
 
 ``mcinv_debug_plan`` returns the record tiles the sweep2 kernel consumes. This
-test executes them with a numpy model of the kernel's data flow -- the same
-prefetch timing (gathers for step T+7 read the HBM state at iteration T),
-the 8-step ring of recent results, the gather buffer, the items -- and
-compares the resulting z, w and accumulators with the oracle. A planner bug
+test executes them with a numpy model of the kernel's data flow -- the warp
+roles A (update), B (gathers), D (accumulation) advancing under the kernel's
+mbarrier rules, in both extreme interleavings, the 16-step result ring, the
+8-step gather buffer, the partner records -- and compares the resulting z, w
+and accumulators with the oracle. A planner bug
 (a row scheduled before a lower neighbour, a stale far read, a wrong ring
 slot or item partner) shows up as an O(1) mismatch; rounding differences
 (no fma in numpy) stay below 1e-12.
@@ -14,7 +15,7 @@ import pytest
 
 import workloads as W
 
-KCAP, PDIST, NRING = 8, 7, 8
+KCAP, PDIST, NGBUF, NRING = 8, 7, 8, 16
 
 
 def r16(x):
@@ -22,29 +23,37 @@ def r16(x):
 
 
 class Tile:
+    """Parse one record tile (layout: plan.h TileLayout)."""
+
     def __init__(self, buf, off, R, esz):
-        self.K, self.I = (int(v) for v in np.frombuffer(buf, np.int32, 2, off))
-        self.rows = np.frombuffer(buf, np.int32, R, off + 32)
-        self.flags = np.frombuffer(buf, np.int32, R, off + 32 + 4 * R)
-        dsig = off + 32 + r16(8 * R)
         ct = np.complex128 if esz == 16 else np.float64
-        self.delta = np.frombuffer(buf, ct, R, dsig)
-        self.sigma = np.frombuffer(buf, ct, R, dsig + R * esz)
-        meta = dsig + r16(2 * R * esz)
+        self.K, self.P, _, self.has_q = (int(v) for v in np.frombuffer(buf, np.int32, 4, off))
+        rs = np.frombuffer(buf, np.int32, 4 * R, off + 32)
+        self.rows, self.flags, self.dslot, self.pslot = rs[:R], rs[R:2 * R], rs[2 * R:3 * R], rs[3 * R:]
+        dsq = off + 32 + r16(16 * R)
+        v = np.frombuffer(buf, ct, 3 * R, dsq)
+        self.delta, self.sigma, self.qself = v[:R], v[R:2 * R], v[2 * R:]
+        meta = dsq + r16(3 * R * esz)
         self.meta = np.frombuffer(buf, np.int32, 2 * self.K * R, meta).reshape(self.K, R, 2)
         coef = meta + r16(8 * self.K * R)
         self.coef = np.frombuffer(buf, ct, 2 * self.K * R, coef).reshape(self.K, R, 2)
-        items = coef + r16(2 * esz * self.K * R)
-        raw = np.frombuffer(buf, np.uint8, 32 * self.I * R, items).reshape(self.I, R, 32)
-        self.icode = raw[:, :, 0:4].copy().view(np.int32)[:, :, 0]
-        self.islot = raw[:, :, 4:8].copy().view(np.int32)[:, :, 0]
-        self.iprow = raw[:, :, 8:12].copy().view(np.int32)[:, :, 0]
-        self.ivoff = raw[:, :, 12:16].copy().view(np.int32)[:, :, 0]
-        self.iq = raw[:, :, 16:16 + esz].copy().view(ct)[:, :, 0]
-        self.size = items + r16(32 * self.I * R) - off
+        part = coef + r16(2 * esz * self.K * R)
+        pb = 16 + 2 * esz
+        raw = np.frombuffer(buf, np.uint8, pb * self.P * R, part).reshape(self.P, R, pb)
+        ints = raw[:, :, :16].copy().view(np.int32)
+        self.voff, self.pzi, self.pzo = ints[:, :, 0], ints[:, :, 1], ints[:, :, 2]
+        qq = raw[:, :, 16:].copy().view(ct)
+        self.qr, self.qc = qq[:, :, 0], qq[:, :, 1]
+        self.size = part + r16(pb * self.P * R) - off
 
 
-def emulate(M, orc, c, C, outputs, q=None, pattern=None, seed=5, chain0=0, burn_in=2, cycles=3, gs=None):
+def emulate(M, orc, c, C, outputs, q=None, pattern=None, seed=5, chain0=0, burn_in=2, cycles=3, lazy_d=False):
+    """Numpy model of sweep2_kernel's data flow for one CTA (C chains).
+
+    Warp roles progress under the kernel's barrier rules: A(T) after B(T);
+    B(U) after A(U-8) and D(U-7); D(T) after A(T). ``lazy_d`` runs D as late
+    as those rules allow (maximal lag), otherwise D follows A immediately and
+    B prefetches as early as allowed."""
     R = 32 // C
     cplx = np.iscomplexobj(c.val)
     esz = 16 if cplx else 8
@@ -59,114 +68,128 @@ def emulate(M, orc, c, C, outputs, q=None, pattern=None, seed=5, chain0=0, burn_
     assert off == len(buf)
     n = c.n
     ct = np.complex128
-    BLK = R * C  # elements per block (z and w kept as separate arrays)
-    zbytes = 2 * esz
-    GB = NRING * 32 * zbytes
-    ZERO = GB + NRING * KCAP * 32 * zbytes
-    # value area modelled as a flat array of (z, w) pairs indexed by byte offset / zbytes
-    nslots = (ZERO + 32 * zbytes) // zbytes
-    vz = np.zeros(nslots, ct)
-    vw = np.zeros(nslots, ct)
+    zb = 2 * esz                 # bytes of one (z, w) pair
+    BLK = 32 * zb
+    nslot = (NRING + NGBUF * KCAP + 1) * BLK // zb
+    vz = np.zeros(nslot, ct)     # value area, indexed by byte offset / zb
+    vw = np.zeros(nslot, ct)
     st_z = np.zeros((n, C), ct)
     st_w = np.zeros((n, C), ct)
-    gs = gs or C
-    chains = np.arange(C)
-    diag = np.zeros((C, n), ct)
     npat = len(pattern[0]) if pattern is not None else c.nnz
+    diag = np.zeros((C, n), ct)
     pat = np.zeros((C, npat), ct)
     trace = np.zeros(C, ct)
-    total = burn_in + cycles
+    total = (burn_in + cycles) * S
 
-    def gather(T):
-        tl = tiles[T % S]
+    def ring_base(T, r):
+        return ((T % NRING) * BLK + r * C * zb) // zb
+
+    for qq in range(1, PDIST + 1):  # prologue: ring of the 7 steps before T0 = 0
+        tl = tiles[(-qq) % S]
+        for r in range(R):
+            if tl.rows[r] >= 0 and tl.flags[r] & 2:
+                b = ring_base(-qq, r)
+                vz[b:b + C] = st_z[tl.rows[r]]
+                vw[b:b + C] = st_w[tl.rows[r]]
+
+    acc_z = np.zeros((R, C), ct)
+    acc_w = np.zeros((R, C), ct)
+
+    def B(U):
+        tl = tiles[U % S]
         for k in range(tl.K):
             for r in range(R):
                 o, j = tl.meta[k, r]
                 if j >= 0:
-                    base = o // zbytes
-                    vz[base:base + C] = st_z[j]
-                    vw[base:base + C] = st_w[j]
+                    vz[o // zb:o // zb + C] = st_z[j]
+                    vw[o // zb:o // zb + C] = st_w[j]
 
-    for qq in range(1, PDIST + 1):  # prologue ring
-        T = -qq
+    def A(T):
         tl = tiles[T % S]
-        for r in range(R):
-            if tl.rows[r] >= 0 and tl.flags[r] & 2:
-                base = ((T % NRING) * 32 * zbytes + r * C * zbytes) // zbytes
-                vz[base:base + C] = st_z[tl.rows[r]]
-                vw[base:base + C] = st_w[tl.rows[r]]
-    for T in range(min(PDIST, total * S)):
-        gather(T)
-    acc_z = np.zeros((R, C), ct)
-    acc_w = np.zeros((R, C), ct)
-    for T in range(total * S):
-        if T + PDIST < total * S:
-            gather(T + PDIST)
-        tl = tiles[T % S]
-        s_loc = T // S
-        zi = np.zeros((R, C), ct)
-        wi = np.zeros((R, C), ct)
         for r in range(R):
             if tl.flags[r] & 1:
                 acc_z[r] = 0
                 acc_w[r] = 0
             for k in range(tl.K):
-                base = (tl.meta[k, r, 0] + r * 0) // zbytes
-                a, b = tl.coef[k, r]
-                acc_z[r] = acc_z[r] + a * vz[base:base + C]
-                acc_w[r] = acc_w[r] + b * vw[base:base + C]
+                b = tl.meta[k, r, 0] // zb
+                a_, b_ = tl.coef[k, r]
+                acc_z[r] = acc_z[r] + a_ * vz[b:b + C]
+                acc_w[r] = acc_w[r] + b_ * vw[b:b + C]
             if tl.flags[r] & 2:
                 i = tl.rows[r]
-                phi = np.array([orc.gaussian(seed, int(i), s_loc, chain0 + int(ch)) for ch in chains])
+                phi = np.array([orc.gaussian(seed, int(i), T // S, chain0 + ch) for ch in range(C)])
                 d, sg = tl.delta[r], tl.sigma[r]
-                zi[r] = -d * acc_z[r] + sg * phi
-                wi[r] = -np.conj(d) * acc_w[r] + np.conj(sg) * phi
-                st_z[i] = zi[r]
-                st_w[i] = wi[r]
-                base = ((T % NRING) * 32 * zbytes + r * C * zbytes) // zbytes
-                vz[base:base + C] = zi[r]
-                vw[base:base + C] = wi[r]
-        if s_loc >= burn_in:
-            for r in range(R):
-                if not tl.flags[r] & 2:
+                zi = -d * acc_z[r] + sg * phi
+                wi = -np.conj(d) * acc_w[r] + np.conj(sg) * phi
+                st_z[i] = zi
+                st_w[i] = wi
+                b = ring_base(T, r)
+                vz[b:b + C] = zi
+                vw[b:b + C] = wi
+
+    def D(T):
+        nonlocal trace
+        if T // S < burn_in:
+            return
+        tl = tiles[T % S]
+        for r in range(R):
+            if not tl.flags[r] & 2:
+                continue
+            b = ring_base(T, r)
+            zi, wi = vz[b:b + C].copy(), vw[b:b + C].copy()
+            if tl.dslot[r] >= 0:
+                diag[:, tl.dslot[r]] += zi * np.conj(wi)
+            if tl.pslot[r] >= 0:
+                pat[:, tl.pslot[r]] += zi * np.conj(wi)
+            qz = tl.qself[r] * zi
+            qw = np.zeros(C, ct)
+            for q_ in range(tl.P):
+                pb = tl.voff[q_, r] // zb
+                pz, pw = vz[pb:pb + C], vw[pb:pb + C]
+                if tl.pzi[q_, r] >= 0:
+                    pat[:, tl.pzi[q_, r]] += zi * np.conj(pw)
+                if tl.pzo[q_, r] >= 0:
+                    pat[:, tl.pzo[q_, r]] += pz * np.conj(wi)
+                qz = qz + tl.qr[q_, r] * pz
+                qw = qw + tl.qc[q_, r] * np.conj(pw)
+            trace += qz * np.conj(wi) + zi * qw
+
+    a_done = d_done = b_done = -1
+    while a_done < total - 1:
+        # B as far as the barrier rules allow (D run lazily on demand when lazy_d)
+        while b_done + 1 < total:
+            U = b_done + 1
+            if U - 8 > a_done:
+                break
+            if U - 7 > d_done:
+                if lazy_d and d_done < a_done:
+                    d_done += 1
+                    D(d_done)
                     continue
-                qz = np.zeros(C, ct)
-                qw = np.zeros(C, ct)
-                for qi in range(tl.I):
-                    op = tl.icode[qi, r] & 7
-                    if op == 0:
-                        continue
-                    if tl.icode[qi, r] & 8:
-                        base = tl.ivoff[qi, r] // zbytes
-                        pz, pw = vz[base:base + C], vw[base:base + C]
-                    elif tl.iprow[qi, r] >= 0:
-                        pz, pw = st_z[tl.iprow[qi, r]], st_w[tl.iprow[qi, r]]
-                    slot = tl.islot[qi, r]
-                    if op in (1, 4):
-                        prod = zi[r] * np.conj(wi[r])
-                    elif op == 2:
-                        prod = zi[r] * np.conj(pw)
-                    elif op == 3:
-                        prod = pz * np.conj(wi[r])
-                    elif op == 5:
-                        qz += tl.iq[qi, r] * pz
-                        continue
-                    elif op == 6:
-                        qz += tl.iq[qi, r] * zi[r]
-                        continue
-                    elif op == 7:
-                        qw += tl.iq[qi, r] * np.conj(pw)
-                        continue
-                    if op == 1:
-                        diag[:, slot] += prod
-                    else:
-                        pat[:, slot] += prod
-                trace += qz * np.conj(wi[r]) + zi[r] * qw
+                break
+            B(U)
+            b_done = U
+        assert b_done > a_done, "deadlock in the emulated schedule"
+        a_done += 1
+        A(a_done)
+        if not lazy_d:
+            while d_done < a_done:
+                d_done += 1
+                D(d_done)
+    while d_done < total - 1:
+        d_done += 1
+        D(d_done)
     return st_z.T, st_w.T, diag, pat, trace
 
 
 def _check(M, orc, c, C, outputs, q=None, pattern=None, burn_in=2, cycles=3):
-    zg, wg, dg, pg, tg = emulate(M, orc, c, C, outputs, q=q, pattern=pattern, burn_in=burn_in, cycles=cycles)
+    for lazy in (False, True):
+        _check1(M, orc, c, C, outputs, q, pattern, burn_in, cycles, lazy)
+
+
+def _check1(M, orc, c, C, outputs, q, pattern, burn_in, cycles, lazy):
+    zg, wg, dg, pg, tg = emulate(M, orc, c, C, outputs, q=q, pattern=pattern, burn_in=burn_in, cycles=cycles,
+                                 lazy_d=lazy)
     pat_o = pattern if pattern is not None else (np.repeat(np.arange(c.n), np.diff(c.row_ptr)).astype(np.int32),
                                                  c.col)
     r = orc.Matrix(c, q=q, pattern=pat_o).run(5, C, burn_in, cycles, outputs)
