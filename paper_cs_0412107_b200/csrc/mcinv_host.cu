@@ -553,8 +553,10 @@ mcinv_status run_typed(mcinv_ctx *ctx, const mcinv_run_args *a, const Layout &L,
     const int pref = kernel_pref();
     const int C = choose_C(L.ld);
     PlanDev *plan = pref == 1 ? nullptr : get_plan<S>(ctx, C, a->outputs);
-    const bool v2 = plan && plan->error.empty();
-    if (pref == 2 && !v2) return fail(ctx, MCINV_E_INVALID, "v2 kernel unavailable: " + plan->error);
+    const bool v2 = plan && plan->error.empty() &&
+                    (int64_t)plan->steps * (a->burn_in + a->cycles) < (int64_t(1) << 31);
+    if (pref == 2 && !v2)
+        return fail(ctx, MCINV_E_INVALID, "v2 kernel unavailable: " + (plan ? plan->error : std::string("forced v1")));
     ctx->last_kernel = v2 ? 2 : 1;
     ctx->last_C = v2 ? plan->C : 32;
     ctx->last_steps = v2 ? plan->steps : n;
@@ -893,7 +895,10 @@ mcinv_status mcinv_debug_plan(mcinv_dtype dtype, int64_t n, const int64_t *row_p
     }
     PlanDev *pd = dtype == MCINV_C128 ? get_plan<cd>(ctx, chains_per_warp, outputs)
                                       : get_plan<double>(ctx, chains_per_warp, outputs);
-    if (!pd->error.empty()) return fail(ctx, MCINV_E_INVALID, pd->error);
+    if (!pd->error.empty()) {
+        std::fprintf(stderr, "mcinv_debug_plan: %s\n", pd->error.c_str());
+        return MCINV_E_INVALID;
+    }
     const mcinv::HostPlan &hp = pd->stats;
     info[0] = hp.steps;
     info[1] = hp.tile_slot_bytes;
