@@ -2,10 +2,11 @@
 
 ``mcinv_debug_plan`` returns the record tiles the sweep2 kernel consumes. This
 test executes them with a numpy model of the kernel's data flow -- the warp
-roles A (update), B (gathers), D (accumulation) advancing under the kernel's
-mbarrier rules, in both extreme interleavings, the 16-step result ring, the
-8-step gather buffer, the partner records -- and compares the resulting z, w
-and accumulators with the oracle. A planner bug
+roles A (update), B (gathers), D (accumulation of A's staged values)
+advancing under the kernel's mbarrier rules, with the earliest and the latest
+producer schedule, the 16-step result ring, the 8-step gather buffer, the
+partner records -- and compares the resulting z, w and accumulators with the
+oracle. A planner bug
 (a row scheduled before a lower neighbour, a stale far read, a wrong ring
 slot or item partner) shows up as an O(1) mismatch; rounding differences
 (no fma in numpy) stay below 1e-12.
@@ -51,9 +52,8 @@ def emulate(M, orc, c, C, outputs, q=None, pattern=None, seed=5, chain0=0, burn_
     """Numpy model of sweep2_kernel's data flow for one CTA (C chains).
 
     Warp roles progress under the kernel's barrier rules: A(T) after B(T);
-    B(U) after A(U-8) and D(U-7); D(T) after A(T). ``lazy_d`` runs D as late
-    as those rules allow (maximal lag), otherwise D follows A immediately and
-    B prefetches as early as allowed."""
+    B(U) after A(U-8); D reduces what A staged at A(T). ``lazy_d`` selects
+    the latest producer schedule, otherwise B prefetches as early as allowed."""
     R = 32 // C
     cplx = np.iscomplexobj(c.val)
     esz = 16 if cplx else 8
@@ -154,31 +154,23 @@ def emulate(M, orc, c, C, outputs, q=None, pattern=None, seed=5, chain0=0, burn_
                 qw = qw + tl.qc[q_, r] * np.conj(pw)
             trace += qz * np.conj(wi) + zi * qw
 
-    a_done = d_done = b_done = -1
+    # A(T) needs B(T); B(U) needs A(U-8). D reduces the values A staged at A(T),
+    # so it runs right after A(T). ``lazy_d`` here selects the latest legal
+    # producer schedule (B(T) just before A(T)) instead of the earliest.
+    a_done = b_done = -1
     while a_done < total - 1:
-        # B as far as the barrier rules allow (D run lazily on demand when lazy_d)
-        while b_done + 1 < total:
-            U = b_done + 1
-            if U - 8 > a_done:
-                break
-            if U - 7 > d_done:
-                if lazy_d and d_done < a_done:
-                    d_done += 1
-                    D(d_done)
-                    continue
-                break
-            B(U)
-            b_done = U
-        assert b_done > a_done, "deadlock in the emulated schedule"
+        if lazy_d:
+            if b_done < a_done + 1:
+                b_done += 1
+                B(b_done)
+        else:
+            while b_done + 1 < total and b_done + 1 - 8 <= a_done:
+                b_done += 1
+                B(b_done)
+        assert b_done > a_done
         a_done += 1
         A(a_done)
-        if not lazy_d:
-            while d_done < a_done:
-                d_done += 1
-                D(d_done)
-    while d_done < total - 1:
-        d_done += 1
-        D(d_done)
+        D(a_done)
     return st_z.T, st_w.T, diag, pat, trace
 
 
