@@ -14,7 +14,7 @@
 //                 (cols, coefficients, smem source offsets, accumulation
 //                 records) and cp.async gathers of step U's far operands
 //                 (>= 8 steps old) from the [n][ld] state in HBM; waits only
-//                 for A (step U-8 done).
+//                 for A (step U-7 done).
 //   D  (ND warps) accumulation (sampling sweeps): A stages each finished
 //                 row's z_i, w_i and its partner values; D forms the diag and
 //                 pattern products (Eq. 1/C), sums them over the
@@ -192,7 +192,9 @@ __global__ void __launch_bounds__(32 * (2 + NW + ND)) sweep2_kernel(const Sweep2
                             b_tile + 8 * (T % NTILE));
             }
         for (uint32_t U = T0; U < T_end; ++U) {
-            if (U >= T0 + 8) mbar_wait(b_adone + 8 * (U % NGBUF), par<NGBUF>(U - 8, T0));
+            // gather slot U % 8 was used by step U-8 and, for partners of a
+            // row's previous segment, by step U-7: wait for A to finish U-7
+            if (U >= T0 + 7) mbar_wait(b_adone + 8 * ((U - 7) % NGBUF), par<NGBUF>(U - 7, T0));
             mbar_wait(b_tile + 8 * (U % NTILE), par<NTILE>(U, T0));
             const unsigned char *tl = tile_of(U);
             const int K = reinterpret_cast<const int *>(tl)[0];

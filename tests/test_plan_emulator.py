@@ -52,7 +52,7 @@ def emulate(M, orc, c, C, outputs, q=None, pattern=None, seed=5, chain0=0, burn_
     """Numpy model of sweep2_kernel's data flow for one CTA (C chains).
 
     Warp roles progress under the kernel's barrier rules: A(T) after B(T);
-    B(U) after A(U-8); D reduces what A staged at A(T). ``lazy_d`` selects
+    B(U) after A(U-7); D reduces what A staged at A(T). ``lazy_d`` selects
     the latest producer schedule, otherwise B prefetches as early as allowed."""
     R = 32 // C
     cplx = np.iscomplexobj(c.val)
@@ -154,7 +154,7 @@ def emulate(M, orc, c, C, outputs, q=None, pattern=None, seed=5, chain0=0, burn_
                 qw = qw + tl.qc[q_, r] * np.conj(pw)
             trace += qz * np.conj(wi) + zi * qw
 
-    # A(T) needs B(T); B(U) needs A(U-8). D reduces the values A staged at A(T),
+    # A(T) needs B(T); B(U) needs A(U-7). D reduces the values A staged at A(T),
     # so it runs right after A(T). ``lazy_d`` here selects the latest legal
     # producer schedule (B(T) just before A(T)) instead of the earliest.
     a_done = b_done = -1
@@ -164,7 +164,7 @@ def emulate(M, orc, c, C, outputs, q=None, pattern=None, seed=5, chain0=0, burn_
                 b_done += 1
                 B(b_done)
         else:
-            while b_done + 1 < total and b_done + 1 - 8 <= a_done:
+            while b_done + 1 < total and b_done + 1 - 7 <= a_done:
                 b_done += 1
                 B(b_done)
         assert b_done > a_done
