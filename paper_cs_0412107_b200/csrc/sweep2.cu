@@ -41,14 +41,29 @@ __device__ __forceinline__ uint32_t smem_u32(const void *p) {
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
 }
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+__device__ __forceinline__ uint32_t mbar_try(uint32_t bar, uint32_t parity) {
+    uint32_t ok;
     asm volatile(
-        "{\n\t.reg .pred p;\n"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra WAIT_%=;\n}" ::"r"(bar),
-        "r"(parity)
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
         : "memory");
+    return ok;
+}
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+// Blocking wait with a watchdog: a protocol bug traps after 20 s instead of
+// hanging the GPU.
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    if (mbar_try(bar, parity)) return;
+    const uint64_t t0 = globaltimer_ns();
+    while (!mbar_try(bar, parity))
+        if (globaltimer_ns() - t0 > 20000000000ull) __trap();
 }
 // non-blocking probe of a phase (result consumed later: hides the latency)
 __device__ __forceinline__ uint32_t mbar_test(uint32_t bar, uint32_t parity) {
@@ -142,6 +157,8 @@ __global__ void __launch_bounds__(32 * (2 + NW + ND)) sweep2_kernel(const Sweep2
     const int roff = r * C * ZWSZ;
     const uint32_t S_n = (uint32_t)p.steps;
     const uint32_t T0 = (uint32_t)p.s_begin * S_n, T_end = (uint32_t)p.s_end * S_n;
+    // first sampling step: the stage ring (A -> D) counts its phases from here
+    const uint32_t Ts = max(T0, (uint32_t)p.burn_in * S_n);
     const uint32_t tile_slot = (uint32_t)p.tile_slot;
     const bool want_tr = (p.outputs & OUT_TRACE) != 0;
     const bool want_red = (p.outputs & (OUT_DIAG | OUT_PATTERN)) != 0;
@@ -267,7 +284,7 @@ __global__ void __launch_bounds__(32 * (2 + NW + ND)) sweep2_kernel(const Sweep2
             ok_n = Tn < T_end ? mbar_test(b_nfull + 8 * (Tn % NQ), par<NQ>(Tn, T0)) : 1u;
             if (stage_on && sampling) {
                 // partner values and slot ids of the finished rows -> stage slot (D reduces)
-                if (!ok_s && T >= T0 + NSTG) mbar_wait(b_sempty + 8 * (T % NSTG), par<NSTG>(T - NSTG, T0));
+                if (!ok_s && T >= Ts + NSTG) mbar_wait(b_sempty + 8 * (T % NSTG), par<NSTG>(T - NSTG, Ts));
                 unsigned char *sg_ = stage0 + (T % NSTG) * stg_bytes;
                 int2 *ids = reinterpret_cast<int2 *>(sg_ + stage_ids_off()) + r;
                 unsigned char *sv = sg_ + stg_vals + lane * ZWSZ;
@@ -292,11 +309,10 @@ __global__ void __launch_bounds__(32 * (2 + NW + ND)) sweep2_kernel(const Sweep2
                 if (want_tr && live) tr = add_s(tr, add_s(zwc_s(qz, wi), mul_s(zi, qw)));
                 __syncwarp();
                 if (lane == 0) mbar_arrive(b_sfull + 8 * (T % NSTG));
-                ok_s = (Tn < T_end && Tn >= T0 + NSTG) ? mbar_test(b_sempty + 8 * (Tn % NSTG), par<NSTG>(Tn - NSTG, T0))
+                ok_s = (Tn < T_end && Tn >= Ts + NSTG) ? mbar_test(b_sempty + 8 * (Tn % NSTG), par<NSTG>(Tn - NSTG, Ts))
                                                        : 1u;
             } else {
                 __syncwarp();
-                if (stage_on && lane == 0) mbar_arrive(b_sfull + 8 * (T % NSTG));  // D skips burn-in steps
                 ok_s = 0;
             }
             if (lane == 0) {
@@ -322,9 +338,8 @@ __global__ void __launch_bounds__(32 * (2 + NW + ND)) sweep2_kernel(const Sweep2
             const int lg_tpr = 5 - lg_gse;          // tasks per (record, role): 32 / gse
             const int lg_gpr = __ffs(C / gse) - 1;  // group parts per row slot
             const bool use_atomic = p.gs > C || ND > 1;
-            for (uint32_t T = T0 + dw; T < T_end; T += ND) {
-                if ((int)(T / S_n) < p.burn_in) continue;  // A staged nothing
-                mbar_wait(b_sfull + 8 * (T % NSTG), par<NSTG>(T, T0));
+            for (uint32_t T = Ts + dw; T < T_end; T += ND) {
+                mbar_wait(b_sfull + 8 * (T % NSTG), par<NSTG>(T, Ts));
                 const unsigned char *sg_ = stage0 + (T % NSTG) * stg_bytes;
                 const int P = reinterpret_cast<const int *>(sg_)[0];
                 const int2 *ids = reinterpret_cast<const int2 *>(sg_ + stage_ids_off());
@@ -361,9 +376,8 @@ __global__ void __launch_bounds__(32 * (2 + NW + ND)) sweep2_kernel(const Sweep2
         } else if (want_tr) {
             // trace only: keep the stage ring turning
             const int dw = warp - WB - 1;
-            for (uint32_t T = T0 + dw; T < T_end; T += ND) {
-                if ((int)(T / S_n) < p.burn_in) continue;
-                mbar_wait(b_sfull + 8 * (T % NSTG), par<NSTG>(T, T0));
+            for (uint32_t T = Ts + dw; T < T_end; T += ND) {
+                mbar_wait(b_sfull + 8 * (T % NSTG), par<NSTG>(T, Ts));
                 __syncwarp();
                 if (lane == 0) mbar_arrive(b_sempty + 8 * (T % NSTG));
             }
