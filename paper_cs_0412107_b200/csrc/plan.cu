@@ -60,6 +60,7 @@ std::string build_plan(const PlanInput &in, int R, int C, HostPlan &out) {
     const int esz = cplx ? 16 : 8;
     const int zwsz = 2 * esz;
     const int BLK = 32 * zwsz;
+    const int NGBUF = ngbuf(esz), NRING = nring(esz);
     const int GB_OFF = NRING * BLK;
     const int ZERO_OFF = GB_OFF + NGBUF * KCAP * BLK;
     if (R * C != 32) return "R * C must be 32";

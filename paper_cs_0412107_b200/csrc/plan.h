@@ -27,10 +27,13 @@ namespace mcinv {
 
 constexpr int KCAP = 8;     // entries per row segment
 constexpr int PDIST = 7;    // near/far threshold (steps): far operands are >= 8 steps old
-constexpr int NGBUF = 8;    // gather-buffer step slots
-constexpr int NRING = 16;   // result-ring step slots (steps per sweep padded to a multiple)
 constexpr int NTILE = 16;   // record tile slots
 constexpr int MAXPART = 2 * KCAP;  // accumulation partners per row
+// Gather-buffer step slots (16 real, 8 complex: shared-memory budget) and
+// result-ring step slots (2 x gather slots; steps per sweep are padded to a
+// multiple). Deeper buffers let the accumulation warps lag the update warp.
+__host__ __device__ constexpr int ngbuf(int esz) { return esz == 8 ? 16 : 8; }
+__host__ __device__ constexpr int nring(int esz) { return 2 * ngbuf(esz); }
 
 struct PlanInput {
     int64_t n = 0;
@@ -49,7 +52,7 @@ struct PlanInput {
 
 struct HostPlan {
     int R = 1, C = 32;
-    int steps = 0;              // steps per sweep (padded to a multiple of NRING)
+    int steps = 0;              // steps per sweep (padded to a multiple of nring)
     int tile_slot_bytes = 0;    // max tile bytes (16-aligned)
     int max_parts = 0;          // max partner records per row slot in a step
     std::vector<unsigned char> tiles;   // concatenated tiles
@@ -86,9 +89,10 @@ struct TileLayout {
 // Shared-memory value area of the kernel (bytes): ring | gather buffer | zero block.
 template <int ESZ> struct ValueArea {
     static constexpr int BLK = 32 * 2 * ESZ;  // one step slot: R rows x C chains x (z, w)
+    static constexpr int NGB = ngbuf(ESZ), NRG = nring(ESZ);
     static constexpr int RING = 0;
-    static constexpr int GBUF = NRING * BLK;
-    static constexpr int ZERO = GBUF + NGBUF * KCAP * BLK;
+    static constexpr int GBUF = NRG * BLK;
+    static constexpr int ZERO = GBUF + NGB * KCAP * BLK;
     static constexpr int BYTES = ZERO + BLK;
 };
 

@@ -9,18 +9,20 @@
 // Warp roles (all synchronised with mbarriers, per step slot):
 //   A  (1 warp)   the serial part: for each step, the fma chains of
 //                 Eq. (4)/(5) over smem operands, z_i, w_i to HBM and to the
-//                 16-step result ring, FULL-output snapshots, staging.
+//                 result ring, FULL-output snapshots, D's records, trace.
 //   B  (1 warp)   producer: TMA bulk copy of the record tile of step U+8
 //                 (cols, coefficients, smem source offsets, accumulation
 //                 records) and cp.async gathers of step U's far operands
-//                 (>= 8 steps old) from the [n][ld] state in HBM; waits only
-//                 for A (step U-7 done).
-//   D  (ND warps) accumulation (sampling sweeps): A stages each finished
-//                 row's z_i, w_i and its partner values; D forms the diag and
-//                 pattern products (Eq. 1/C), sums them over the
+//                 (>= 8 steps old) from the [n][ld] state in HBM; waits for
+//                 A(U-8) and, for gather-slot reuse, D(U-NGB+1).
+//   D  (ND warps) accumulation (sampling sweeps): A hands each finished row's
+//                 accumulation records (value offsets, slots) to D through a
+//                 record ring; D forms the diag and pattern products (Eq. 1/C,
+//                 P:173-176) from the values in smem, sums them over the
 //                 chains of an SE group and does one RMW (or RED) per group
-//                 slot. The trace w^dagger Q z (Eq. tr) is summed
-//                 in A's registers.
+//                 slot. Deep gather/result buffers (16/32 steps for f64) let
+//                 D lag A. The trace w^dagger Q z (Eq. tr) is
+//                 summed in A's registers.
 //   N  (NW warps) noise: phi(row, sweep, chain) by Philox4x32-10 + Box-Muller
 //                 (noise.cuh) into an smem ring, round-robin over steps.
 // A and B are single warps; N and D are NW / ND warps taking steps in turn.
@@ -107,19 +109,14 @@ __device__ __forceinline__ uint32_t par(uint32_t T, uint32_t T0) {
 
 }  // namespace
 
-// Stage slot (A -> D): int P; int2 ids[P+1][R] ({pzi, pzo} per partner record,
-// {dslot, pslot} for the row itself at index P); ZW vals[P+1][32] (partner
-// values per lane, the row's own z_i, w_i at index P).
-__host__ __device__ constexpr int stage_ids_off() { return 16; }
+// Record-ring slot (A -> D), one per step: int P (header, 16 B), then
+// int4 rec[P+1][R]: {smem value offset, pzi, pzo, -} per partner record and,
+// at index P, {offset of the row's own z_i, w_i in the ring, dslot, pslot, -};
+// slots are -1 for row slots whose row did not finish in the step.
+__host__ __device__ inline int rec_slot_bytes(int max_parts, int R) { return 16 + 16 * (max_parts + 1) * R; }
+// D scratch: products [2 (P+1)][32] for the transpose reduction
 template <int ESZ>
-__host__ __device__ inline int stage_vals_off(int max_parts, int R) {
-    return (16 + 8 * (max_parts + 1) * R + 15) & ~15;
-}
-template <int ESZ>
-__host__ __device__ inline int stage_slot_bytes(int max_parts, int R) {
-    return stage_vals_off<ESZ>(max_parts, R) + (max_parts + 1) * 32 * 2 * ESZ;
-}
-constexpr int NSTG = 4;  // stage slots
+__host__ __device__ inline int dstage_bytes(int max_parts) { return 2 * (max_parts + 1) * 32 * ESZ; }
 
 // Warp roles: 0 = A; 1..NW = N; NW+1 = B; NW+2 .. NW+1+ND = D. Warps share an
 // SMSP by index mod 4, so A pairs with B and each D with a noise warp.
@@ -129,22 +126,23 @@ __global__ void __launch_bounds__(32 * (2 + NW + ND)) sweep2_kernel(const Sweep2
     constexpr int ZWSZ = 2 * ESZ;
     using VA = ValueArea<ESZ>;
     constexpr int BLK = VA::BLK;
+    constexpr int NGB = VA::NGB, NRG = VA::NRG;
     constexpr int WB = NW + 1;  // producer warp
 
     extern __shared__ __align__(128) unsigned char smem[];
     unsigned char *vals = smem;
     unsigned char *tiles = smem + VA::BYTES;
     double *noise = reinterpret_cast<double *>(tiles + NTILE * p.tile_slot);   // [NQ][32]
-    unsigned char *stage0 = reinterpret_cast<unsigned char *>(noise + NQ * 32);  // [NSTG] stage slots
-    const int stg_bytes = stage_slot_bytes<ESZ>(p.max_items, R);
-    const int stg_vals = stage_vals_off<ESZ>(p.max_items, R);
-    uint64_t *bars = reinterpret_cast<uint64_t *>(stage0 + (size_t)NSTG * stg_bytes);
+    unsigned char *recring = reinterpret_cast<unsigned char *>(noise + NQ * 32);  // [NGB] record slots
+    const int rec_bytes = rec_slot_bytes(p.max_items, R);
+    unsigned char *dstage0 = recring + (size_t)NGB * rec_bytes;
+    const int dst_bytes = dstage_bytes<ESZ>(p.max_items);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(dstage0 + (size_t)ND * dst_bytes);
     const uint32_t b_tile = smem_u32(bars);               // [NTILE] TMA complete_tx
-    const uint32_t b_gather = b_tile + 8 * NTILE;         // [NGBUF] 32 cp.async arrivals
-    const uint32_t b_adone = b_gather + 8 * NGBUF;        // [NGBUF] A finished step
-    const uint32_t b_sfull = b_adone + 8 * NGBUF;         // [NSTG] stage written
-    const uint32_t b_sempty = b_sfull + 8 * NSTG;         // [NSTG] stage reduced
-    const uint32_t b_nfull = b_sempty + 8 * NSTG;         // [NQ] noise ready
+    const uint32_t b_gather = b_tile + 8 * NTILE;         // [NGB] 32 cp.async arrivals
+    const uint32_t b_adone = b_gather + 8 * NGB;          // [NGB] A finished step
+    const uint32_t b_ddone = b_adone + 8 * NGB;           // [NGB] D finished (sampling) step
+    const uint32_t b_nfull = b_ddone + 8 * NGB;           // [NQ] noise ready
     const uint32_t b_nempty = b_nfull + 8 * NQ;           // [NQ] noise consumed
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -157,8 +155,8 @@ __global__ void __launch_bounds__(32 * (2 + NW + ND)) sweep2_kernel(const Sweep2
     const int roff = r * C * ZWSZ;
     const uint32_t S_n = (uint32_t)p.steps;
     const uint32_t T0 = (uint32_t)p.s_begin * S_n, T_end = (uint32_t)p.s_end * S_n;
-    // first sampling step: the stage ring (A -> D) counts its phases from here
-    const uint32_t Ts = max(T0, (uint32_t)p.burn_in * S_n);
+    // first sampling step: D and the d_done barriers count their phases from here
+    const uint32_t Ts = min(T_end, max(T0, (uint32_t)p.burn_in * S_n));
     const uint32_t tile_slot = (uint32_t)p.tile_slot;
     const bool want_tr = (p.outputs & OUT_TRACE) != 0;
     const bool want_red = (p.outputs & (OUT_DIAG | OUT_PATTERN)) != 0;
@@ -166,13 +164,10 @@ __global__ void __launch_bounds__(32 * (2 + NW + ND)) sweep2_kernel(const Sweep2
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < NTILE; ++s) mbar_init(b_tile + 8 * s, 1);
-        for (int s = 0; s < NGBUF; ++s) {
+        for (int s = 0; s < NGB; ++s) {
             mbar_init(b_gather + 8 * s, 32);
             mbar_init(b_adone + 8 * s, 1);
-        }
-        for (int s = 0; s < NSTG; ++s) {
-            mbar_init(b_sfull + 8 * s, 1);
-            mbar_init(b_sempty + 8 * s, 1);
+            mbar_init(b_ddone + 8 * s, ND > 0 ? 1 : 1);
         }
         for (int s = 0; s < NQ; ++s) {
             mbar_init(b_nfull + 8 * s, 1);
@@ -190,18 +185,19 @@ __global__ void __launch_bounds__(32 * (2 + NW + ND)) sweep2_kernel(const Sweep2
             const int *g = reinterpret_cast<const int *>(p.tiles + p.tile_off[t] + 32);
             const int row = g[r], flg = g[R + r];
             if (row >= 0 && (flg & 2))
-                *reinterpret_cast<ZW<S> *>(vals + (((T % NRING) + NRING) % NRING) * BLK + roff + coff) =
+                *reinterpret_cast<ZW<S> *>(vals + (((T % NRG) + NRG) % NRG) * BLK + roff + coff) =
                     p.zw[(int64_t)row * p.ld + chain];
         }
     }
     __syncthreads();
 
     if (warp == WB) {
-        // ================= B: tiles and gathers (waits only for A)
+        // ================= B: tiles and gathers
         const unsigned char *zw_chain = reinterpret_cast<const unsigned char *>(p.zw + chain);
         const int64_t row_bytes = (int64_t)p.ld * ZWSZ;
         const unsigned char *gtiles = p.tiles;
         const uint32_t vbase = smem_u32(vals) + coff;
+        const bool wait_d = want_red;  // D reads gather slots of steps T and T-1
         if (lane == 0)
             for (uint32_t T = T0; T < T0 + 8 && T < T_end; ++T) {
                 const int t = (int)(T % S_n);
@@ -209,9 +205,10 @@ __global__ void __launch_bounds__(32 * (2 + NW + ND)) sweep2_kernel(const Sweep2
                             b_tile + 8 * (T % NTILE));
             }
         for (uint32_t U = T0; U < T_end; ++U) {
-            // gather slot U % 8 was used by step U-8 and, for partners of a
-            // row's previous segment, by step U-7: wait for A to finish U-7
-            if (U >= T0 + 7) mbar_wait(b_adone + 8 * ((U - 7) % NGBUF), par<NGBUF>(U - 7, T0));
+            // far operands of step U were produced at steps <= U-8 (A done); the
+            // gather slot U % NGB was last read by A(U-NGB) and by D(U-NGB), D(U-NGB+1)
+            if (U >= T0 + 8) mbar_wait(b_adone + 8 * ((U - 8) % NGB), par<NGB>(U - 8, T0));
+            if (wait_d && U + 1 >= Ts + NGB) mbar_wait(b_ddone + 8 * ((U + 1 - NGB) % NGB), par<NGB>(U + 1 - NGB, Ts));
             mbar_wait(b_tile + 8 * (U % NTILE), par<NTILE>(U, T0));
             const unsigned char *tl = tile_of(U);
             const int K = reinterpret_cast<const int *>(tl)[0];
@@ -230,18 +227,17 @@ __global__ void __launch_bounds__(32 * (2 + NW + ND)) sweep2_kernel(const Sweep2
                     for (int h = 0; h < ZWSZ / 16; ++h) cp_async16(dst + 16 * h, src + 16 * h);
                 }
             }
-            cp_async_arrive(b_gather + 8 * (U % NGBUF));
+            cp_async_arrive(b_gather + 8 * (U % NGB));
         }
     } else if (warp == 0) {
-        // ================= A: the serial fma chains, then stage the row's accumulation operands
+        // ================= A: the serial fma chains
         S acc_z = zero_s<S>(), acc_w = zero_s<S>(), tr = zero_s<S>();
         ZW<S> *zw_chain = p.zw + chain;
         const unsigned char *vlane = vals + coff;
         unsigned char *ring_lane = vals + roff + coff;
-        const bool stage_on = want_red || want_tr;
-        uint32_t ok_g = 0, ok_n = 0, ok_s = 0;
+        uint32_t ok_g = 0, ok_n = 0;
         for (uint32_t T = T0; T < T_end; ++T) {
-            if (!ok_g) mbar_wait(b_gather + 8 * (T % NGBUF), par<NGBUF>(T, T0));
+            if (!ok_g) mbar_wait(b_gather + 8 * (T % NGB), par<NGB>(T, T0));
             const unsigned char *tl = tile_of(T);
             const int K = reinterpret_cast<const int *>(tl)[0];
             const int P = reinterpret_cast<const int *>(tl)[1];
@@ -258,14 +254,13 @@ __global__ void __launch_bounds__(32 * (2 + NW + ND)) sweep2_kernel(const Sweep2
                 acc_z = fma_s(lds_s<S>(cf + 2 * ESZ * R * k), v.z, acc_z);
                 acc_w = fma_s(lds_s<S>(cf + 2 * ESZ * R * k + ESZ), v.w, acc_w);
             }
-            // probe the next step's barriers while the fma chains drain
+            // probe the next step's gathers while the fma chains drain
             const uint32_t Tn = T + 1;
-            ok_g = Tn < T_end ? mbar_test(b_gather + 8 * (Tn % NGBUF), par<NGBUF>(Tn, T0)) : 1u;
+            ok_g = Tn < T_end ? mbar_test(b_gather + 8 * (Tn % NGB), par<NGB>(Tn, T0)) : 1u;
             if (!ok_n) mbar_wait(b_nfull + 8 * (T % NQ), par<NQ>(T, T0));
-            const uint32_t s_loc = T / S_n;
-            const bool sampling = (int)s_loc >= p.burn_in;
-            S zi = zero_s<S>(), wi = zero_s<S>();
             const bool last = (flags & 2) != 0;
+            const bool sampling = T >= Ts;
+            S zi = zero_s<S>(), wi = zero_s<S>();
             if (last) {
                 const int row = reinterpret_cast<const int *>(tl + 32)[r];
                 const double phi = noise[(T % NQ) * 32 + lane];
@@ -274,50 +269,46 @@ __global__ void __launch_bounds__(32 * (2 + NW + ND)) sweep2_kernel(const Sweep2
                 zi = fma_s(neg_s(dl), acc_z, scale_s(sg, phi));
                 wi = fma_s(neg_s(conj_s(dl)), acc_w, scale_s(conj_s(sg), phi));
                 zw_chain[(int64_t)row * p.ld] = ZW<S>{zi, wi};
-                *reinterpret_cast<ZW<S> *>(ring_lane + (T % NRING) * BLK) = ZW<S>{zi, wi};
+                *reinterpret_cast<ZW<S> *>(ring_lane + (T % NRG) * BLK) = ZW<S>{zi, wi};
                 if ((p.outputs & OUT_FULL) && sampling) {
-                    const int64_t t = (int64_t)s_loc - p.snap_s0;
+                    const int64_t t = (int64_t)(T / S_n) - p.snap_s0;
                     p.snap_x[(t * p.n + row) * p.ld + chain] = zi;
                     p.snap_y[(t * p.n + row) * p.ld + chain] = wi;
                 }
             }
             ok_n = Tn < T_end ? mbar_test(b_nfull + 8 * (Tn % NQ), par<NQ>(Tn, T0)) : 1u;
-            if (stage_on && sampling) {
-                // partner values and slot ids of the finished rows -> stage slot (D reduces)
-                if (!ok_s && T >= Ts + NSTG) mbar_wait(b_sempty + 8 * (T % NSTG), par<NSTG>(T - NSTG, Ts));
-                unsigned char *sg_ = stage0 + (T % NSTG) * stg_bytes;
-                int2 *ids = reinterpret_cast<int2 *>(sg_ + stage_ids_off()) + r;
-                unsigned char *sv = sg_ + stg_vals + lane * ZWSZ;
-                const int *rs = reinterpret_cast<const int *>(tl + 32);
-                const bool live = last && active;
-                S qz = mul_s(lds_s<S>(tl + L.dsq() + (2 * R + r) * ESZ), zi);
-                S qw = zero_s<S>();
+            if (sampling && (want_red || want_tr)) {
                 const unsigned char *pr = tl + L.part() + L.part_bytes() * r;
-                for (int q = 0; q < P; ++q, pr += L.part_bytes() * R) {
-                    const int4 rec = *reinterpret_cast<const int4 *>(pr);
-                    const ZW<S> v = *reinterpret_cast<const ZW<S> *>(vlane + rec.x);
-                    *reinterpret_cast<ZW<S> *>(sv + q * 32 * ZWSZ) = v;
-                    if (c == 0) ids[q * R] = last ? make_int2(rec.y, rec.z) : make_int2(-1, -1);
-                    if (want_tr) {
-                        qz = add_s(qz, mul_s(lds_s<S>(pr + 16), v.z));
-                        qw = add_s(qw, mul_s(lds_s<S>(pr + 16 + ESZ), conj_s(v.w)));
+                if (want_red && c == 0) {
+                    // hand the row's accumulation records to D (one lane per row slot)
+                    unsigned char *rs_ = recring + (T % NGB) * rec_bytes;
+                    int4 *rec = reinterpret_cast<int4 *>(rs_ + 16) + r;
+                    for (int q = 0; q < P; ++q) {
+                        int4 v = *reinterpret_cast<const int4 *>(pr + q * L.part_bytes() * R);
+                        if (!last) v.y = v.z = -1;
+                        rec[q * R] = v;
                     }
+                    const int *rs = reinterpret_cast<const int *>(tl + 32);
+                    rec[P * R] = last ? make_int4((int)((T % NRG) * BLK) + roff, rs[2 * R + r], rs[3 * R + r], 0)
+                                      : make_int4(0, -1, -1, 0);
+                    if (r == 0) reinterpret_cast<int *>(rs_)[0] = P;
                 }
-                *reinterpret_cast<ZW<S> *>(sv + P * 32 * ZWSZ) = ZW<S>{zi, wi};
-                if (c == 0) ids[P * R] = last ? make_int2(rs[2 * R + r], rs[3 * R + r]) : make_int2(-1, -1);
-                if (lane == 0) reinterpret_cast<int *>(sg_)[0] = P;
-                if (want_tr && live) tr = add_s(tr, add_s(zwc_s(qz, wi), mul_s(zi, qw)));
-                __syncwarp();
-                if (lane == 0) mbar_arrive(b_sfull + 8 * (T % NSTG));
-                ok_s = (Tn < T_end && Tn >= Ts + NSTG) ? mbar_test(b_sempty + 8 * (Tn % NSTG), par<NSTG>(Tn - NSTG, Ts))
-                                                       : 1u;
-            } else {
-                __syncwarp();
-                ok_s = 0;
+                if (want_tr && last) {
+                    S qz = mul_s(lds_s<S>(tl + L.dsq() + (2 * R + r) * ESZ), zi);
+                    S qw = zero_s<S>();
+                    for (int q = 0; q < P; ++q) {
+                        const unsigned char *pq = pr + q * L.part_bytes() * R;
+                        const ZW<S> v = *reinterpret_cast<const ZW<S> *>(vlane + reinterpret_cast<const int *>(pq)[0]);
+                        qz = add_s(qz, mul_s(lds_s<S>(pq + 16), v.z));
+                        qw = add_s(qw, mul_s(lds_s<S>(pq + 16 + ESZ), conj_s(v.w)));
+                    }
+                    if (active) tr = add_s(tr, add_s(zwc_s(qz, wi), mul_s(zi, qw)));
+                }
             }
+            __syncwarp();
             if (lane == 0) {
                 mbar_arrive(b_nempty + 8 * (T % NQ));
-                mbar_arrive(b_adone + 8 * (T % NGBUF));
+                mbar_arrive(b_adone + 8 * (T % NGB));
             }
         }
         if (want_tr) {
@@ -330,56 +321,56 @@ __global__ void __launch_bounds__(32 * (2 + NW + ND)) sweep2_kernel(const Sweep2
                 atomic_add_to(p.slot_trace + (int64_t)((cb + c) / p.gs) * (ESZ / 8), v);
         }
     } else if (warp > WB) {
-        // ================= D: group reductions of the staged products, steps T0 + dw, T0 + dw + ND, ...
+        // ================= D: diag / pattern products and group reductions,
+        // sampling steps Ts + dw, Ts + dw + ND, ...; reads values in place
         if (want_red) {
             const int dw = warp - WB - 1;
+            S *st = reinterpret_cast<S *>(dstage0 + (size_t)dw * dst_bytes);
             const int gse = p.gs < C ? p.gs : C;
             const int lg_gse = __ffs(gse) - 1;
-            const int lg_tpr = 5 - lg_gse;          // tasks per (record, role): 32 / gse
+            const int lg_tpr = 5 - lg_gse;          // tasks per product record: 32 / gse
             const int lg_gpr = __ffs(C / gse) - 1;  // group parts per row slot
             const bool use_atomic = p.gs > C || ND > 1;
+            const unsigned char *vlane = vals + coff;
             for (uint32_t T = Ts + dw; T < T_end; T += ND) {
-                mbar_wait(b_sfull + 8 * (T % NSTG), par<NSTG>(T, Ts));
-                const unsigned char *sg_ = stage0 + (T % NSTG) * stg_bytes;
-                const int P = reinterpret_cast<const int *>(sg_)[0];
-                const int2 *ids = reinterpret_cast<const int2 *>(sg_ + stage_ids_off());
-                const ZW<S> *sv = reinterpret_cast<const ZW<S> *>(sg_ + stg_vals);
-                // task = (record q, role h, row slot r2, group part g2)
+                mbar_wait(b_adone + 8 * (T % NGB), par<NGB>(T, T0));
+                const unsigned char *rs_ = recring + (T % NGB) * rec_bytes;
+                const int P = reinterpret_cast<const int *>(rs_)[0];
+                const int4 *rec = reinterpret_cast<const int4 *>(rs_ + 16);
+                const int4 self = rec[P * R + r];
+                const ZW<S> me = *reinterpret_cast<const ZW<S> *>(vlane + self.x);
+                const bool live = self.y >= 0 || self.z >= 0;
+                const S sp = (live && active) ? zwc_s(me.z, me.w) : zero_s<S>();
+                st[(2 * P) * 32 + lane] = sp;       // diag
+                st[(2 * P + 1) * 32 + lane] = sp;   // pattern (i,i)
+                for (int q = 0; q < P; ++q) {
+                    const int4 rc = rec[q * R + r];
+                    const ZW<S> v = *reinterpret_cast<const ZW<S> *>(vlane + rc.x);
+                    st[(2 * q) * 32 + lane] = zwc_s(me.z, v.w);
+                    st[(2 * q + 1) * 32 + lane] = zwc_s(v.z, me.w);
+                }
+                __syncwarp();
+                // task = (product record qh, row slot r2, group part g2): sum gse chains, one RMW/RED
                 const int nt = (2 * P + 2) << lg_tpr;
                 for (int tk = lane; tk < nt; tk += 32) {
                     const int qh = tk >> lg_tpr, rem = tk & ((1 << lg_tpr) - 1);
-                    const int q = qh >> 1, h = qh & 1;
                     const int r2 = rem >> lg_gpr, g2 = rem & ((1 << lg_gpr) - 1);
-                    const int2 id = ids[q * R + r2];
-                    const int slot = h ? id.y : id.x;
+                    const int4 rc = rec[(qh >> 1) * R + r2];
+                    const int slot = (qh & 1) ? rc.z : rc.y;
                     const int c0 = g2 << lg_gse;
                     if (slot < 0 || cb + c0 >= p.chains) continue;
-                    const ZW<S> *me = sv + P * 32 + r2 * C + c0;
-                    const ZW<S> *pv = sv + q * 32 + r2 * C + c0;
-                    S sum = zero_s<S>();
-                    if (q == P) {
-                        for (int cc = 0; cc < gse; ++cc) sum = add_s(sum, zwc_s(me[cc].z, me[cc].w));
-                    } else if (h == 0) {
-                        for (int cc = 0; cc < gse; ++cc) sum = add_s(sum, zwc_s(me[cc].z, pv[cc].w));
-                    } else {
-                        for (int cc = 0; cc < gse; ++cc) sum = add_s(sum, zwc_s(pv[cc].z, me[cc].w));
-                    }
-                    const bool to_diag = q == P && h == 0;
-                    double *dst = (to_diag ? p.slot_diag + (((int64_t)(cb + c0) / p.gs) * p.n + slot) * (ESZ / 8)
-                                           : p.slot_pat + (((int64_t)(cb + c0) / p.gs) * p.pcount + slot) * (ESZ / 8));
+                    const S *sv = st + qh * 32 + r2 * C + c0;
+                    S sum = sv[0];
+                    for (int cc = 1; cc < gse; ++cc) sum = add_s(sum, sv[cc]);
+                    const bool to_diag = qh == 2 * P;
+                    const int64_t grp = (cb + c0) / p.gs;
+                    double *dst = to_diag ? p.slot_diag + (grp * p.n + slot) * (ESZ / 8)
+                                          : p.slot_pat + (grp * p.pcount + slot) * (ESZ / 8);
                     if (use_atomic) atomic_add_to(dst, sum);
                     else add_to(dst, sum);
                 }
                 __syncwarp();
-                if (lane == 0) mbar_arrive(b_sempty + 8 * (T % NSTG));
-            }
-        } else if (want_tr) {
-            // trace only: keep the stage ring turning
-            const int dw = warp - WB - 1;
-            for (uint32_t T = Ts + dw; T < T_end; T += ND) {
-                mbar_wait(b_sfull + 8 * (T % NSTG), par<NSTG>(T, Ts));
-                __syncwarp();
-                if (lane == 0) mbar_arrive(b_sempty + 8 * (T % NSTG));
+                if (lane == 0) mbar_arrive(b_ddone + 8 * (T % NGB));
             }
         }
     } else {
@@ -408,10 +399,12 @@ constexpr int kNW = 3, kND = 2;  // noise and accumulation warps per CTA
 template <typename S>
 size_t sweep2_smem(int tile_slot, int max_parts) {
     constexpr int ESZ = sizeof(S);
-    // stage slots are sized for R = 4 (the largest id section)
-    const size_t stage = (size_t)NSTG * stage_slot_bytes<ESZ>(max_parts, 4);
-    const size_t nbars = NTILE + 2 * NGBUF + 2 * NSTG + 2 * NQ;
-    return (size_t)ValueArea<ESZ>::BYTES + (size_t)NTILE * tile_slot + NQ * 32 * 8 + stage + nbars * 8;
+    using VA = ValueArea<ESZ>;
+    // record slots are sized for R = 4 (the largest)
+    const size_t recs = (size_t)VA::NGB * rec_slot_bytes(max_parts, 4);
+    const size_t dst = (size_t)kND * dstage_bytes<ESZ>(max_parts);
+    const size_t nbars = NTILE + 3 * VA::NGB + 2 * NQ;
+    return (size_t)VA::BYTES + (size_t)NTILE * tile_slot + NQ * 32 * 8 + recs + dst + nbars * 8;
 }
 
 template <typename S, int C, int R>

@@ -2,11 +2,10 @@
 
 ``mcinv_debug_plan`` returns the record tiles the sweep2 kernel consumes. This
 test executes them with a numpy model of the kernel's data flow -- the warp
-roles A (update), B (gathers), D (accumulation of A's staged values)
-advancing under the kernel's mbarrier rules, with the earliest and the latest
-producer schedule, the 16-step result ring, the 8-step gather buffer, the
-partner records -- and compares the resulting z, w and accumulators with the
-oracle. A planner bug
+roles A (update), B (gathers), D (accumulation, reading values in place)
+advancing under the kernel's mbarrier rules in two extreme interleavings, the
+result ring, the gather buffer, the partner records -- and compares the
+resulting z, w and accumulators with the oracle. A planner bug
 (a row scheduled before a lower neighbour, a stale far read, a wrong ring
 slot or item partner) shows up as an O(1) mismatch; rounding differences
 (no fma in numpy) stay below 1e-12.
@@ -16,7 +15,11 @@ import pytest
 
 import workloads as W
 
-KCAP, PDIST, NGBUF, NRING = 8, 7, 8, 16
+KCAP, PDIST = 8, 7
+
+
+def ngbuf(esz):
+    return 16 if esz == 8 else 8
 
 
 def r16(x):
@@ -52,8 +55,8 @@ def emulate(M, orc, c, C, outputs, q=None, pattern=None, seed=5, chain0=0, burn_
     """Numpy model of sweep2_kernel's data flow for one CTA (C chains).
 
     Warp roles progress under the kernel's barrier rules: A(T) after B(T);
-    B(U) after A(U-7); D reduces what A staged at A(T). ``lazy_d`` selects
-    the latest producer schedule, otherwise B prefetches as early as allowed."""
+    B(U) after A(U-8) and D(U-NGBUF+1); D(T) after A(T), reading values in
+    place. ``lazy_d``: earliest producer, maximally lagging D."""
     R = 32 // C
     cplx = np.iscomplexobj(c.val)
     esz = 16 if cplx else 8
@@ -70,6 +73,8 @@ def emulate(M, orc, c, C, outputs, q=None, pattern=None, seed=5, chain0=0, burn_
     ct = np.complex128
     zb = 2 * esz                 # bytes of one (z, w) pair
     BLK = 32 * zb
+    NGBUF = ngbuf(esz)
+    NRING = 2 * NGBUF
     nslot = (NRING + NGBUF * KCAP + 1) * BLK // zb
     vz = np.zeros(nslot, ct)     # value area, indexed by byte offset / zb
     vw = np.zeros(nslot, ct)
@@ -154,23 +159,33 @@ def emulate(M, orc, c, C, outputs, q=None, pattern=None, seed=5, chain0=0, burn_
                 qw = qw + tl.qc[q_, r] * np.conj(pw)
             trace += qz * np.conj(wi) + zi * qw
 
-    # A(T) needs B(T); B(U) needs A(U-7). D reduces the values A staged at A(T),
-    # so it runs right after A(T). ``lazy_d`` here selects the latest legal
-    # producer schedule (B(T) just before A(T)) instead of the earliest.
-    a_done = b_done = -1
-    while a_done < total - 1:
-        if lazy_d:
-            if b_done < a_done + 1:
-                b_done += 1
-                B(b_done)
+    # A(T) needs B(T); B(U) needs A(U-8) and, once sampling, D(U-NGBUF+1);
+    # D(T) needs A(T). Mode ``lazy_d``: priority B > A > D (earliest producer,
+    # maximally lagging D); otherwise D > A > B (producer just in time).
+    Ts = burn_in * S
+    a = b = d = -1
+
+    def can_b():
+        U = b + 1
+        return U < total and U - 8 <= a and (U - NGBUF + 1 < Ts or U - NGBUF + 1 <= d)
+
+    while d < total - 1:
+        order = "BAD" if lazy_d else "DAB"
+        for role in order:
+            if role == "B" and can_b():
+                b += 1
+                B(b)
+                break
+            if role == "A" and a + 1 <= b:
+                a += 1
+                A(a)
+                break
+            if role == "D" and d + 1 <= a:
+                d += 1
+                D(d)
+                break
         else:
-            while b_done + 1 < total and b_done + 1 - 7 <= a_done:
-                b_done += 1
-                B(b_done)
-        assert b_done > a_done
-        a_done += 1
-        A(a_done)
-        D(a_done)
+            raise AssertionError("deadlock in the emulated schedule")
     return st_z.T, st_w.T, diag, pat, trace
 
 
