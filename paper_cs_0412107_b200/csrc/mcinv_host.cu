@@ -821,6 +821,15 @@ mcinv_status mcinv_result(mcinv_ctx *ctx, unsigned output, int64_t total_chains,
     double bad = 0.0;
     CK(cudaMemcpyAsync(&bad, mom + L.mom_count - 1, sizeof(double), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    if (ctx->last_kernel == 2) {
+        unsigned int dbg[6] = {0, 0, 0, 0, 0, 0};
+        if (mcinv::sweep2_debug(dbg)) {
+            std::fprintf(stderr,
+                         "mcinv: sweep2 protocol watchdog: block %u warp %u barrier +%u parity %u step %u\n",
+                         dbg[0], dbg[1], dbg[2] - dbg[5], dbg[3], dbg[4]);
+            return fail(ctx, MCINV_E_CUDA, "sweep kernel protocol watchdog fired", (int64_t)dbg[4]);
+        }
+    }
     if (bad > 0.0) return fail(ctx, MCINV_E_DIVERGED, "state non-finite or above 1e12", (int64_t)bad);
     return MCINV_OK;
 }

@@ -111,6 +111,7 @@ template <typename S>
 cudaError_t launch_sweep2(const Sweep2Params<S> &p, int C, cudaStream_t st);
 template <typename S>
 size_t sweep2_smem(int tile_slot, int max_items);
+int sweep2_debug(unsigned int *dbg);
 
 // A_g[i][j] += sum_{t < T, c in group g} X[t][i][c] conj(Y[t][j][c]).
 template <typename S>

@@ -59,13 +59,33 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
     return t;
 }
-// Blocking wait with a watchdog: a protocol bug traps after 20 s instead of
-// hanging the GPU.
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-    if (mbar_try(bar, parity)) return;
+// Protocol watchdog: a wait that does not complete in 20 s records who waited
+// (block, warp, barrier, parity, step) in g_sweep2_dbg, raises g_sweep2_abort
+// so that every other wait returns, and the kernel drains; the host reports
+// it as a divergence-style failure (mcinv_result) with the record on stderr.
+__device__ unsigned int g_sweep2_abort;
+__device__ unsigned int g_sweep2_dbg[8];
+
+__device__ __noinline__ void mbar_wait_slow(uint32_t bar, uint32_t parity, uint32_t tag) {
     const uint64_t t0 = globaltimer_ns();
-    while (!mbar_try(bar, parity))
-        if (globaltimer_ns() - t0 > 20000000000ull) __trap();
+    while (!mbar_try(bar, parity)) {
+        if (*reinterpret_cast<volatile unsigned int *>(&g_sweep2_abort)) return;
+        if (globaltimer_ns() - t0 > 20000000000ull) {
+            if (atomicCAS(&g_sweep2_abort, 0u, 1u) == 0u) {
+                g_sweep2_dbg[0] = blockIdx.x;
+                g_sweep2_dbg[1] = threadIdx.x >> 5;
+                g_sweep2_dbg[2] = bar;
+                g_sweep2_dbg[3] = parity;
+                g_sweep2_dbg[4] = tag;
+                __threadfence();
+            }
+            return;
+        }
+    }
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity, uint32_t tag = 0) {
+    if (mbar_try(bar, parity)) return;
+    mbar_wait_slow(bar, parity, tag);
 }
 // non-blocking probe of a phase (result consumed later: hides the latency)
 __device__ __forceinline__ uint32_t mbar_test(uint32_t bar, uint32_t parity) {
@@ -139,6 +159,7 @@ __global__ void __launch_bounds__(32 * (2 + NW + ND)) sweep2_kernel(const Sweep2
     const int dst_bytes = dstage_bytes<ESZ>(p.max_items);
     uint64_t *bars = reinterpret_cast<uint64_t *>(dstage0 + (size_t)ND * dst_bytes);
     const uint32_t b_tile = smem_u32(bars);               // [NTILE] TMA complete_tx
+    if (threadIdx.x == 0 && blockIdx.x == 0) g_sweep2_dbg[5] = b_tile;
     const uint32_t b_gather = b_tile + 8 * NTILE;         // [NGB] 32 cp.async arrivals
     const uint32_t b_adone = b_gather + 8 * NGB;          // [NGB] A finished step
     const uint32_t b_ddone = b_adone + 8 * NGB;           // [NGB] D finished (sampling) step
@@ -207,9 +228,9 @@ __global__ void __launch_bounds__(32 * (2 + NW + ND)) sweep2_kernel(const Sweep2
         for (uint32_t U = T0; U < T_end; ++U) {
             // far operands of step U were produced at steps <= U-8 (A done); the
             // gather slot U % NGB was last read by A(U-NGB) and by D(U-NGB), D(U-NGB+1)
-            if (U >= T0 + 8) mbar_wait(b_adone + 8 * ((U - 8) % NGB), par<NGB>(U - 8, T0));
-            if (wait_d && U + 1 >= Ts + NGB) mbar_wait(b_ddone + 8 * ((U + 1 - NGB) % NGB), par<NGB>(U + 1 - NGB, Ts));
-            mbar_wait(b_tile + 8 * (U % NTILE), par<NTILE>(U, T0));
+            if (U >= T0 + 8) mbar_wait(b_adone + 8 * ((U - 8) % NGB), par<NGB>(U - 8, T0), U);
+            if (wait_d && U + 1 >= Ts + NGB) mbar_wait(b_ddone + 8 * ((U + 1 - NGB) % NGB), par<NGB>(U + 1 - NGB, Ts), U);
+            mbar_wait(b_tile + 8 * (U % NTILE), par<NTILE>(U, T0), U);
             const unsigned char *tl = tile_of(U);
             const int K = reinterpret_cast<const int *>(tl)[0];
             if (lane == 0 && U + 8 < T_end) {
@@ -237,7 +258,7 @@ __global__ void __launch_bounds__(32 * (2 + NW + ND)) sweep2_kernel(const Sweep2
         unsigned char *ring_lane = vals + roff + coff;
         uint32_t ok_g = 0, ok_n = 0;
         for (uint32_t T = T0; T < T_end; ++T) {
-            if (!ok_g) mbar_wait(b_gather + 8 * (T % NGB), par<NGB>(T, T0));
+            if (!ok_g) mbar_wait(b_gather + 8 * (T % NGB), par<NGB>(T, T0), T);
             const unsigned char *tl = tile_of(T);
             const int K = reinterpret_cast<const int *>(tl)[0];
             const int P = reinterpret_cast<const int *>(tl)[1];
@@ -257,7 +278,7 @@ __global__ void __launch_bounds__(32 * (2 + NW + ND)) sweep2_kernel(const Sweep2
             // probe the next step's gathers while the fma chains drain
             const uint32_t Tn = T + 1;
             ok_g = Tn < T_end ? mbar_test(b_gather + 8 * (Tn % NGB), par<NGB>(Tn, T0)) : 1u;
-            if (!ok_n) mbar_wait(b_nfull + 8 * (T % NQ), par<NQ>(T, T0));
+            if (!ok_n) mbar_wait(b_nfull + 8 * (T % NQ), par<NQ>(T, T0), T);
             const bool last = (flags & 2) != 0;
             const bool sampling = T >= Ts;
             S zi = zero_s<S>(), wi = zero_s<S>();
@@ -333,7 +354,7 @@ __global__ void __launch_bounds__(32 * (2 + NW + ND)) sweep2_kernel(const Sweep2
             const bool use_atomic = p.gs > C || ND > 1;
             const unsigned char *vlane = vals + coff;
             for (uint32_t T = Ts + dw; T < T_end; T += ND) {
-                mbar_wait(b_adone + 8 * (T % NGB), par<NGB>(T, T0));
+                mbar_wait(b_adone + 8 * (T % NGB), par<NGB>(T, T0), T);
                 const unsigned char *rs_ = recring + (T % NGB) * rec_bytes;
                 const int P = reinterpret_cast<const int *>(rs_)[0];
                 const int4 *rec = reinterpret_cast<const int4 *>(rs_ + 16);
@@ -377,8 +398,8 @@ __global__ void __launch_bounds__(32 * (2 + NW + ND)) sweep2_kernel(const Sweep2
         // ================= N: noise, steps T0 + w, T0 + w + NW, ...
         const int w = warp - 1;
         for (uint32_t T = T0 + w; T < T_end; T += NW) {
-            if (T >= T0 + NQ) mbar_wait(b_nempty + 8 * (T % NQ), par<NQ>(T - NQ, T0));
-            mbar_wait(b_tile + 8 * (T % NTILE), par<NTILE>(T, T0));
+            if (T >= T0 + NQ) mbar_wait(b_nempty + 8 * (T % NQ), par<NQ>(T - NQ, T0), T);
+            mbar_wait(b_tile + 8 * (T % NTILE), par<NTILE>(T, T0), T);
             const int *rs = reinterpret_cast<const int *>(tile_of(T) + 32);
             double phi = 0.0;
             if (rs[R + r] & 2) {
@@ -411,6 +432,8 @@ template <typename S, int C, int R>
 static cudaError_t launch2(const Sweep2Params<S> &p, cudaStream_t st) {
     const size_t smem = sweep2_smem<S>(p.tile_slot, p.max_items);
     auto kern = sweep2_kernel<S, C, R, kNW, kND>;
+    const unsigned int zero = 0;
+    cudaMemcpyToSymbolAsync(g_sweep2_abort, &zero, sizeof(zero), 0, cudaMemcpyHostToDevice, st);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     kern<<<p.ld / C, 32 * (2 + kNW + kND), smem, st>>>(p);
@@ -424,6 +447,14 @@ cudaError_t launch_sweep2(const Sweep2Params<S> &p, int C, cudaStream_t st) {
         case 16: return launch2<S, 16, 2>(p, st);
         default: return launch2<S, 32, 1>(p, st);
     }
+}
+
+// 1 if a protocol watchdog fired since the last launch; dbg[6] receives the record
+int sweep2_debug(unsigned int *dbg) {
+    unsigned int a = 0;
+    cudaMemcpyFromSymbol(&a, g_sweep2_abort, sizeof(a));
+    if (dbg) cudaMemcpyFromSymbol(dbg, g_sweep2_dbg, 6 * sizeof(unsigned int));
+    return (int)a;
 }
 
 template cudaError_t launch_sweep2<double>(const Sweep2Params<double> &, int, cudaStream_t);
