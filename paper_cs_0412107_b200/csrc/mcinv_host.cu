@@ -822,11 +822,15 @@ mcinv_status mcinv_result(mcinv_ctx *ctx, unsigned output, int64_t total_chains,
     CK(cudaMemcpyAsync(&bad, mom + L.mom_count - 1, sizeof(double), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     if (ctx->last_kernel == 2) {
-        unsigned int dbg[6] = {0, 0, 0, 0, 0, 0};
+        unsigned int dbg[38] = {0};
         if (mcinv::sweep2_debug(dbg)) {
             std::fprintf(stderr,
                          "mcinv: sweep2 protocol watchdog: block %u warp %u barrier +%u parity %u step %u\n",
                          dbg[0], dbg[1], dbg[2] - dbg[5], dbg[3], dbg[4]);
+            for (int w = 0; w < 8; ++w)
+                if (dbg[6 + 4 * w + 3])
+                    std::fprintf(stderr, "mcinv:   warp %d waited on barrier +%u parity %u step %u\n", w,
+                                 dbg[6 + 4 * w] - dbg[5], dbg[6 + 4 * w + 1], dbg[6 + 4 * w + 2]);
             return fail(ctx, MCINV_E_CUDA, "sweep kernel protocol watchdog fired", (int64_t)dbg[4]);
         }
     }

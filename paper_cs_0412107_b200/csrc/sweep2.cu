@@ -65,11 +65,22 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
 // it as a divergence-style failure (mcinv_result) with the record on stderr.
 __device__ unsigned int g_sweep2_abort;
 __device__ unsigned int g_sweep2_dbg[8];
+__device__ unsigned int g_sweep2_warps[8][4];  // block dbg[0]: per warp {bar, parity, tag, 1}
 
 __device__ __noinline__ void mbar_wait_slow(uint32_t bar, uint32_t parity, uint32_t tag) {
     const uint64_t t0 = globaltimer_ns();
     while (!mbar_try(bar, parity)) {
-        if (*reinterpret_cast<volatile unsigned int *>(&g_sweep2_abort)) return;
+        if (*reinterpret_cast<volatile unsigned int *>(&g_sweep2_abort)) {
+            if (blockIdx.x == *reinterpret_cast<volatile unsigned int *>(&g_sweep2_dbg[0]) &&
+                (threadIdx.x & 31) == 0) {
+                const int w = (threadIdx.x >> 5) & 7;
+                g_sweep2_warps[w][0] = bar;
+                g_sweep2_warps[w][1] = parity;
+                g_sweep2_warps[w][2] = tag;
+                g_sweep2_warps[w][3] = 1;
+            }
+            return;
+        }
         if (globaltimer_ns() - t0 > 20000000000ull) {
             if (atomicCAS(&g_sweep2_abort, 0u, 1u) == 0u) {
                 g_sweep2_dbg[0] = blockIdx.x;
@@ -432,8 +443,10 @@ template <typename S, int C, int R>
 static cudaError_t launch2(const Sweep2Params<S> &p, cudaStream_t st) {
     const size_t smem = sweep2_smem<S>(p.tile_slot, p.max_items);
     auto kern = sweep2_kernel<S, C, R, kNW, kND>;
-    const unsigned int zero = 0;
-    cudaMemcpyToSymbolAsync(g_sweep2_abort, &zero, sizeof(zero), 0, cudaMemcpyHostToDevice, st);
+    static const unsigned int zeros[32] = {0};
+    cudaMemcpyToSymbolAsync(g_sweep2_abort, zeros, sizeof(unsigned int), 0, cudaMemcpyHostToDevice, st);
+    cudaMemcpyToSymbolAsync(g_sweep2_warps, zeros, sizeof(zeros), 0, cudaMemcpyHostToDevice, st);
+    cudaMemcpyToSymbolAsync(g_sweep2_dbg, zeros, 8 * sizeof(unsigned int), 0, cudaMemcpyHostToDevice, st);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     kern<<<p.ld / C, 32 * (2 + kNW + kND), smem, st>>>(p);
@@ -453,7 +466,10 @@ cudaError_t launch_sweep2(const Sweep2Params<S> &p, int C, cudaStream_t st) {
 int sweep2_debug(unsigned int *dbg) {
     unsigned int a = 0;
     cudaMemcpyFromSymbol(&a, g_sweep2_abort, sizeof(a));
-    if (dbg) cudaMemcpyFromSymbol(dbg, g_sweep2_dbg, 6 * sizeof(unsigned int));
+    if (dbg) {
+        cudaMemcpyFromSymbol(dbg, g_sweep2_dbg, 6 * sizeof(unsigned int));
+        cudaMemcpyFromSymbol(dbg + 6, g_sweep2_warps, 32 * sizeof(unsigned int));
+    }
     return (int)a;
 }
 
