@@ -364,8 +364,11 @@ __global__ void __launch_bounds__(32 * (2 + NW + ND)) sweep2_kernel(const Sweep2
             const int lg_gpr = __ffs(C / gse) - 1;  // group parts per row slot
             const bool use_atomic = p.gs > C || ND > 1;
             const unsigned char *vlane = vals + coff;
-            for (uint32_t T = Ts + dw; T < T_end; T += ND) {
+            // every step is waited in order (also in burn-in): a parity wait may
+            // only target the phase right after the last one observed
+            for (uint32_t T = T0 + dw; T < T_end; T += ND) {
                 mbar_wait(b_adone + 8 * (T % NGB), par<NGB>(T, T0), T);
+                if (T < Ts) continue;
                 const unsigned char *rs_ = recring + (T % NGB) * rec_bytes;
                 const int P = reinterpret_cast<const int *>(rs_)[0];
                 const int4 *rec = reinterpret_cast<const int4 *>(rs_ + 16);
