@@ -67,9 +67,24 @@ __device__ unsigned int g_sweep2_abort;
 __device__ unsigned int g_sweep2_dbg[8];
 __device__ unsigned int g_sweep2_warps[8][4];  // block dbg[0]: per warp {bar, parity, tag, 1}
 
+// suspend-hinted try_wait: the thread sleeps (up to ~1 us) instead of spinning
+__device__ __forceinline__ uint32_t mbar_try_sleep(uint32_t bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity), "r"(1000u)
+        : "memory");
+    return ok;
+}
+
 __device__ __noinline__ void mbar_wait_slow(uint32_t bar, uint32_t parity, uint32_t tag) {
     const uint64_t t0 = globaltimer_ns();
-    while (!mbar_try(bar, parity)) {
+    for (uint32_t it = 1;; ++it) {
+        if (mbar_try_sleep(bar, parity)) return;
+        if ((it & 255) != 0) continue;
         if (*reinterpret_cast<volatile unsigned int *>(&g_sweep2_abort)) {
             if (blockIdx.x == *reinterpret_cast<volatile unsigned int *>(&g_sweep2_dbg[0]) &&
                 (threadIdx.x & 31) == 0) {
@@ -98,6 +113,7 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity, uint32_
     if (mbar_try(bar, parity)) return;
     mbar_wait_slow(bar, parity, tag);
 }
+
 // non-blocking probe of a phase (result consumed later: hides the latency)
 __device__ __forceinline__ uint32_t mbar_test(uint32_t bar, uint32_t parity) {
     uint32_t ok;
@@ -148,6 +164,31 @@ __host__ __device__ inline int rec_slot_bytes(int max_parts, int R) { return 16 
 // D scratch: products [2 (P+1)][32] for the transpose reduction
 template <int ESZ>
 __host__ __device__ inline int dstage_bytes(int max_parts) { return 2 * (max_parts + 1) * 32 * ESZ; }
+
+// The serial part of Eq. (4)/(5) for one step: load all KU operands first
+// (entries k >= K read the zero block with coefficient 0, an exact no-op), then
+// the two fma chains in ascending CSR order (reading R10).
+template <typename S, int KU, int R>
+__device__ __forceinline__ void fma_chain(int K, const int2 *meta, const unsigned char *cf,
+                                          const unsigned char *vlane, const unsigned char *zero, S &acc_z,
+                                          S &acc_w) {
+    constexpr int ESZ = sizeof(S);
+    ZW<S> v[KU];
+    S a[KU], b[KU];
+#pragma unroll
+    for (int k = 0; k < KU; ++k) {
+        const bool in = k < K;
+        const unsigned char *src = in ? vlane + meta[k * R].x : zero;
+        v[k] = *reinterpret_cast<const ZW<S> *>(src);
+        a[k] = in ? *reinterpret_cast<const S *>(cf + 2 * ESZ * R * k) : zero_s<S>();
+        b[k] = in ? *reinterpret_cast<const S *>(cf + 2 * ESZ * R * k + ESZ) : zero_s<S>();
+    }
+#pragma unroll
+    for (int k = 0; k < KU; ++k) {
+        acc_z = fma_s(a[k], v[k].z, acc_z);
+        acc_w = fma_s(b[k], v[k].w, acc_w);
+    }
+}
 
 // Warp roles: 0 = A; 1..NW = N; NW+1 = B; NW+2 .. NW+1+ND = D. Warps share an
 // SMSP by index mod 4, so A pairs with B and each D with a noise warp.
@@ -281,11 +322,8 @@ __global__ void __launch_bounds__(32 * (2 + NW + ND)) sweep2_kernel(const Sweep2
             }
             const int2 *meta = reinterpret_cast<const int2 *>(tl + L.meta()) + r;
             const unsigned char *cf = tl + L.coef() + 2 * ESZ * r;
-            for (int k = 0; k < K; ++k) {
-                const ZW<S> v = *reinterpret_cast<const ZW<S> *>(vlane + meta[k * R].x);
-                acc_z = fma_s(lds_s<S>(cf + 2 * ESZ * R * k), v.z, acc_z);
-                acc_w = fma_s(lds_s<S>(cf + 2 * ESZ * R * k + ESZ), v.w, acc_w);
-            }
+            if (K <= 4) fma_chain<S, 4, R>(K, meta, cf, vlane, vals + VA::ZERO, acc_z, acc_w);
+            else fma_chain<S, KCAP, R>(K, meta, cf, vlane, vals + VA::ZERO, acc_z, acc_w);
             // probe the next step's gathers while the fma chains drain
             const uint32_t Tn = T + 1;
             ok_g = Tn < T_end ? mbar_test(b_gather + 8 * (Tn % NGB), par<NGB>(Tn, T0)) : 1u;
