@@ -151,10 +151,11 @@ mcinv_status mcinv_set_timing(mcinv_ctx *ctx, int enable);
 mcinv_status mcinv_stats(mcinv_ctx *ctx, int64_t *launches, double *sweep_ms, int64_t *sweep_launches,
                          double *contract_ms, int64_t *contract_launches);
 
-/* Which sweep kernel the last mcinv_run used: version 2 = step-scheduled
- * kernel (sweep2.cu) with chains_per_warp C and steps_per_sweep steps;
- * version 1 = row-by-row kernel (sweep.cu; used when the v2 plan does not fit
- * shared memory, or with MCINV_KERNEL=v1 in the environment). */
+/* Which sweep kernel the last mcinv_run used: version 3 = level-scheduled
+ * kernel (sweep3.cu, the default) with chains_per_warp = chains per CTA and
+ * steps_per_sweep = levels D; version 2 = step-scheduled kernel (sweep2.cu)
+ * with C chains per warp and that many steps; version 1 = row-by-row kernel
+ * (sweep.cu). MCINV_KERNEL=v1|v2|v3 in the environment forces one. */
 mcinv_status mcinv_kernel_info(const mcinv_ctx *ctx, int *version, int *chains_per_warp, int64_t *steps_per_sweep);
 
 /* ------------------------------------------------------------ test-only */
@@ -176,6 +177,15 @@ mcinv_status mcinv_debug_plan(mcinv_dtype dtype, int64_t n, const int64_t *row_p
                               const void *values, const int64_t *q_row_ptr, const int32_t *q_col_idx,
                               const void *q_values, int64_t pcount, const int32_t *p_rows, const int32_t *p_cols,
                               unsigned outputs, int chains_per_warp, void *tiles, size_t capacity, int64_t *info);
+/* Host-only (no GPU needed): mcinv_create's preprocessing and the level
+ * planner of the v3 sweep kernel for C, with the
+ * default pattern and an optional Q, for the accumulation of `outputs`.
+ * level[n] (may be NULL) receives lev(i); info[6] = {levels D, max items of a
+ * phase, fused pattern pairs, deferred pattern pairs, trace items, union
+ * entries}. For CPU tests of the planner. */
+mcinv_status mcinv_debug_levels(mcinv_dtype dtype, int64_t n, const int64_t *row_ptr, const int32_t *col_idx,
+                                const void *values, const int64_t *q_row_ptr, const int32_t *q_col_idx,
+                                const void *q_values, unsigned outputs, int32_t *level, int64_t *info);
 /* Copy the state of chains [chain_begin, chain_begin+chains) (relative to the
  * last run's chain_begin) to host arrays z, w of shape [chains][n] (x2 doubles
  * for C128). Synchronizes. */

@@ -75,6 +75,8 @@ SYMBOLS = {
     "mcinv_debug_plan": (ctypes.c_int, [ctypes.c_int, ctypes.c_int64] + [ctypes.c_void_p] * 6 +
                          [ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint, ctypes.c_int,
                           ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
+    "mcinv_debug_levels": (ctypes.c_int, [ctypes.c_int, ctypes.c_int64] + [ctypes.c_void_p] * 6 +
+                           [ctypes.c_uint, ctypes.c_void_p, ctypes.c_void_p]),
     "mcinv_debug_get_state": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p,
                                              ctypes.c_void_p]),
     "mcinv_debug_set_state": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p,
@@ -160,6 +162,30 @@ def debug_plan(csr, chains_per_warp: int, outputs=("diag",), q=None, pattern=Non
     _check(L.mcinv_debug_plan(*args, bits, chains_per_warp, buf.ctypes.data, buf.size, info.ctypes.data))
     names = ["steps", "tile_slot", "max_items", "bytes", "segments", "entries", "near", "items"]
     return buf, dict(zip(names, (int(x) for x in info)))
+
+
+def debug_levels(csr, outputs=("diag",), q=None):
+    """Host-only v3 level schedule (no GPU): (lev[n], info dict). For CPU tests."""
+    cplx = np.iscomplexobj(csr.val)
+    rp = np.ascontiguousarray(csr.row_ptr, np.int64)
+    col = np.ascontiguousarray(csr.col, np.int32)
+    val = _doubles(csr.val, cplx)
+    args = [C128 if cplx else F64, csr.n, rp.ctypes.data, col.ctypes.data, val.ctypes.data]
+    keep = [rp, col, val]
+    if q is not None:
+        qa = [np.ascontiguousarray(q.row_ptr, np.int64), np.ascontiguousarray(q.col, np.int32), _doubles(q.val, cplx)]
+        keep += qa
+        args += [a.ctypes.data for a in qa]
+    else:
+        args += [None, None, None]
+    bits = 0
+    for o in outputs:
+        bits |= OUTPUTS[o]
+    lev = np.zeros(csr.n, np.int32)
+    info = np.zeros(6, np.int64)
+    _check(load().mcinv_debug_levels(*args, bits, lev.ctypes.data, info.ctypes.data))
+    names = ["levels", "max_items", "fused_pairs", "deferred_pairs", "trace_items", "entries"]
+    return lev, dict(zip(names, (int(x) for x in info)))
 
 
 class Inverter:

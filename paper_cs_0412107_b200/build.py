@@ -15,8 +15,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libmcinv.so")
-SOURCES = ["mcinv_host.cu", "plan.cu", "sweep.cu", "sweep2.cu", "contract.cu", "reduce.cu"]
-HEADERS = ["mcinv_internal.cuh", "noise.cuh", "scalar.cuh", "plan.h"]
+SOURCES = ["mcinv_host.cu", "levels.cu", "plan.cu", "sweep.cu", "sweep2.cu", "sweep3.cu", "contract.cu", "reduce.cu"]
+HEADERS = ["mcinv_internal.cuh", "noise.cuh", "scalar.cuh", "plan.h", "levels.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "--fmad=false", "-Xcompiler", "-fPIC,-O2",

@@ -1,0 +1,167 @@
+// levels.cu -- host planner of the level schedule (levels.h). Host code only.
+#include <algorithm>
+#include <unordered_map>
+
+#include "levels.h"
+
+namespace mcinv {
+
+namespace {
+
+// stable counting sort of items by key in [0, nkeys): returns the permutation
+// and fills ptr[nkeys + 1]
+std::vector<int> bucket(const std::vector<int> &key, int nkeys, std::vector<int> &ptr) {
+    ptr.assign(nkeys + 1, 0);
+    for (int k : key) ptr[k + 1]++;
+    for (int k = 0; k < nkeys; ++k) ptr[k + 1] += ptr[k];
+    std::vector<int> fill(ptr.begin(), ptr.end() - 1), perm(key.size());
+    for (size_t t = 0; t < key.size(); ++t) perm[fill[key[t]]++] = (int)t;
+    return perm;
+}
+
+}  // namespace
+
+std::string build_levels(const LevelInput &in, LevelPlan &P) {
+    const int64_t n = in.n;
+    const auto &up = *in.u_ptr;
+    const auto &uc = *in.u_col;
+    if ((int64_t)up.size() != n + 1) return "union lists missing";
+
+    // lev(i) = 1 + max lev(j) over lower neighbours j < i (rows ascend, so
+    // every lower neighbour is already levelled)
+    P.level.assign(n, 0);
+    int D = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        int l = 0;
+        for (int e = up[i]; e < up[i + 1]; ++e) {
+            const int j = uc[e];
+            if (j < i) l = std::max(l, P.level[j] + 1);
+        }
+        P.level[i] = l;
+        D = std::max(D, l + 1);
+    }
+    P.D = D;
+    const int nph = D + 1;
+
+    // rows in level order (ascending i within a level)
+    std::vector<int> key(P.level.begin(), P.level.end());
+    P.ord_row = bucket(key, nph, P.ph_row);
+    P.ph_row.push_back(P.ph_row.back());  // [D+2]; phase D holds no rows
+
+    // pattern slots: fused at the update of max(i, j) when min(i, j) is a lower
+    // neighbour (or i == j); the first occurrence of a pair is fused, the rest
+    // (duplicates, non-neighbour pairs) are deferred
+    std::unordered_map<uint64_t, int> first;
+    std::vector<char> used;
+    const auto pk = [](int64_t a, int64_t b) { return (uint64_t)a << 32 | (uint64_t)(uint32_t)b; };
+    const int64_t pc = in.want_pattern ? (int64_t)in.p_row->size() : 0;
+    if (pc > 0) {
+        first.reserve((size_t)pc * 2);
+        used.assign(pc, 0);
+        for (int64_t p = 0; p < pc; ++p) first.emplace(pk((*in.p_row)[p], (*in.p_col)[p]), (int)p);
+    }
+    const auto take = [&](int64_t a, int64_t b) -> int {
+        if (pc == 0) return -1;
+        auto it = first.find(pk(a, b));
+        if (it == first.end() || used[it->second]) return -1;
+        used[it->second] = 1;
+        return it->second;
+    };
+
+    P.ord_eptr.assign(n + 1, 0);
+    P.ord_dl.resize(n);
+    P.ord_sg.resize(n);
+    P.ord_pself.assign(n, -1);
+    P.ent_col.clear();
+    P.ent_a.clear();
+    P.ent_b.clear();
+    P.ent_pz.clear();
+    P.ent_col.reserve(uc.size());
+    P.fused_pairs = 0;
+    for (int64_t o = 0; o < n; ++o) {
+        const int i = P.ord_row[o];
+        for (int e = up[i]; e < up[i + 1]; ++e) {
+            const int j = uc[e];
+            P.ent_col.push_back(j);
+            P.ent_a.push_back((*in.u_a)[e]);
+            P.ent_b.push_back((*in.u_b)[e]);
+            if (in.want_pattern) {
+                const int zx = j < i ? take(i, j) : -1;  // z_i conj(w_j)
+                const int zy = j < i ? take(j, i) : -1;  // z_j conj(w_i)
+                P.fused_pairs += (zx >= 0) + (zy >= 0);
+                P.ent_pz.push_back(zx);
+                P.ent_pz.push_back(zy);
+            }
+        }
+        P.ord_eptr[o + 1] = (int)P.ent_col.size();
+        P.ord_dl[o] = (*in.delta)[i];
+        P.ord_sg[o] = (*in.sigma)[i];
+        if (in.want_pattern) {
+            P.ord_pself[o] = take(i, i);
+            P.fused_pairs += P.ord_pself[o] >= 0;
+        }
+    }
+
+    // deferred pattern pairs
+    P.pp_i.clear();
+    P.pp_j.clear();
+    P.pp_slot.clear();
+    {
+        std::vector<int> pkey, pidx;
+        for (int64_t p = 0; p < pc; ++p) {
+            if (used[p]) continue;
+            const int a = (*in.p_row)[p], b = (*in.p_col)[p];
+            pkey.push_back(std::max(P.level[a], P.level[b]) + 1);
+            pidx.push_back((int)p);
+        }
+        const std::vector<int> perm = bucket(pkey, nph, P.ph_pp);
+        P.ph_pp.push_back(P.ph_pp.back());
+        for (int t : perm) {
+            const int p = pidx[t];
+            P.pp_i.push_back((*in.p_row)[p]);
+            P.pp_j.push_back((*in.p_col)[p]);
+            P.pp_slot.push_back(p);
+        }
+        P.deferred_pairs = (int64_t)pidx.size();
+    }
+
+    // deferred trace items: Q row i -> conj(w_i) sum_j Q_ij z_j
+    P.tq_row.clear();
+    P.tq_eptr.assign(1, 0);
+    P.tq_col.clear();
+    P.tq_val.clear();
+    {
+        std::vector<int> tkey, trow;
+        if (in.want_trace) {
+            const auto &qp = *in.q_ptr;
+            const auto &qc = *in.q_col;
+            for (int64_t i = 0; i < n; ++i) {
+                if (qp[i + 1] == qp[i]) continue;
+                int l = P.level[i];
+                for (int64_t e = qp[i]; e < qp[i + 1]; ++e) l = std::max(l, P.level[qc[e]]);
+                tkey.push_back(l + 1);
+                trow.push_back((int)i);
+            }
+        }
+        const std::vector<int> perm = bucket(tkey, nph, P.ph_tq);
+        P.ph_tq.push_back(P.ph_tq.back());
+        for (int t : perm) {
+            const int i = trow[t];
+            P.tq_row.push_back(i);
+            for (int64_t e = (*in.q_ptr)[i]; e < (*in.q_ptr)[i + 1]; ++e) {
+                P.tq_col.push_back((*in.q_col)[e]);
+                P.tq_val.push_back((*in.q_val)[e]);
+            }
+            P.tq_eptr.push_back((int)P.tq_col.size());
+        }
+    }
+
+    P.max_rows = 0;
+    for (int p = 0; p < nph; ++p) {
+        const int w = (P.ph_row[p + 1] - P.ph_row[p]) + (P.ph_tq[p + 1] - P.ph_tq[p]) + (P.ph_pp[p + 1] - P.ph_pp[p]);
+        P.max_rows = std::max(P.max_rows, w);
+    }
+    return "";
+}
+
+}  // namespace mcinv

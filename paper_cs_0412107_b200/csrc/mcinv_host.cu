@@ -20,6 +20,7 @@
 
 #include "../../include/mcinv.h"
 #include "mcinv_internal.cuh"
+#include "levels.h"
 #include "plan.h"
 
 using mcinv::cd;
@@ -50,7 +51,19 @@ struct PlanDev {
     mcinv::HostPlan stats;
 };
 
+// Device copy of the level schedule (levels.h) for the v3 kernel.
+struct LevelDev {
+    DevBuf ph_row, ord_row, ord_eptr, ent_col, ent_ab, ent_pz, ord_dsg, ord_pself;
+    DevBuf ph_tq, tq_row, tq_eptr, tq_col, tq_val, ph_pp, pp_i, pp_j, pp_slot;
+    int D = 0, max_rows = 0;
+    std::string error;
+    mcinv::LevelPlan host;  // kept only for mcinv_debug_levels
+};
+
 struct Layout {
+    int ver = 3;            // sweep kernel: 1 row-by-row, 2 step schedule, 3 level schedule
+    int lgC = 0, lgP = 0;   // v3: log2 chains per CTA and per accumulator sub-slot
+    int Gs = 0, ksub = 1;   // accumulator sub-slots (Gs = G * ksub)
     int ld = 0, G = 0, T = 0;
     int e = 1;              // doubles per scalar
     size_t zw = 0, slot_diag = 0, slot_pat = 0, slot_full = 0, slot_trace = 0, snap_x = 0, snap_y = 0, mom = 0;
@@ -81,6 +94,8 @@ struct mcinv_ctx {
     std::vector<int> h_q_col;
     std::vector<std::complex<double>> h_q_val;
     std::map<std::tuple<int, unsigned>, std::unique_ptr<PlanDev>> plans;  // (C, outputs) -> plan
+    std::map<unsigned, std::unique_ptr<LevelDev>> levels;                 // outputs -> level schedule
+    int nsm = 148;
     int last_kernel = 0;  // 1 = v1, 2 = v2
     int last_C = 0;
     int64_t last_steps = 0;
@@ -296,6 +311,7 @@ mcinv_status build_pattern(mcinv_ctx *ctx, int64_t count, const int32_t *rows, c
     ctx->h_prow.assign(rows, rows + count);
     ctx->h_pcol.assign(cols, cols + count);
     ctx->plans.clear();
+    ctx->levels.clear();
     TRY(upload(ctx, ctx->p_ptr, ptr));
     TRY(upload(ctx, ctx->p_idx, idx));
     TRY(upload(ctx, ctx->p_other, other));
@@ -328,6 +344,7 @@ mcinv_status build_q(mcinv_ctx *ctx, const std::vector<std::vector<Entry>> &rows
         ctx->h_q_ptr[i + 1] = (int64_t)ctx->h_q_col.size();
     }
     ctx->plans.clear();
+    ctx->levels.clear();
     for (int64_t i = 0; i < n; ++i) {
         for (const Entry &e : rows[i]) {
             if (e.j <= i) {
@@ -402,6 +419,30 @@ mcinv_status check_args(const mcinv_ctx *ctx_c, const mcinv_run_args *a) {
     return MCINV_OK;
 }
 
+int kernel_pref() {  // 0 auto (v3), 1 force v1, 2 force v2, 3 force v3
+    const char *e = std::getenv("MCINV_KERNEL");
+    if (!e) return 0;
+    if (!std::strcmp(e, "v1")) return 1;
+    if (!std::strcmp(e, "v2")) return 2;
+    if (!std::strcmp(e, "v3")) return 3;
+    return 0;
+}
+
+int ilog2(int64_t x) {
+    int l = 0;
+    while ((int64_t(1) << (l + 1)) <= x) ++l;
+    return l;
+}
+
+// v3: C = chains per CTA, the smallest power of two that fits the chains in
+// one wave of CTAs (one per SM), at most 1024 (MCINV_C overrides)
+int choose_lgC(const mcinv_ctx *ctx, int64_t chains) {
+    if (const char *e = std::getenv("MCINV_C")) return ilog2(std::max(1, std::atoi(e)));
+    int lg = 0;
+    while (lg < 10 && ((chains + (int64_t(1) << lg) - 1) >> lg) > ctx->nsm) ++lg;
+    return lg;
+}
+
 Layout make_layout(const mcinv_ctx *ctx, const mcinv_run_args *a) {
     Layout L;
     const int64_t n = ctx->n;
@@ -410,6 +451,18 @@ Layout make_layout(const mcinv_ctx *ctx, const mcinv_run_args *a) {
     const size_t sz = 8 * L.e;
     L.ld = (int)((a->chains + 31) / 32 * 32);
     L.G = (int)(a->chains / a->group_size);
+    const int pref = kernel_pref();
+    L.ver = pref == 0 ? 3 : pref;
+    L.Gs = L.G;
+    L.ksub = 1;
+    if (L.ver == 3) {
+        L.lgC = choose_lgC(ctx, a->chains);
+        const int64_t q = std::max<int64_t>(32, int64_t(1) << L.lgC);  // padded chains stay in bounds
+        L.ld = (int)((a->chains + q - 1) / q * q);
+        L.lgP = std::min(L.lgC, ilog2(a->group_size));
+        L.ksub = a->group_size >> L.lgP;
+        L.Gs = L.G * L.ksub;
+    }
     L.T = 0;
     if (a->outputs & MCINV_FULL) {
         int T = a->snapshot_sweeps;
@@ -428,14 +481,14 @@ Layout make_layout(const mcinv_ctx *ctx, const mcinv_run_args *a) {
         return o;
     };
     L.zw = take((size_t)n * L.ld * 2 * sz);
-    if (a->outputs & MCINV_DIAG) L.slot_diag = take((size_t)L.G * n * sz);
-    if (a->outputs & MCINV_PATTERN) L.slot_pat = take((size_t)L.G * std::max<int64_t>(ctx->pcount, 1) * sz);
+    if (a->outputs & MCINV_DIAG) L.slot_diag = take((size_t)L.Gs * n * sz);
+    if (a->outputs & MCINV_PATTERN) L.slot_pat = take((size_t)L.Gs * std::max<int64_t>(ctx->pcount, 1) * sz);
     if (a->outputs & MCINV_FULL) {
         L.slot_full = take((size_t)L.G * n * n * sz);
         L.snap_x = take((size_t)L.T * n * L.ld * sz);
         L.snap_y = take((size_t)L.T * n * L.ld * sz);
     }
-    if (a->outputs & MCINV_TRACE) L.slot_trace = take((size_t)L.G * sz);
+    if (a->outputs & MCINV_TRACE) L.slot_trace = take((size_t)L.Gs * sz);
     size_t m = 0;
     if (a->outputs & MCINV_DIAG) { L.mom_diag = m; m += 2 * (size_t)n * L.e; }
     if (a->outputs & MCINV_PATTERN) { L.mom_pat = m; m += 2 * (size_t)ctx->pcount * L.e; }
@@ -456,13 +509,6 @@ int choose_C(int64_t ld) {
     return 8;
 }
 
-int kernel_pref() {  // 0 auto, 1 force v1, 2 force v2
-    const char *e = std::getenv("MCINV_KERNEL");
-    if (!e) return 0;
-    if (!std::strcmp(e, "v1")) return 1;
-    if (!std::strcmp(e, "v2")) return 2;
-    return 0;
-}
 
 template <typename S>
 PlanDev *get_plan(mcinv_ctx *ctx, int C, unsigned outputs) {
@@ -513,6 +559,73 @@ PlanDev *get_plan(mcinv_ctx *ctx, int C, unsigned outputs) {
 }
 
 template <typename S>
+LevelDev *get_levels(mcinv_ctx *ctx, unsigned outputs) {
+    const unsigned key = outputs & (MCINV_PATTERN | MCINV_TRACE);
+    auto it = ctx->levels.find(key);
+    if (it != ctx->levels.end()) return it->second.get();
+    std::unique_ptr<LevelDev> ld(new LevelDev());
+    mcinv::LevelInput in;
+    in.n = ctx->n;
+    in.u_ptr = &ctx->h_u_ptr;
+    in.u_col = &ctx->h_u_col;
+    in.u_a = &ctx->h_u_a;
+    in.u_b = &ctx->h_u_b;
+    in.delta = &ctx->h_delta;
+    in.sigma = &ctx->h_sigma;
+    in.want_pattern = key & MCINV_PATTERN;
+    in.want_trace = key & MCINV_TRACE;
+    in.p_row = &ctx->h_prow;
+    in.p_col = &ctx->h_pcol;
+    in.q_ptr = &ctx->h_q_ptr;
+    in.q_col = &ctx->h_q_col;
+    in.q_val = &ctx->h_q_val;
+    mcinv::LevelPlan &P = ld->host;
+    ld->error = mcinv::build_levels(in, P);
+    if (ld->error.empty()) {
+        ld->D = P.D;
+        ld->max_rows = P.max_rows;
+        const size_t ne = P.ent_col.size();
+        std::vector<S> ab(2 * std::max<size_t>(ne, 1)), dsg(2 * ctx->n);
+        for (size_t e = 0; e < ne; ++e) {
+            ab[2 * e] = to_s<S>(P.ent_a[e]);
+            ab[2 * e + 1] = to_s<S>(P.ent_b[e]);
+        }
+        for (int64_t o = 0; o < ctx->n; ++o) {
+            dsg[2 * o] = to_s<S>(P.ord_dl[o]);
+            dsg[2 * o + 1] = to_s<S>(P.ord_sg[o]);
+        }
+        std::vector<S> tqv(P.tq_val.size());
+        for (size_t e = 0; e < tqv.size(); ++e) tqv[e] = to_s<S>(P.tq_val[e]);
+        mcinv_status st = MCINV_OK;
+        auto up = [&](DevBuf &b, const auto &v) {
+            if (st == MCINV_OK) st = upload(ctx, b, v);
+        };
+        up(ld->ph_row, P.ph_row);
+        up(ld->ord_row, P.ord_row);
+        up(ld->ord_eptr, P.ord_eptr);
+        up(ld->ent_col, P.ent_col);
+        up(ld->ent_ab, ab);
+        up(ld->ord_dsg, dsg);
+        up(ld->ent_pz, P.ent_pz);
+        up(ld->ord_pself, P.ord_pself);
+        up(ld->ph_tq, P.ph_tq);
+        up(ld->tq_row, P.tq_row);
+        up(ld->tq_eptr, P.tq_eptr);
+        up(ld->tq_col, P.tq_col);
+        up(ld->tq_val, tqv);
+        up(ld->ph_pp, P.ph_pp);
+        up(ld->pp_i, P.pp_i);
+        up(ld->pp_j, P.pp_j);
+        up(ld->pp_slot, P.pp_slot);
+        if (st != MCINV_OK) ld->error = "level plan upload failed";
+        if (!ctx->host_only) P = mcinv::LevelPlan();  // device copy only
+    }
+    LevelDev *raw = ld.get();
+    ctx->levels[key] = std::move(ld);
+    return raw;
+}
+
+template <typename S>
 mcinv_status run_typed(mcinv_ctx *ctx, const mcinv_run_args *a, const Layout &L, char *ws, cudaStream_t st) {
     using namespace mcinv;
     const int64_t n = ctx->n;
@@ -543,23 +656,67 @@ mcinv_status run_typed(mcinv_ctx *ctx, const mcinv_run_args *a, const Layout &L,
 
     if (!a->resume) {
         CK(cudaMemsetAsync(ws + L.zw, 0, (size_t)n * L.ld * sizeof(ZW<S>), st));
-        if (a->outputs & MCINV_DIAG) CK(cudaMemsetAsync(p.slot_diag, 0, (size_t)L.G * n * sizeof(S), st));
+        if (a->outputs & MCINV_DIAG) CK(cudaMemsetAsync(p.slot_diag, 0, (size_t)L.Gs * n * sizeof(S), st));
         if (a->outputs & MCINV_PATTERN)
-            CK(cudaMemsetAsync(p.slot_pat, 0, (size_t)L.G * std::max<int64_t>(ctx->pcount, 1) * sizeof(S), st));
+            CK(cudaMemsetAsync(p.slot_pat, 0, (size_t)L.Gs * std::max<int64_t>(ctx->pcount, 1) * sizeof(S), st));
         if (a->outputs & MCINV_FULL) CK(cudaMemsetAsync(ws + L.slot_full, 0, (size_t)L.G * n * n * sizeof(S), st));
-        if (a->outputs & MCINV_TRACE) CK(cudaMemsetAsync(p.slot_trace, 0, (size_t)L.G * sizeof(S), st));
+        if (a->outputs & MCINV_TRACE) CK(cudaMemsetAsync(p.slot_trace, 0, (size_t)L.Gs * sizeof(S), st));
     }
-    // kernel choice: v2 (step schedule, sweep2.cu) unless its plan does not fit
-    const int pref = kernel_pref();
+    // kernel choice (Layout::ver): v3 level schedule (default), v2 step schedule, v1 row by row
     const int C = choose_C(L.ld);
-    PlanDev *plan = pref == 1 ? nullptr : get_plan<S>(ctx, C, a->outputs);
+    PlanDev *plan = L.ver == 2 ? get_plan<S>(ctx, C, a->outputs) : nullptr;
     const bool v2 = plan && plan->error.empty() &&
                     (int64_t)plan->steps * (a->burn_in + a->cycles) < (int64_t(1) << 31);
-    if (pref == 2 && !v2)
-        return fail(ctx, MCINV_E_INVALID, "v2 kernel unavailable: " + (plan ? plan->error : std::string("forced v1")));
-    ctx->last_kernel = v2 ? 2 : 1;
-    ctx->last_C = v2 ? plan->C : 32;
-    ctx->last_steps = v2 ? plan->steps : n;
+    if (L.ver == 2 && !v2)
+        return fail(ctx, MCINV_E_INVALID, "v2 kernel unavailable: " + (plan ? plan->error : std::string("no plan")));
+    LevelDev *lv = L.ver == 3 ? get_levels<S>(ctx, a->outputs) : nullptr;
+    if (lv && !lv->error.empty()) return fail(ctx, MCINV_E_INVALID, "level schedule: " + lv->error);
+    ctx->last_kernel = L.ver;
+    ctx->last_C = v2 ? plan->C : (lv ? (1 << L.lgC) : 32);
+    ctx->last_steps = v2 ? plan->steps : (lv ? lv->D : n);
+    Sweep3Params<S> q3{};
+    int threads3 = 0;
+    if (lv) {
+        q3.ph_row = (const int *)lv->ph_row.p;
+        q3.ord_row = (const int *)lv->ord_row.p;
+        q3.ord_eptr = (const int *)lv->ord_eptr.p;
+        q3.ent_col = (const int *)lv->ent_col.p;
+        q3.ent_ab = (const S *)lv->ent_ab.p;
+        q3.ent_pz = (const int2 *)lv->ent_pz.p;
+        q3.ord_dsg = (const S *)lv->ord_dsg.p;
+        q3.ord_pself = (const int *)lv->ord_pself.p;
+        q3.ph_tq = (const int *)lv->ph_tq.p;
+        q3.tq_row = (const int *)lv->tq_row.p;
+        q3.tq_eptr = (const int *)lv->tq_eptr.p;
+        q3.tq_col = (const int *)lv->tq_col.p;
+        q3.tq_val = (const S *)lv->tq_val.p;
+        q3.ph_pp = (const int *)lv->ph_pp.p;
+        q3.pp_i = (const int *)lv->pp_i.p;
+        q3.pp_j = (const int *)lv->pp_j.p;
+        q3.pp_slot = (const int *)lv->pp_slot.p;
+        q3.D = lv->D;
+        q3.zw = p.zw;
+        q3.n = (int)n;
+        q3.ld = L.ld;
+        q3.chains = p.chains;
+        q3.chain0 = p.chain0;
+        q3.key0 = p.key0;
+        q3.key1 = p.key1;
+        q3.noise = p.noise;
+        q3.sweep_abs0 = p.sweep_abs0;
+        q3.burn_in = p.burn_in;
+        q3.lgC = L.lgC;
+        q3.lgP = L.lgP;
+        q3.pcount = (int)ctx->pcount;
+        q3.slot_diag = p.slot_diag;
+        q3.slot_pat = p.slot_pat;
+        q3.slot_trace = p.slot_trace;
+        // threads: enough for the widest phase x C, a multiple of 32 and of C, <= 1024
+        int64_t want = (int64_t)std::max(lv->max_rows, 1) << L.lgC;
+        if (const char *e = std::getenv("MCINV_THREADS")) want = std::atoi(e);
+        want = std::min<int64_t>(1024, std::max<int64_t>(want, int64_t(1) << L.lgC));
+        threads3 = (int)((want + 31) / 32 * 32);
+    }
     Sweep2Params<S> q2{};
     if (v2) {
         q2.tiles = (const unsigned char *)plan->tiles.p;
@@ -585,7 +742,19 @@ mcinv_status run_typed(mcinv_ctx *ctx, const mcinv_run_args *a, const Layout &L,
     }
     cudaError_t lerr = cudaSuccess;
     auto sweep = [&](int s0, int s1, int snap_s0, unsigned outs) {
-        if (v2) {
+        if (lv) {
+            Sweep3Params<S> q = q3;
+            q.s_begin = s0;
+            q.s_end = s1;
+            q.snap_s0 = snap_s0;
+            q.outputs = outs;
+            q.snap_x = (S *)(ws + L.snap_x);
+            q.snap_y = (S *)(ws + L.snap_y);
+            timed(ctx, 0, st, [&] {
+                cudaError_t e = launch_sweep3<S>(q, threads3, st);
+                if (e != cudaSuccess) lerr = e;
+            });
+        } else if (v2) {
             Sweep2Params<S> q = q2;
             q.s_begin = s0;
             q.s_end = s1;
@@ -624,7 +793,7 @@ mcinv_status run_typed(mcinv_ctx *ctx, const mcinv_run_args *a, const Layout &L,
             });
         }
     }
-    if (lerr != cudaSuccess) return fail(ctx, MCINV_E_CUDA, std::string("sweep2 launch: ") + cudaGetErrorString(lerr));
+    if (lerr != cudaSuccess) return fail(ctx, MCINV_E_CUDA, std::string("sweep launch: ") + cudaGetErrorString(lerr));
     CK(cudaGetLastError());
     // moments and divergence flag
     double *mom = (double *)(ws + L.mom);
@@ -634,13 +803,15 @@ mcinv_status run_typed(mcinv_ctx *ctx, const mcinv_run_args *a, const Layout &L,
     const int e = L.e;
     ctx->launches += __builtin_popcount(a->outputs);  // one moments kernel per output
     if (a->outputs & MCINV_DIAG)
-        launch_moments(p.slot_diag, L.G, n * e, mom + L.mom_diag, mom + L.mom_diag + n * e, st);
+        launch_moments(p.slot_diag, L.G, L.ksub, n * e, mom + L.mom_diag, mom + L.mom_diag + n * e, st);
     if (a->outputs & MCINV_PATTERN)
-        launch_moments(p.slot_pat, L.G, ctx->pcount * e, mom + L.mom_pat, mom + L.mom_pat + ctx->pcount * e, st);
+        launch_moments(p.slot_pat, L.G, L.ksub, ctx->pcount * e, mom + L.mom_pat, mom + L.mom_pat + ctx->pcount * e,
+                       st);
     if (a->outputs & MCINV_FULL)
-        launch_moments((const double *)(ws + L.slot_full), L.G, n * n * e, mom + L.mom_full,
+        launch_moments((const double *)(ws + L.slot_full), L.G, 1, n * n * e, mom + L.mom_full,
                        mom + L.mom_full + n * n * e, st);
-    if (a->outputs & MCINV_TRACE) launch_moments(p.slot_trace, L.G, e, mom + L.mom_trace, mom + L.mom_trace + e, st);
+    if (a->outputs & MCINV_TRACE)
+        launch_moments(p.slot_trace, L.G, L.ksub, e, mom + L.mom_trace, mom + L.mom_trace + e, st);
     CK(cudaGetLastError());
     return MCINV_OK;
 }
@@ -684,6 +855,7 @@ mcinv_status mcinv_create(mcinv_ctx **out, int device, mcinv_dtype dtype, int64_
     if (dtype != MCINV_F64 && dtype != MCINV_C128) return fail(ctx, MCINV_E_INVALID, "dtype");
     if (n < 1 || n >= (int64_t(1) << 31)) return fail(ctx, MCINV_E_INVALID, "n out of range");
     CK(cudaSetDevice(device));
+    CK(cudaDeviceGetAttribute(&ctx->nsm, cudaDevAttrMultiProcessorCount, device));
     std::vector<std::vector<Entry>> rows;
     TRY(read_csr(ctx, n, row_ptr, col_idx, (const double *)values, dtype == MCINV_C128, rows));
     TRY(dtype == MCINV_C128 ? build_matrix<cd>(ctx, rows) : build_matrix<double>(ctx, rows));
@@ -925,6 +1097,39 @@ mcinv_status mcinv_debug_plan(mcinv_dtype dtype, int64_t n, const int64_t *row_p
         if (capacity < hp.tiles.size()) return MCINV_E_BUFFER;
         std::memcpy(tiles, hp.tiles.data(), hp.tiles.size());
     }
+    return MCINV_OK;
+}
+
+mcinv_status mcinv_debug_levels(mcinv_dtype dtype, int64_t n, const int64_t *row_ptr, const int32_t *col_idx,
+                                const void *values, const int64_t *q_row_ptr, const int32_t *q_col_idx,
+                                const void *q_values, unsigned outputs, int32_t *level, int64_t *info) {
+    if (!info) return MCINV_E_INVALID;
+    mcinv_ctx c;
+    mcinv_ctx *ctx = &c;
+    ctx->host_only = true;
+    ctx->dtype = dtype;
+    ctx->n = n;
+    if (dtype != MCINV_F64 && dtype != MCINV_C128) return MCINV_E_INVALID;
+    if (n < 1 || n >= (int64_t(1) << 31)) return MCINV_E_INVALID;
+    std::vector<std::vector<Entry>> rows;
+    TRY(read_csr(ctx, n, row_ptr, col_idx, (const double *)values, dtype == MCINV_C128, rows));
+    TRY(dtype == MCINV_C128 ? build_matrix<cd>(ctx, rows) : build_matrix<double>(ctx, rows));
+    TRY(default_pattern(ctx));
+    if (q_row_ptr) {
+        std::vector<std::vector<Entry>> qrows;
+        TRY(read_csr(ctx, n, q_row_ptr, q_col_idx, (const double *)q_values, dtype == MCINV_C128, qrows));
+        TRY(dtype == MCINV_C128 ? build_q<cd>(ctx, qrows) : build_q<double>(ctx, qrows));
+    }
+    LevelDev *lv = dtype == MCINV_C128 ? get_levels<cd>(ctx, outputs) : get_levels<double>(ctx, outputs);
+    if (!lv->error.empty()) return fail(ctx, MCINV_E_INVALID, lv->error);
+    const mcinv::LevelPlan &P = lv->host;
+    info[0] = P.D;
+    info[1] = P.max_rows;
+    info[2] = P.fused_pairs;
+    info[3] = P.deferred_pairs;
+    info[4] = (int64_t)P.tq_row.size();
+    info[5] = (int64_t)P.ent_col.size();
+    if (level) std::copy(P.level.begin(), P.level.end(), level);
     return MCINV_OK;
 }
 

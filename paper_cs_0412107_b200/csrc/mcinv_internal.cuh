@@ -113,12 +113,43 @@ template <typename S>
 size_t sweep2_smem(int tile_slot, int max_items);
 int sweep2_debug(unsigned int *dbg);
 
+// v3 sweep kernel on the level schedule (levels.h / sweep3.cu). Arrays are in
+// level order; see LevelPlan for their meaning.
+template <typename S>
+struct Sweep3Params {
+    const int *ph_row, *ord_row, *ord_eptr, *ent_col;
+    const S *ent_ab;      // [nnz_u][2]: a = c_ij (Eq. 4), b = conj(c_ji) (Eq. 5)
+    const int2 *ent_pz;   // [nnz_u] pattern slots, or nullptr
+    const S *ord_dsg;     // [n][2]: delta_i, sigma_i
+    const int *ord_pself;
+    const int *ph_tq, *tq_row, *tq_eptr, *tq_col;
+    const S *tq_val;
+    const int *ph_pp, *pp_i, *pp_j, *pp_slot;
+    int D;
+    ZW<S> *zw;
+    int n, ld, chains;
+    uint32_t chain0, key0, key1;
+    int noise;
+    uint32_t sweep_abs0;
+    int s_begin, s_end, burn_in;
+    unsigned outputs;
+    int lgC, lgP;         // log2 chains per CTA, log2 chains per accumulator sub-slot
+    int pcount;
+    double *slot_diag, *slot_pat, *slot_trace;  // [chains / P][count] (x e doubles)
+    S *snap_x, *snap_y;
+    int snap_s0;
+};
+
+template <typename S>
+cudaError_t launch_sweep3(const Sweep3Params<S> &p, int threads, cudaStream_t st);
+
 // A_g[i][j] += sum_{t < T, c in group g} X[t][i][c] conj(Y[t][j][c]).
 template <typename S>
 void launch_contract(const S *x, const S *y, double *acc, int n, int ld, int chains, int gs, int T,
                      cudaStream_t st);
 
-void launch_moments(const double *slot, int G, int64_t comps, double *s1, double *s2, cudaStream_t st);
+// slot layout [G * k][comps]: group g is the sum of sub-slots g*k .. g*k+k-1
+void launch_moments(const double *slot, int G, int k, int64_t comps, double *s1, double *s2, cudaStream_t st);
 void launch_finalize(const double *s1, const double *s2, int64_t comps, double m_cycles, double gs_cycles,
                      double G, double *est, double *se, cudaStream_t st);
 template <typename S>

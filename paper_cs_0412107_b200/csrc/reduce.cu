@@ -10,14 +10,16 @@
 
 namespace mcinv {
 
-// slot layout [G][comps]; s1[c] = sum_g slot, s2[c] = sum_g slot^2.
-__global__ void moments_kernel(const double *__restrict__ slot, int G, int64_t comps, double *__restrict__ s1,
-                               double *__restrict__ s2) {
+// slot layout [G * k][comps]: the sum of group g is the sum of its k
+// sub-slots; s1[c] = sum_g group sum, s2[c] = sum_g (group sum)^2.
+__global__ void moments_kernel(const double *__restrict__ slot, int G, int k, int64_t comps,
+                               double *__restrict__ s1, double *__restrict__ s2) {
     for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < comps;
          c += (int64_t)gridDim.x * blockDim.x) {
         double a = 0.0, b = 0.0;
         for (int g = 0; g < G; ++g) {
-            const double v = slot[(int64_t)g * comps + c];
+            double v = 0.0;
+            for (int h = 0; h < k; ++h) v += slot[((int64_t)g * k + h) * comps + c];
             a += v;
             b = fma(v, v, b);
         }
@@ -79,8 +81,8 @@ static int grid_for(int64_t work, int threads) {
     return b < 1 ? 1 : (int)b;
 }
 
-void launch_moments(const double *slot, int G, int64_t comps, double *s1, double *s2, cudaStream_t st) {
-    moments_kernel<<<grid_for(comps, 256), 256, 0, st>>>(slot, G, comps, s1, s2);
+void launch_moments(const double *slot, int G, int k, int64_t comps, double *s1, double *s2, cudaStream_t st) {
+    moments_kernel<<<grid_for(comps, 256), 256, 0, st>>>(slot, G, k, comps, s1, s2);
 }
 
 void launch_finalize(const double *s1, const double *s2, int64_t comps, double m_cycles, double gs_cycles, double G,

@@ -236,12 +236,15 @@ def test_errors(mc):
     assert e.value.code == 8
 
 
-@pytest.mark.parametrize("kernel", ["v1", "v2"])
+@pytest.mark.parametrize("kernel", ["v1", "v2", "v3"])
 def test_both_kernels(mc, orc, kernel, monkeypatch):
-    """The row-by-row kernel (v1) and the step-scheduled kernel (v2) both
-    match the oracle; v2 is forced for every chains-per-warp layout."""
+    """The row-by-row kernel (v1), the step-scheduled kernel (v2) and the
+    level-scheduled kernel (v3) all match the oracle, for every chains-per-warp
+    (v2) / chains-per-CTA (v3) layout: C below, equal to and above the group
+    size (accumulator sub-slots) and above a warp."""
     monkeypatch.setenv("MCINV_KERNEL", kernel)
-    for C in ((8, 16, 32) if kernel == "v2" else (32,)):
+    Cs = {"v1": (32,), "v2": (8, 16, 32), "v3": (1, 4, 8, 32, 64)}[kernel]
+    for C in Cs:
         monkeypatch.setenv("MCINV_C", str(C))
         compare_run(mc, orc, W.pedigree(500, seed=21), seed=4, chains=64, burn_in=2, cycles=4,
                     outputs=("diag", "pattern"), group_size=8)
@@ -250,13 +253,31 @@ def test_both_kernels(mc, orc, kernel, monkeypatch):
                     outputs=("diag", "trace", "full"), group_size=4, snapshot_sweeps=2)
 
 
-def test_bench_configs_use_v2(mc):
+def test_v3_custom_pattern_and_threads(mc, orc, monkeypatch):
+    """v3 with a custom pattern (non-neighbour pairs, duplicates, diagonal
+    elements: deferred items) and forced block sizes (several rounds of items
+    per phase)."""
+    monkeypatch.setenv("MCINV_KERNEL", "v3")
+    c = W.pedigree(300, seed=31)
+    rng = np.random.default_rng(32)
+    pr = rng.integers(0, c.n, 200).astype(np.int32)
+    pc = rng.integers(0, c.n, 200).astype(np.int32)
+    pr[:5] = pc[:5]            # diagonal elements
+    pr[5:10] = pr[0:5]         # duplicates
+    pc[5:10] = pc[0:5]
+    for th in ("32", "96", "1024"):
+        monkeypatch.setenv("MCINV_THREADS", th)
+        compare_run(mc, orc, c, pattern=(pr, pc), seed=6, chains=48, burn_in=1, cycles=3,
+                    outputs=("pattern", "diag"), group_size=16)
+
+
+def test_bench_configs_use_v3(mc):
     for k in (2, 3, 5):
         c, q, run = W.config(k)
         inv = mc.Inverter(c, q=q)
         inv.run(run.seed, run.chains, 0, 1, tuple(o for o in run.outputs if o != "full") or ("diag",),
                 group_size=run.group_size)
-        assert inv.kernel_info()["version"] == 2, k
+        assert inv.kernel_info()["version"] == 3, k
         inv.close()
 
 

@@ -1,0 +1,110 @@
+"""CPU tests of the v3 level schedule (paper_cs_0412107_b200/csrc/levels.cu).
+
+The sweep of Eq. (4)/(5) reads new values of lower
+neighbours and old values of upper neighbours; running rows level by level,
+lev(i) = 1 + max lev(lower neighbours), reproduces exactly those operands
+(DESIGN.md "Level schedule"). These tests pin the planner against an
+independent pure-Python longest-path computation and check the invariants
+the kernel relies on. No GPU needed (mcinv_debug_levels is host-only).
+"""
+import numpy as np
+import pytest
+
+import workloads as W
+
+
+@pytest.fixture(scope="module")
+def mc():
+    import paper_cs_0412107_b200 as M
+    M.load()
+    return M
+
+
+def neighbours(c):
+    """Undirected neighbour sets of the off-diagonal pattern of C and C^T."""
+    nb = [set() for _ in range(c.n)]
+    for i in range(c.n):
+        for e in range(c.row_ptr[i], c.row_ptr[i + 1]):
+            j = int(c.col[e])
+            if j != i:
+                nb[i].add(j)
+                nb[j].add(i)
+    return nb
+
+
+def brute_levels(c):
+    """Longest path in the DAG j -> i (j < i neighbours), by repeated
+    relaxation until a fixed point (Bellman-Ford style; independent of the
+    planner's single ascending pass)."""
+    nb = neighbours(c)
+    lev = [0] * c.n
+    changed = True
+    while changed:
+        changed = False
+        for i in range(c.n):
+            want = max([lev[j] + 1 for j in nb[i] if j < i], default=0)
+            if want != lev[i]:
+                lev[i] = want
+                changed = True
+    return np.array(lev)
+
+
+@pytest.mark.parametrize("make", [
+    lambda: W.pedigree(400, seed=3),
+    lambda: W.lattice(6, 2, 0.2, seed=4),
+    lambda: W.lattice(3, 4, 0.1, seed=5),
+    lambda: W.dense_config1(24, seed=6),
+    lambda: W.diagonal(np.arange(1.0, 9.0)),
+])
+def test_levels_match_longest_path(mc, make):
+    c = make()
+    lev, info = mc.debug_levels(c)
+    ref = brute_levels(c)
+    assert np.array_equal(lev, ref)
+    assert info["levels"] == (ref.max() + 1)
+    # the schedule respects every ordering constraint of the sequential sweep
+    nb = neighbours(c)
+    for i in range(c.n):
+        for j in nb[i]:
+            if j < i:
+                assert lev[j] < lev[i]
+
+
+def test_dense_is_fully_sequential(mc):
+    """A dense C (config 1) admits no reordering: n levels of one row."""
+    c = W.dense_config1(16, seed=7)
+    lev, info = mc.debug_levels(c)
+    assert np.array_equal(lev, np.arange(16)) and info["levels"] == 16
+
+
+def test_diagonal_is_one_level(mc):
+    """Diagonal C: rows are independent, one level."""
+    lev, info = mc.debug_levels(W.diagonal([2.0, 4.0, 1.0]))
+    assert info["levels"] == 1 and not lev.any()
+
+
+def test_lattice_depth_closed_form(mc):
+    """Periodic L^d lattice, x0 fastest: the longest increasing neighbour path
+    walks each coordinate from 0 to L-1, d(L-1)+1 levels (config 3: 127,
+    config 5: 61)."""
+    for L, d in ((8, 2), (4, 3), (5, 2)):
+        c = W.lattice(L, d, 0.1, seed=8)
+        _, info = mc.debug_levels(c)
+        assert info["levels"] == d * (L - 1) + 1
+
+
+def test_pattern_pairs_all_assigned(mc):
+    """Default pattern (the pattern of C): every element is fused into an
+    update (diagonal or lower-neighbour pair), none deferred."""
+    c = W.pedigree(300, seed=9)
+    _, info = mc.debug_levels(c, outputs=("pattern",))
+    assert info["fused_pairs"] == c.nnz and info["deferred_pairs"] == 0
+
+
+def test_trace_items(mc):
+    """One deferred trace item per non-empty row of Q."""
+    c = W.lattice(4, 2, 0.2, seed=10)
+    q = W.random_q(c.n, 11, 3)
+    _, info = mc.debug_levels(c, outputs=("trace",), q=q)
+    assert info["trace_items"] == int(np.sum(np.diff(q.row_ptr) > 0))
+    assert info["levels"] == 2 * 3 + 1
