@@ -53,7 +53,7 @@ struct PlanDev {
 
 // Device copy of the level schedule (levels.h) for the v3 kernel.
 struct LevelDev {
-    DevBuf ph_row, ord_row, ord_eptr, ent_col, ent_ab, ent_pz, ord_dsg, ord_pself;
+    DevBuf ph_row, ord_rec, ent_col, ent_ab, ent_pz, ord_dsg;
     DevBuf ph_tq, tq_row, tq_eptr, tq_col, tq_val, ph_pp, pp_i, pp_j, pp_slot;
     int D = 0, max_rows = 0;
     std::string error;
@@ -459,9 +459,11 @@ Layout make_layout(const mcinv_ctx *ctx, const mcinv_run_args *a) {
         L.lgC = choose_lgC(ctx, a->chains);
         const int64_t q = std::max<int64_t>(32, int64_t(1) << L.lgC);  // padded chains stay in bounds
         L.ld = (int)((a->chains + q - 1) / q * q);
-        L.lgP = std::min(L.lgC, ilog2(a->group_size));
-        L.ksub = a->group_size >> L.lgP;
-        L.Gs = L.G * L.ksub;
+        // accumulator slots are the SE groups (the kernel sums the chains of a
+        // group inside the CTA, then reduces into the group slot in L2)
+        L.lgP = std::min(ilog2(a->group_size), L.lgC);  // lanes of one SE group inside a CTA
+        L.ksub = 1;
+        L.Gs = L.G;
     }
     L.T = 0;
     if (a->outputs & MCINV_FULL) {
@@ -594,6 +596,15 @@ LevelDev *get_levels(mcinv_ctx *ctx, unsigned outputs) {
             dsg[2 * o] = to_s<S>(P.ord_dl[o]);
             dsg[2 * o + 1] = to_s<S>(P.ord_sg[o]);
         }
+        // row record {i, entry begin, entries | lower entries << 16, pattern slot of (i,i)}
+        std::vector<int4> rec(ctx->n);
+        for (int64_t o = 0; o < ctx->n; ++o) {
+            const int i = P.ord_row[o], beg = P.ord_eptr[o], cnt = P.ord_eptr[o + 1] - beg;
+            int nlow = 0;
+            while (nlow < cnt && P.ent_col[beg + nlow] < i) ++nlow;  // lower neighbours: a prefix
+            if (cnt >= 65536) ld->error = "a row has 65536 or more off-diagonal entries";
+            rec[o] = make_int4(i, beg, cnt | nlow << 16, P.ord_pself[o]);
+        }
         std::vector<S> tqv(P.tq_val.size());
         for (size_t e = 0; e < tqv.size(); ++e) tqv[e] = to_s<S>(P.tq_val[e]);
         mcinv_status st = MCINV_OK;
@@ -601,13 +612,11 @@ LevelDev *get_levels(mcinv_ctx *ctx, unsigned outputs) {
             if (st == MCINV_OK) st = upload(ctx, b, v);
         };
         up(ld->ph_row, P.ph_row);
-        up(ld->ord_row, P.ord_row);
-        up(ld->ord_eptr, P.ord_eptr);
+        up(ld->ord_rec, rec);
         up(ld->ent_col, P.ent_col);
         up(ld->ent_ab, ab);
         up(ld->ord_dsg, dsg);
         up(ld->ent_pz, P.ent_pz);
-        up(ld->ord_pself, P.ord_pself);
         up(ld->ph_tq, P.ph_tq);
         up(ld->tq_row, P.tq_row);
         up(ld->tq_eptr, P.tq_eptr);
@@ -617,7 +626,7 @@ LevelDev *get_levels(mcinv_ctx *ctx, unsigned outputs) {
         up(ld->pp_i, P.pp_i);
         up(ld->pp_j, P.pp_j);
         up(ld->pp_slot, P.pp_slot);
-        if (st != MCINV_OK) ld->error = "level plan upload failed";
+        if (st != MCINV_OK && ld->error.empty()) ld->error = "level plan upload failed";
         if (!ctx->host_only) P = mcinv::LevelPlan();  // device copy only
     }
     LevelDev *raw = ld.get();
@@ -671,6 +680,7 @@ mcinv_status run_typed(mcinv_ctx *ctx, const mcinv_run_args *a, const Layout &L,
         return fail(ctx, MCINV_E_INVALID, "v2 kernel unavailable: " + (plan ? plan->error : std::string("no plan")));
     LevelDev *lv = L.ver == 3 ? get_levels<S>(ctx, a->outputs) : nullptr;
     if (lv && !lv->error.empty()) return fail(ctx, MCINV_E_INVALID, "level schedule: " + lv->error);
+    if (lv && L.lgP > L.lgC) return fail(ctx, MCINV_E_INVALID, "layout: group lanes exceed chains per CTA");
     ctx->last_kernel = L.ver;
     ctx->last_C = v2 ? plan->C : (lv ? (1 << L.lgC) : 32);
     ctx->last_steps = v2 ? plan->steps : (lv ? lv->D : n);
@@ -678,13 +688,11 @@ mcinv_status run_typed(mcinv_ctx *ctx, const mcinv_run_args *a, const Layout &L,
     int threads3 = 0;
     if (lv) {
         q3.ph_row = (const int *)lv->ph_row.p;
-        q3.ord_row = (const int *)lv->ord_row.p;
-        q3.ord_eptr = (const int *)lv->ord_eptr.p;
+        q3.ord_rec = (const int4 *)lv->ord_rec.p;
         q3.ent_col = (const int *)lv->ent_col.p;
         q3.ent_ab = (const S *)lv->ent_ab.p;
         q3.ent_pz = (const int2 *)lv->ent_pz.p;
         q3.ord_dsg = (const S *)lv->ord_dsg.p;
-        q3.ord_pself = (const int *)lv->ord_pself.p;
         q3.ph_tq = (const int *)lv->ph_tq.p;
         q3.tq_row = (const int *)lv->tq_row.p;
         q3.tq_eptr = (const int *)lv->tq_eptr.p;
@@ -707,6 +715,7 @@ mcinv_status run_typed(mcinv_ctx *ctx, const mcinv_run_args *a, const Layout &L,
         q3.burn_in = p.burn_in;
         q3.lgC = L.lgC;
         q3.lgP = L.lgP;
+        q3.lgG = ilog2(a->group_size);
         q3.pcount = (int)ctx->pcount;
         q3.slot_diag = p.slot_diag;
         q3.slot_pat = p.slot_pat;

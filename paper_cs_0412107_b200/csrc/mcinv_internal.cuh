@@ -117,11 +117,13 @@ int sweep2_debug(unsigned int *dbg);
 // level order; see LevelPlan for their meaning.
 template <typename S>
 struct Sweep3Params {
-    const int *ph_row, *ord_row, *ord_eptr, *ent_col;
+    const int *ph_row;
+    const int4 *ord_rec;  // [n] level-order row records {i, entry begin, entries | lower entries << 16,
+                          //     pattern slot of (i,i) or -1}
+    const int *ent_col;
     const S *ent_ab;      // [nnz_u][2]: a = c_ij (Eq. 4), b = conj(c_ji) (Eq. 5)
     const int2 *ent_pz;   // [nnz_u] pattern slots, or nullptr
     const S *ord_dsg;     // [n][2]: delta_i, sigma_i
-    const int *ord_pself;
     const int *ph_tq, *tq_row, *tq_eptr, *tq_col;
     const S *tq_val;
     const int *ph_pp, *pp_i, *pp_j, *pp_slot;
@@ -133,9 +135,11 @@ struct Sweep3Params {
     uint32_t sweep_abs0;
     int s_begin, s_end, burn_in;
     unsigned outputs;
-    int lgC, lgP;         // log2 chains per CTA, log2 chains per accumulator sub-slot
+    int lgC;              // log2 chains per CTA
+    int lgP;              // log2 lanes of one SE group inside a CTA: min(group size, C) (kernel template)
+    int lgG;              // log2 group size: chain c accumulates into group slot c >> lgG
     int pcount;
-    double *slot_diag, *slot_pat, *slot_trace;  // [chains / P][count] (x e doubles)
+    double *slot_diag, *slot_pat, *slot_trace;  // [groups][count] (x e doubles)
     S *snap_x, *snap_y;
     int snap_s0;
 };

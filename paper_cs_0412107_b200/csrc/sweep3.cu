@@ -15,12 +15,17 @@
 //
 // with the sums by serial fma from 0 in ascending j (reading R10)
 // and phi = phi(chain, sweep, row) shared by z_i and w_i.
-// Sampling sweeps accumulate (Eq. 1/C and Eq. tr): diag and the
-// pattern pairs of row i with its lower neighbours at the update; deferred
-// pattern pairs and the trace terms w_i^* Q_ij z_j as extra items of the
-// phase after both values became final. Sums over the P = min(gs, C) chains
-// of an accumulator sub-slot are warp shuffles; each sub-slot belongs to one
-// CTA, so the slot updates are plain (deterministic) read-modify-writes.
+//
+// Sampling sweeps accumulate (Eq. 1/C and Eq. tr): at row i's
+// update the products z_i w_i^* (diag, and the pattern element (i,i)) and,
+// for every lower neighbour j (a prefix of the ascending entry list, values
+// final), z_i w_j^* and z_j w_i^*; other pattern pairs and the trace terms
+// w_i^* Q_ij z_j are deferred items of the phase after both values became
+// final. The P lanes of one SE group (P = min(group size, C), a template
+// parameter) sum their products with a transpose-reduction (V = min(P, 8)
+// products over P lanes in V-1 shuffles, then log2(P/V) butterflies), after
+// which each lane posts ONE fire-and-forget reduction (red.global.add) into
+// the group's slot; the slots of all groups (41 MB for config 2) stay in L2.
 #include "mcinv_internal.cuh"
 #include "noise.cuh"
 #include "scalar.cuh"
@@ -29,17 +34,46 @@ namespace mcinv {
 
 namespace {
 
-template <typename S>
-__device__ __forceinline__ S seg_sum(S v, int P, unsigned mask) {
-    for (int off = 1; off < P; off <<= 1) {
-        if constexpr (ScalarTraits<S>::kDoubles == 1) {
-            v += __shfl_xor_sync(mask, v, off);
+__device__ __forceinline__ double shfl_x(double v, int off) { return __shfl_xor_sync(0xffffffffu, v, off); }
+__device__ __forceinline__ cd shfl_x(cd v, int off) { return cd{shfl_x(v.re, off), shfl_x(v.im, off)}; }
+__device__ __forceinline__ double sel(bool c, double a, double b) { return c ? a : b; }
+__device__ __forceinline__ cd sel(bool c, cd a, cd b) { return cd{c ? a.re : b.re, c ? a.im : b.im}; }
+
+// Sum over the P lanes of each aligned lane group (converged warp, full mask).
+template <int P, typename S>
+__device__ __forceinline__ S group_sum(S v) {
+#pragma unroll
+    for (int off = 1; off < P; off <<= 1) v = add_s(v, shfl_x(v, off));
+    return v;
+}
+
+// Transpose-reduction of V values per lane over the P lanes of a group
+// (V <= P, both powers of two). On return the lane holds the group total of
+// value index `held`; P/V lanes hold each index, the one with
+// (lane & (P/V - 1)) == 0 is its owner.
+template <int P, int V, typename S>
+__device__ __forceinline__ S transpose_sum(S (&v)[V], int lane, int &held) {
+    held = 0;
+    int nv = V;
+#pragma unroll
+    for (int off = P / 2; off >= 1; off >>= 1) {
+        if (nv > 1) {
+            const bool up = (lane & off) != 0;  // this lane keeps the upper half
+#pragma unroll
+            for (int q = 0; q < V / 2; ++q) {
+                if (q < nv / 2) {
+                    const S send = sel(up, v[q], v[q + nv / 2]);
+                    const S keep = sel(up, v[q + nv / 2], v[q]);
+                    v[q] = add_s(keep, shfl_x(send, off));
+                }
+            }
+            if (up) held += nv / 2;
+            nv /= 2;
         } else {
-            v.re += __shfl_xor_sync(mask, v.re, off);
-            v.im += __shfl_xor_sync(mask, v.im, off);
+            v[0] = add_s(v[0], shfl_x(v[0], off));
         }
     }
-    return v;
+    return v[0];
 }
 
 template <typename S>
@@ -74,31 +108,40 @@ __device__ __forceinline__ void row_sums(const Sweep3Params<S> &p, const ZW<S> *
     }
 }
 
-template <typename S>
-__device__ __forceinline__ void slot_rmw(double *slot, S v) {
-    add_to(slot, v);
+__device__ __forceinline__ void red_add(double *p, double v) {
+    asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+__device__ __forceinline__ void slot_red(double *slot, double v) { red_add(slot, v); }
+__device__ __forceinline__ void slot_red(double *slot, cd v) {
+    red_add(slot, v.re);
+    red_add(slot + 1, v.im);
 }
 
 }  // namespace
 
-template <typename S, int KU, int NT>
+template <typename S, int KU, int NT, int LGP>
 __global__ void __launch_bounds__(NT, 1) sweep3_kernel(const Sweep3Params<S> p) {
     constexpr int E = ScalarTraits<S>::kDoubles;
+    constexpr int P = 1 << LGP;        // lanes of one SE group inside this CTA (<= C)
+    constexpr int V = P < 8 ? P : 8;   // products per transpose-reduction
     const int tid = threadIdx.x;
-    const int B = blockDim.x;
-    const int lgC = p.lgC, lgP = p.lgP;
-    const int C = 1 << lgC, P = 1 << lgP;
+    const int B = blockDim.x;  // a multiple of 32 and of C
+    const int lane = tid & 31;
+    const int wbase = tid - lane;
+    const int lgC = p.lgC;
+    const int C = 1 << lgC;
     const int c = tid & (C - 1);
     const int chain = (blockIdx.x << lgC) + c;
     const bool active = chain < p.chains;
     const uint32_t gchain = p.chain0 + static_cast<uint32_t>(chain);
-    const int lane = tid & 31;
-    const unsigned pmask = P >= 32 ? 0xffffffffu : (((1u << P) - 1u) << (lane & ~(P - 1)));
-    const bool pleader = (c & (P - 1)) == 0;
-    const int64_t sub = chain >> lgP;  // accumulator sub-slot of this chain
+    const bool gleader = (c & (P - 1)) == 0;           // owner of a plain group sum
+    const bool towner = (lane & (P / V - 1)) == 0;     // owner of a transposed value
+    const int64_t grp = chain >> p.lgG;                // SE group of this chain = its accumulator slot
     ZW<S> *__restrict__ zcol = p.zw + chain;
     const bool want_diag = p.outputs & OUT_DIAG, want_pat = p.outputs & OUT_PATTERN;
     const bool want_tr = p.outputs & OUT_TRACE, want_full = p.outputs & OUT_FULL;
+    double *const sd = p.slot_diag + grp * p.n * E;
+    double *const sp = p.slot_pat + grp * p.pcount * E;
     S tr = zero_s<S>();
 
     for (int s = p.s_begin; s < p.s_end; ++s) {
@@ -106,57 +149,76 @@ __global__ void __launch_bounds__(NT, 1) sweep3_kernel(const Sweep3Params<S> p) 
         const bool sampling = s >= p.burn_in;
         const int nph = sampling ? p.D + 1 : p.D;
         for (int ph = 0; ph < nph; ++ph) {
-            // ---- row updates of level ph
+            // ---- row updates of level ph; warp-uniform trip count (shuffles below)
             const int r0 = __ldg(p.ph_row + ph);
             const int nu = (__ldg(p.ph_row + ph + 1) - r0) << lgC;
-            for (int t = tid; t < nu; t += B) {
+            for (int base = wbase; base < nu; base += B) {
+                const int t = base + lane;
+                const bool valid = t < nu;
                 const int o = r0 + (t >> lgC);
-                const int i = __ldg(p.ord_row + o);
-                const int beg = __ldg(p.ord_eptr + o), end = __ldg(p.ord_eptr + o + 1);
-                double phi;
-                if (p.noise == 0) phi = gaussian(static_cast<uint32_t>(i), k, gchain, p.key0, p.key1);
-                else phi = p.noise == 2 ? 1.0 : 0.0;
-                S az = zero_s<S>(), aw = zero_s<S>();
-                row_sums<S, KU>(p, zcol, beg, end, az, aw);
-                const S dl = ldg_s(p.ord_dsg + 2 * o), sg = ldg_s(p.ord_dsg + 2 * o + 1);
-                const S zi = fma_s(neg_s(dl), az, scale_s(sg, phi));
-                const S wi = fma_s(neg_s(conj_s(dl)), aw, scale_s(conj_s(sg), phi));
-                zcol[(int64_t)i * p.ld] = ZW<S>{zi, wi};
+                const int4 rec = valid ? __ldg(p.ord_rec + o) : make_int4(0, 0, 0, -1);
+                const int i = rec.x, beg = rec.y, cnt = rec.z & 0xffff;
+                S zi = zero_s<S>(), wi = zero_s<S>();
+                if (valid) {
+                    // noise first: its temporaries are dead before the gathers are in flight
+                    double phi;
+                    if (p.noise == 0) phi = gaussian(static_cast<uint32_t>(i), k, gchain, p.key0, p.key1);
+                    else phi = p.noise == 2 ? 1.0 : 0.0;
+                    S az = zero_s<S>(), aw = zero_s<S>();
+                    row_sums<S, KU>(p, zcol, beg, beg + cnt, az, aw);
+                    const S dl = ldg_s(p.ord_dsg + 2 * o), sg = ldg_s(p.ord_dsg + 2 * o + 1);
+                    zi = fma_s(neg_s(dl), az, scale_s(sg, phi));
+                    wi = fma_s(neg_s(conj_s(dl)), aw, scale_s(conj_s(sg), phi));
+                    zcol[(int64_t)i * p.ld] = ZW<S>{zi, wi};
+                    if (want_full && sampling) {
+                        const int64_t ts = s - p.snap_s0;
+                        p.snap_x[(ts * p.n + i) * p.ld + chain] = zi;
+                        p.snap_y[(ts * p.n + i) * p.ld + chain] = wi;
+                    }
+                }
                 if (!sampling) continue;
-                if (want_full) {
-                    const int64_t ts = s - p.snap_s0;
-                    p.snap_x[(ts * p.n + i) * p.ld + chain] = zi;
-                    p.snap_y[(ts * p.n + i) * p.ld + chain] = wi;
-                }
-                if (want_diag || want_pat) {
-                    const S d = seg_sum(active ? zwc_s(zi, wi) : zero_s<S>(), P, pmask);
-                    if (pleader && active) {
-                        if (want_diag) slot_rmw(p.slot_diag + (sub * p.n + i) * E, d);
-                        if (want_pat) {
-                            const int ps = __ldg(p.ord_pself + o);
-                            if (ps >= 0) slot_rmw(p.slot_pat + (sub * p.pcount + ps) * E, d);
-                        }
-                    }
-                }
+                const bool acc = valid && active;
                 if (want_pat) {
-                    // pairs with lower neighbours j: z_i w_j^* and z_j w_i^* (values final; L1-hot)
-                    for (int e = beg; e < end; ++e) {
-                        const int2 pz = __ldg(p.ent_pz + e);
-                        if ((pz.x & pz.y) < 0) continue;  // both -1
-                        const ZW<S> v = ld_zw(zcol + (int64_t)__ldg(p.ent_col + e) * p.ld);
-                        if (pz.x >= 0) {
-                            const S x = seg_sum(active ? zwc_s(zi, v.w) : zero_s<S>(), P, pmask);
-                            if (pleader && active) slot_rmw(p.slot_pat + (sub * p.pcount + pz.x) * E, x);
+                    // products of row i: [0] z_i w_i^*, [1 + 2e] z_i w_j^*, [2 + 2e] z_j w_i^* for the
+                    // lower neighbours j = col[beg + e], e < nlow
+                    const int nprod = acc ? 1 + 2 * (rec.z >> 16) : 0;
+                    const int nb = (__reduce_max_sync(0xffffffffu, nprod) + V - 1) / V;
+                    for (int b = 0; b < nb; ++b) {
+                        S v[V];
+#pragma unroll
+                        for (int q = 0; q < V; ++q) {
+                            const int idx = b * V + q;
+                            v[q] = zero_s<S>();
+                            if (idx == 0) {
+                                if (acc) v[q] = zwc_s(zi, wi);
+                            } else if (idx < nprod) {
+                                const ZW<S> u =
+                                    ld_zw(zcol + (int64_t)__ldg(p.ent_col + beg + ((idx - 1) >> 1)) * p.ld);
+                                v[q] = ((idx - 1) & 1) ? zwc_s(u.z, wi) : zwc_s(zi, u.w);
+                            }
                         }
-                        if (pz.y >= 0) {
-                            const S x = seg_sum(active ? zwc_s(v.z, wi) : zero_s<S>(), P, pmask);
-                            if (pleader && active) slot_rmw(p.slot_pat + (sub * p.pcount + pz.y) * E, x);
+                        int held;
+                        const S x = transpose_sum<P, V>(v, lane, held);
+                        const int idx = b * V + held;
+                        if (towner && idx < nprod) {
+                            if (idx == 0) {
+                                if (want_diag) slot_red(sd + (int64_t)i * E, x);
+                                if (rec.w >= 0) slot_red(sp + (int64_t)rec.w * E, x);
+                            } else {
+                                const int2 pz = __ldg(p.ent_pz + beg + ((idx - 1) >> 1));
+                                const int slot = ((idx - 1) & 1) ? pz.y : pz.x;
+                                if (slot >= 0) slot_red(sp + (int64_t)slot * E, x);
+                            }
                         }
                     }
+                } else if (want_diag) {
+                    const S d = group_sum<P>(acc ? zwc_s(zi, wi) : zero_s<S>());
+                    if (acc && gleader) slot_red(sd + (int64_t)i * E, d);
                 }
             }
             if (sampling) {
-                // ---- deferred trace items: conj(w_i) sum_j Q_ij z_j  (w^dagger Q z, reading R2)
+                // ---- deferred trace items: conj(w_i) sum_j Q_ij z_j  (w^dagger Q z, reading R2);
+                // per-thread register sums, no shuffles
                 if (want_tr) {
                     const int q0 = __ldg(p.ph_tq + ph);
                     const int nq = (__ldg(p.ph_tq + ph + 1) - q0) << lgC;
@@ -165,7 +227,8 @@ __global__ void __launch_bounds__(NT, 1) sweep3_kernel(const Sweep3Params<S> p) 
                         const int i = __ldg(p.tq_row + o);
                         S qz = zero_s<S>();
                         for (int e = __ldg(p.tq_eptr + o); e < __ldg(p.tq_eptr + o + 1); ++e)
-                            qz = add_s(qz, mul_s(ldg_s(p.tq_val + e), ld_zw(zcol + (int64_t)__ldg(p.tq_col + e) * p.ld).z));
+                            qz = add_s(qz, mul_s(ldg_s(p.tq_val + e),
+                                                 ld_zw(zcol + (int64_t)__ldg(p.tq_col + e) * p.ld).z));
                         tr = add_s(tr, zwc_s(qz, ld_zw(zcol + (int64_t)i * p.ld).w));
                     }
                 }
@@ -173,12 +236,16 @@ __global__ void __launch_bounds__(NT, 1) sweep3_kernel(const Sweep3Params<S> p) 
                 if (want_pat) {
                     const int q0 = __ldg(p.ph_pp + ph);
                     const int nq = (__ldg(p.ph_pp + ph + 1) - q0) << lgC;
-                    for (int t = tid; t < nq; t += B) {
+                    for (int base = wbase; base < nq; base += B) {
+                        const int t = base + lane;
+                        const bool valid = t < nq;
                         const int o = q0 + (t >> lgC);
-                        const S zi = ld_zw(zcol + (int64_t)__ldg(p.pp_i + o) * p.ld).z;
-                        const S wj = ld_zw(zcol + (int64_t)__ldg(p.pp_j + o) * p.ld).w;
-                        const S x = seg_sum(active ? zwc_s(zi, wj) : zero_s<S>(), P, pmask);
-                        if (pleader && active) slot_rmw(p.slot_pat + (sub * p.pcount + __ldg(p.pp_slot + o)) * E, x);
+                        S x = zero_s<S>();
+                        if (valid && active)
+                            x = zwc_s(ld_zw(zcol + (int64_t)__ldg(p.pp_i + o) * p.ld).z,
+                                      ld_zw(zcol + (int64_t)__ldg(p.pp_j + o) * p.ld).w);
+                        x = group_sum<P>(x);
+                        if (valid && active && gleader) slot_red(sp + (int64_t)__ldg(p.pp_slot + o) * E, x);
                     }
                 }
             }
@@ -187,32 +254,48 @@ __global__ void __launch_bounds__(NT, 1) sweep3_kernel(const Sweep3Params<S> p) 
     }
 
     if (want_tr) {
-        // per-chain trace: sum over the threads of each chain, then over the P chains of a sub-slot
+        // per-chain trace: sum over the threads of each chain, then over the P chains of a group
         extern __shared__ __align__(16) unsigned char red_raw[];
         S *red = reinterpret_cast<S *>(red_raw);
         red[tid] = active ? tr : zero_s<S>();
         __syncthreads();
-        if (tid < C) {
+        if (wbase < C) {  // whole warps (C < 32: lanes >= C hold zeros and are not leaders)
             S v = zero_s<S>();
-            for (int h = tid; h < B; h += C) v = add_s(v, red[h]);
-            const unsigned m = C >= 32 ? 0xffffffffu : ((1u << C) - 1u);
-            const unsigned pm = P >= 32 ? m : (((1u << P) - 1u) << (lane & ~(P - 1)));
-            v = seg_sum(v, P, pm);
-            if (pleader && active) slot_rmw(p.slot_trace + sub * E, v);
+            if (tid < C)
+                for (int h = tid; h < B; h += C) v = add_s(v, red[h]);
+            v = group_sum<P>(v);
+            if (tid < C && gleader && active) slot_red(p.slot_trace + grp * E, v);
         }
     }
 }
 
-template <typename S>
-cudaError_t launch_sweep3(const Sweep3Params<S> &p, int threads, cudaStream_t st) {
-    constexpr int KU = ScalarTraits<S>::kDoubles == 1 ? 4 : 2;
+namespace {
+
+template <typename S, int LGP>
+cudaError_t launch3(const Sweep3Params<S> &p, int threads, cudaStream_t st) {
+    // gathers in flight per row chunk: 64 registers at 1024 threads, 128 at 512
+    constexpr int KS = ScalarTraits<S>::kDoubles == 1 ? 4 : 2;
     const int C = 1 << p.lgC;
     const int blocks = (p.chains + C - 1) / C;
     const size_t smem = (p.outputs & OUT_TRACE) ? (size_t)threads * sizeof(S) : 0;
-    // <= 512 threads: up to 128 registers, no spills; else 64 registers
-    if (threads <= 512) sweep3_kernel<S, KU, 512><<<blocks, threads, smem, st>>>(p);
-    else sweep3_kernel<S, KU, 1024><<<blocks, threads, smem, st>>>(p);
+    if (threads <= 512) sweep3_kernel<S, 2 * KS, 512, LGP><<<blocks, threads, smem, st>>>(p);
+    else sweep3_kernel<S, KS, 1024, LGP><<<blocks, threads, smem, st>>>(p);
     return cudaGetLastError();
+}
+
+}  // namespace
+
+template <typename S>
+cudaError_t launch_sweep3(const Sweep3Params<S> &p, int threads, cudaStream_t st) {
+    switch (p.lgP) {
+        case 0: return launch3<S, 0>(p, threads, st);
+        case 1: return launch3<S, 1>(p, threads, st);
+        case 2: return launch3<S, 2>(p, threads, st);
+        case 3: return launch3<S, 3>(p, threads, st);
+        case 4: return launch3<S, 4>(p, threads, st);
+        case 5: return launch3<S, 5>(p, threads, st);
+        default: return cudaErrorInvalidValue;
+    }
 }
 
 template cudaError_t launch_sweep3<double>(const Sweep3Params<double> &, int, cudaStream_t);
