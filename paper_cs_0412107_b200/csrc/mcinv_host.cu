@@ -586,8 +586,12 @@ LevelDev *get_levels(mcinv_ctx *ctx, unsigned outputs) {
     if (ld->error.empty()) {
         ld->D = P.D;
         ld->max_rows = P.max_rows;
+        // entry arrays padded by 8 entries (col 0, zero coefficients, no pattern slot) so the
+        // kernel's unrolled loads past a row's last entry stay in bounds
         const size_t ne = P.ent_col.size();
-        std::vector<S> ab(2 * std::max<size_t>(ne, 1)), dsg(2 * ctx->n);
+        P.ent_col.resize(ne + 8, 0);
+        if (!P.ent_pz.empty()) P.ent_pz.resize(2 * (ne + 8), -1);
+        std::vector<S> ab(2 * (ne + 8)), dsg(2 * ctx->n);
         for (size_t e = 0; e < ne; ++e) {
             ab[2 * e] = to_s<S>(P.ent_a[e]);
             ab[2 * e + 1] = to_s<S>(P.ent_b[e]);
@@ -720,8 +724,10 @@ mcinv_status run_typed(mcinv_ctx *ctx, const mcinv_run_args *a, const Layout &L,
         q3.slot_diag = p.slot_diag;
         q3.slot_pat = p.slot_pat;
         q3.slot_trace = p.slot_trace;
-        // threads: enough for the widest phase x C, a multiple of 32 and of C, <= 1024
+        // threads: enough for the widest phase x C, a multiple of 32 and of C, <= 768 (85
+        // registers per thread: measured best for configs 2-5)
         int64_t want = (int64_t)std::max(lv->max_rows, 1) << L.lgC;
+        want = std::min<int64_t>(768, want);
         if (const char *e = std::getenv("MCINV_THREADS")) want = std::atoi(e);
         want = std::min<int64_t>(1024, std::max<int64_t>(want, int64_t(1) << L.lgC));
         threads3 = (int)((want + 31) / 32 * 32);
@@ -1137,7 +1143,7 @@ mcinv_status mcinv_debug_levels(mcinv_dtype dtype, int64_t n, const int64_t *row
     info[2] = P.fused_pairs;
     info[3] = P.deferred_pairs;
     info[4] = (int64_t)P.tq_row.size();
-    info[5] = (int64_t)P.ent_col.size();
+    info[5] = (int64_t)P.ent_col.size() - 8;  // without the kernel padding
     if (level) std::copy(P.level.begin(), P.level.end(), level);
     return MCINV_OK;
 }

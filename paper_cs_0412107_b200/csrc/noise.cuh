@@ -6,7 +6,9 @@
 // counter {i, k, c, 0} and key {seed lo, seed hi}, then the cosine branch of
 // Box-Muller on two 53-bit uniforms (reading R4):
 //   u1 = ((r0:r1 >> 11) + 1) 2^-53 in (0, 1],  u2 = (r2:r3 >> 11) 2^-53,
-//   phi = sqrt(-2 ln u1) cos(2 pi u2).
+//   phi = sqrt(-2 ln u1) cos(2 pi u2),
+// with ln and cos specialised to these argument ranges (log_unit, cos_0_2pi:
+// < 1 ulp each, so phi matches the oracle's libm evaluation to a few ulp).
 #pragma once
 #include <stdint.h>
 
@@ -34,12 +36,57 @@ __device__ __forceinline__ PhiloxOut philox4x32_10(uint32_t c0, uint32_t c1, uin
     return PhiloxOut{c0, c1, c2, c3};
 }
 
+// ln(x) for x in (0, 1] (normal doubles only): the fdlibm method (reduce to
+// m in [sqrt(2)/2, sqrt(2)), s = f / (2 + f), ln(1 + f) = f - f^2/2 +
+// s (f^2/2 + R(s^2)) with a degree-14 minimax R); < 1 ulp, no special cases.
+__device__ __forceinline__ double log_unit(double x) {
+    int hx = __double2hiint(x);
+    const int lx = __double2loint(x);
+    int k = (hx >> 20) - 1023;
+    hx &= 0x000fffff;
+    const int i = (hx + 0x95f64) & 0x100000;  // 1 when the mantissa exceeds sqrt(2): use x / 2
+    const double m = __hiloint2double(hx | (i ^ 0x3ff00000), lx);
+    k += i >> 20;
+    const double f = m - 1.0;
+    const double s = f / (2.0 + f);
+    const double dk = static_cast<double>(k);
+    const double z = s * s, w = z * z;
+    const double t1 = w * (3.999999999940941908e-01 + w * (2.222219843214978396e-01 + w * 1.531383769920937332e-01));
+    const double t2 = z * (6.666666666666735130e-01 +
+                           w * (2.857142874366239149e-01 + w * (1.818357216161805012e-01 + w * 1.479819860511658591e-01)));
+    const double hfsq = 0.5 * f * f;
+    return dk * 6.93147180369123816490e-01 - ((hfsq - (s * (hfsq + (t1 + t2)) + dk * 1.90821492927058770002e-10)) - f);
+}
+
+// cos(x) for x in [0, 2 pi]: x - q pi/2 by two fma (Cody-Waite; exact up to the
+// final rounding), then the fdlibm kernels on [-pi/4, pi/4]; < 1 ulp.
+__device__ __forceinline__ double cos_0_2pi(double x) {
+    const double q = rint(x * 0.6366197723675814);
+    double r = fma(-q, 1.5707963267948966, x);
+    r = fma(-q, 6.123233995736766e-17, r);
+    const double z = r * r;
+    const double rc = z * (4.16666666666666019037e-02 +
+                           z * (-1.38888888888741095749e-03 +
+                                z * (2.48015872894767294178e-05 +
+                                     z * (-2.75573143513906633035e-07 +
+                                          z * (2.08757232129817482790e-09 + z * -1.13596475577881948265e-11)))));
+    const double hz = 0.5 * z, w = 1.0 - hz;
+    const double c = w + (((1.0 - w) - hz) + z * rc);
+    const double rs = 8.33333333332248946124e-03 +
+                      z * (-1.98412698298579493134e-04 +
+                           z * (2.75573137070700676789e-06 + z * (-2.50507602534068634195e-08 + z * 1.58969099521155010221e-10)));
+    const double sn = r + (z * r) * (-1.66666666666666324348e-01 + z * rs);
+    const int qi = static_cast<int>(q) & 3;  // cos(r + q pi/2)
+    const double v = (qi & 1) ? sn : c;
+    return (qi == 1 || qi == 2) ? -v : v;
+}
+
 __device__ __forceinline__ double box_muller(PhiloxOut r) {
     const unsigned long long a = (static_cast<unsigned long long>(r.x) << 32) | r.y;
     const unsigned long long b = (static_cast<unsigned long long>(r.z) << 32) | r.w;
     const double u1 = static_cast<double>((a >> 11) + 1ull) * 0x1p-53;
     const double u2 = static_cast<double>(b >> 11) * 0x1p-53;
-    return sqrt(-2.0 * log(u1)) * cos(6.283185307179586 * u2);
+    return sqrt(-2.0 * log_unit(u1)) * cos_0_2pi(6.283185307179586 * u2);
 }
 
 __device__ __forceinline__ double gaussian(uint32_t row, uint32_t sweep, uint32_t chain, uint32_t k0,

@@ -76,34 +76,45 @@ __device__ __forceinline__ S transpose_sum(S (&v)[V], int lane, int &held) {
     return v[0];
 }
 
+// the (a, b) coefficient pair of an entry in one (real) or two (complex) 16-B loads
+__device__ __forceinline__ ZW<double> ldg_ab(const ZW<double> *p) {
+    const double2 v = __ldg(reinterpret_cast<const double2 *>(p));
+    return ZW<double>{v.x, v.y};
+}
+__device__ __forceinline__ ZW<cd> ldg_ab(const ZW<cd> *p) {
+    const double2 a = __ldg(reinterpret_cast<const double2 *>(p));
+    const double2 b = __ldg(reinterpret_cast<const double2 *>(p) + 1);
+    return ZW<cd>{cd{a.x, a.y}, cd{b.x, b.y}};
+}
+
 template <typename S>
 __device__ __forceinline__ ZW<S> ld_zw(const ZW<S> *p) {
     return *p;  // coherent load: values written by other threads of the CTA before __syncthreads
 }
 
-// fma chains of Eq. (4)/(5) over entries [beg, end), KU loads in flight
+// fma chains of Eq. (4)/(5) over the cnt entries at beg, KU gathers in flight.
+// Branch-free: the entry arrays are padded by KU entries, so every load is
+// unconditional; slots past the row's end gather row 0 of this chain (an
+// L1-hot dummy) and their fma is predicated off, so the sums are exactly the
+// serial ones.
 template <typename S, int KU>
-__device__ __forceinline__ void row_sums(const Sweep3Params<S> &p, const ZW<S> *zcol, int beg, int end, S &az,
+__device__ __forceinline__ void row_sums(const Sweep3Params<S> &p, const ZW<S> *zcol, int beg, int cnt, S &az,
                                          S &aw) {
-    for (int e0 = beg; e0 < end; e0 += KU) {
+    for (int e0 = 0; e0 < cnt; e0 += KU) {
         int j[KU];
-        ZW<S> v[KU];
-        S a[KU], b[KU];
+        ZW<S> v[KU], ab[KU];
+#pragma unroll
+        for (int k = 0; k < KU; ++k) j[k] = __ldg(p.ent_col + beg + e0 + k);
+#pragma unroll
+        for (int k = 0; k < KU; ++k) {
+            v[k] = ld_zw(zcol + (int64_t)(e0 + k < cnt ? j[k] : 0) * p.ld);
+            ab[k] = ldg_ab(reinterpret_cast<const ZW<S> *>(p.ent_ab) + beg + e0 + k);
+        }
 #pragma unroll
         for (int k = 0; k < KU; ++k)
-            if (e0 + k < end) j[k] = __ldg(p.ent_col + e0 + k);
-#pragma unroll
-        for (int k = 0; k < KU; ++k)
-            if (e0 + k < end) {
-                v[k] = ld_zw(zcol + (int64_t)j[k] * p.ld);
-                a[k] = ldg_s(p.ent_ab + 2 * (e0 + k));
-                b[k] = ldg_s(p.ent_ab + 2 * (e0 + k) + 1);
-            }
-#pragma unroll
-        for (int k = 0; k < KU; ++k)
-            if (e0 + k < end) {
-                az = fma_s(a[k], v[k].z, az);
-                aw = fma_s(b[k], v[k].w, aw);
+            if (e0 + k < cnt) {
+                az = fma_s(ab[k].z, v[k].z, az);
+                aw = fma_s(ab[k].w, v[k].w, aw);
             }
     }
 }
@@ -123,7 +134,7 @@ template <typename S, int KU, int NT, int LGP>
 __global__ void __launch_bounds__(NT, 1) sweep3_kernel(const Sweep3Params<S> p) {
     constexpr int E = ScalarTraits<S>::kDoubles;
     constexpr int P = 1 << LGP;        // lanes of one SE group inside this CTA (<= C)
-    constexpr int V = P < 8 ? P : 8;   // products per transpose-reduction
+    constexpr int V = P < 8 ? P : 8;   // products per transpose-reduction (pairs of one entry)
     const int tid = threadIdx.x;
     const int B = blockDim.x;  // a multiple of 32 and of C
     const int lane = tid & 31;
@@ -135,7 +146,7 @@ __global__ void __launch_bounds__(NT, 1) sweep3_kernel(const Sweep3Params<S> p) 
     const bool active = chain < p.chains;
     const uint32_t gchain = p.chain0 + static_cast<uint32_t>(chain);
     const bool gleader = (c & (P - 1)) == 0;           // owner of a plain group sum
-    const bool towner = (lane & (P / V - 1)) == 0;     // owner of a transposed value
+    const bool towner = (lane & ((P > V ? P / V : 1) - 1)) == 0;  // owner of a transposed value
     const int64_t grp = chain >> p.lgG;                // SE group of this chain = its accumulator slot
     ZW<S> *__restrict__ zcol = p.zw + chain;
     const bool want_diag = p.outputs & OUT_DIAG, want_pat = p.outputs & OUT_PATTERN;
@@ -165,7 +176,7 @@ __global__ void __launch_bounds__(NT, 1) sweep3_kernel(const Sweep3Params<S> p) 
                     if (p.noise == 0) phi = gaussian(static_cast<uint32_t>(i), k, gchain, p.key0, p.key1);
                     else phi = p.noise == 2 ? 1.0 : 0.0;
                     S az = zero_s<S>(), aw = zero_s<S>();
-                    row_sums<S, KU>(p, zcol, beg, beg + cnt, az, aw);
+                    row_sums<S, KU>(p, zcol, beg, cnt, az, aw);
                     const S dl = ldg_s(p.ord_dsg + 2 * o), sg = ldg_s(p.ord_dsg + 2 * o + 1);
                     zi = fma_s(neg_s(dl), az, scale_s(sg, phi));
                     wi = fma_s(neg_s(conj_s(dl)), aw, scale_s(conj_s(sg), phi));
@@ -178,42 +189,49 @@ __global__ void __launch_bounds__(NT, 1) sweep3_kernel(const Sweep3Params<S> p) 
                 }
                 if (!sampling) continue;
                 const bool acc = valid && active;
+                if (want_diag || want_pat) {
+                    // z_i w_i^*: diag element i and pattern element (i, i)
+                    const S d = group_sum<P>(acc ? zwc_s(zi, wi) : zero_s<S>());
+                    if (acc && gleader) {
+                        if (want_diag) slot_red(sd + (int64_t)i * E, d);
+                        if (want_pat && rec.w >= 0) slot_red(sp + (int64_t)rec.w * E, d);
+                    }
+                }
                 if (want_pat) {
-                    // products of row i: [0] z_i w_i^*, [1 + 2e] z_i w_j^*, [2 + 2e] z_j w_i^* for the
-                    // lower neighbours j = col[beg + e], e < nlow
-                    const int nprod = acc ? 1 + 2 * (rec.z >> 16) : 0;
-                    const int nb = (__reduce_max_sync(0xffffffffu, nprod) + V - 1) / V;
-                    for (int b = 0; b < nb; ++b) {
-                        S v[V];
-#pragma unroll
-                        for (int q = 0; q < V; ++q) {
-                            const int idx = b * V + q;
-                            v[q] = zero_s<S>();
-                            if (idx == 0) {
-                                if (acc) v[q] = zwc_s(zi, wi);
-                            } else if (idx < nprod) {
-                                const ZW<S> u =
-                                    ld_zw(zcol + (int64_t)__ldg(p.ent_col + beg + ((idx - 1) >> 1)) * p.ld);
-                                v[q] = ((idx - 1) & 1) ? zwc_s(u.z, wi) : zwc_s(zi, u.w);
-                            }
+                    // z_i w_j^* and z_j w_i^* for the lower neighbours j = col[beg + e], e < nlow
+                    // (values final and L1-hot from the gathers above)
+                    const int nlow = acc ? rec.z >> 16 : 0;
+                    if constexpr (P == 1) {
+                        for (int e = 0; e < nlow; ++e) {
+                            const ZW<S> u = ld_zw(zcol + (int64_t)__ldg(p.ent_col + beg + e) * p.ld);
+                            const int2 pz = __ldg(p.ent_pz + beg + e);
+                            if (pz.x >= 0) slot_red(sp + (int64_t)pz.x * E, zwc_s(zi, u.w));
+                            if (pz.y >= 0) slot_red(sp + (int64_t)pz.y * E, zwc_s(u.z, wi));
                         }
-                        int held;
-                        const S x = transpose_sum<P, V>(v, lane, held);
-                        const int idx = b * V + held;
-                        if (towner && idx < nprod) {
-                            if (idx == 0) {
-                                if (want_diag) slot_red(sd + (int64_t)i * E, x);
-                                if (rec.w >= 0) slot_red(sp + (int64_t)rec.w * E, x);
-                            } else {
-                                const int2 pz = __ldg(p.ent_pz + beg + ((idx - 1) >> 1));
-                                const int slot = ((idx - 1) & 1) ? pz.y : pz.x;
+                    } else {
+                        constexpr int VE = V / 2;  // entries per transpose-reduction
+                        const int nb = (__reduce_max_sync(0xffffffffu, nlow) + VE - 1) / VE;
+                        for (int b = 0; b < nb; ++b) {
+                            S v[V];
+#pragma unroll
+                            for (int q = 0; q < VE; ++q) {
+                                const int e = b * VE + q;
+                                const int jc = __ldg(p.ent_col + beg + e);  // padded: always in bounds
+                                const bool ok = e < nlow;
+                                const ZW<S> u = ld_zw(zcol + (int64_t)(ok ? jc : 0) * p.ld);
+                                v[2 * q] = ok ? zwc_s(zi, u.w) : zero_s<S>();
+                                v[2 * q + 1] = ok ? zwc_s(u.z, wi) : zero_s<S>();
+                            }
+                            int held;
+                            const S x = transpose_sum<P, V>(v, lane, held);
+                            const int e = b * VE + (held >> 1);
+                            if (towner && e < nlow) {
+                                const int2 pz = __ldg(p.ent_pz + beg + e);
+                                const int slot = (held & 1) ? pz.y : pz.x;
                                 if (slot >= 0) slot_red(sp + (int64_t)slot * E, x);
                             }
                         }
                     }
-                } else if (want_diag) {
-                    const S d = group_sum<P>(acc ? zwc_s(zi, wi) : zero_s<S>());
-                    if (acc && gleader) slot_red(sd + (int64_t)i * E, d);
                 }
             }
             if (sampling) {
@@ -273,12 +291,14 @@ namespace {
 
 template <typename S, int LGP>
 cudaError_t launch3(const Sweep3Params<S> &p, int threads, cudaStream_t st) {
-    // gathers in flight per row chunk: 64 registers at 1024 threads, 128 at 512
+    // gathers in flight per row chunk: 64 registers at 1024 threads, 85 at 768, 128 at 512
+    // (the entry arrays are padded by 8 entries: KU <= 8)
     constexpr int KS = ScalarTraits<S>::kDoubles == 1 ? 4 : 2;
     const int C = 1 << p.lgC;
     const int blocks = (p.chains + C - 1) / C;
     const size_t smem = (p.outputs & OUT_TRACE) ? (size_t)threads * sizeof(S) : 0;
     if (threads <= 512) sweep3_kernel<S, 2 * KS, 512, LGP><<<blocks, threads, smem, st>>>(p);
+    else if (threads <= 768) sweep3_kernel<S, KS, 768, LGP><<<blocks, threads, smem, st>>>(p);
     else sweep3_kernel<S, KS, 1024, LGP><<<blocks, threads, smem, st>>>(p);
     return cudaGetLastError();
 }
