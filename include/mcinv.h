@@ -153,9 +153,9 @@ mcinv_status mcinv_stats(mcinv_ctx *ctx, int64_t *launches, double *sweep_ms, in
 
 /* Which sweep kernel the last mcinv_run used: version 3 = level-scheduled
  * kernel (sweep3.cu, the default) with chains_per_warp = chains per CTA and
- * steps_per_sweep = levels D; version 2 = step-scheduled kernel (sweep2.cu)
- * with C chains per warp and that many steps; version 1 = row-by-row kernel
- * (sweep.cu). MCINV_KERNEL=v1|v2|v3 in the environment forces one. */
+ * steps_per_sweep = levels D; version 1 = row-by-row kernel (sweep.cu, one
+ * thread per chain; the simple reference kernel). MCINV_KERNEL=v1|v3 in the
+ * environment forces one. */
 mcinv_status mcinv_kernel_info(const mcinv_ctx *ctx, int *version, int *chains_per_warp, int64_t *steps_per_sweep);
 
 /* ------------------------------------------------------------ test-only */
@@ -167,16 +167,6 @@ mcinv_status mcinv_debug_philox(int device, uint64_t seed, int64_t count, const 
 /* Box-Muller Gaussian of Philox(ctr, seed) for each counter (host arrays). */
 mcinv_status mcinv_debug_gaussian(int device, uint64_t seed, int64_t count, const uint32_t *ctr4,
                                   double *out);
-/* Host-only (no GPU needed): run mcinv_create's preprocessing and the v2
- * step planner for C (and optional Q / pattern;
- * p_rows == NULL selects the default pattern) and copy the record tiles of
- * one sweep into `tiles` (NULL: size query). info[8] = {steps per sweep,
- * tile slot bytes, max items per step, tile bytes, segments, entries, near
- * entries, items}. For CPU tests of the planner. */
-mcinv_status mcinv_debug_plan(mcinv_dtype dtype, int64_t n, const int64_t *row_ptr, const int32_t *col_idx,
-                              const void *values, const int64_t *q_row_ptr, const int32_t *q_col_idx,
-                              const void *q_values, int64_t pcount, const int32_t *p_rows, const int32_t *p_cols,
-                              unsigned outputs, int chains_per_warp, void *tiles, size_t capacity, int64_t *info);
 /* Host-only (no GPU needed): mcinv_create's preprocessing and the level
  * planner of the v3 sweep kernel for C, with the
  * default pattern and an optional Q, for the accumulation of `outputs`.

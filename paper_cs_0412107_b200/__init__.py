@@ -72,9 +72,6 @@ SYMBOLS = {
                                           ctypes.c_void_p]),
     "mcinv_debug_gaussian": (ctypes.c_int, [ctypes.c_int, ctypes.c_uint64, ctypes.c_int64, ctypes.c_void_p,
                                             ctypes.c_void_p]),
-    "mcinv_debug_plan": (ctypes.c_int, [ctypes.c_int, ctypes.c_int64] + [ctypes.c_void_p] * 6 +
-                         [ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint, ctypes.c_int,
-                          ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
     "mcinv_debug_levels": (ctypes.c_int, [ctypes.c_int, ctypes.c_int64] + [ctypes.c_void_p] * 6 +
                            [ctypes.c_uint, ctypes.c_void_p, ctypes.c_void_p]),
     "mcinv_debug_get_state": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p,
@@ -129,39 +126,6 @@ def gaussian(ctr: np.ndarray, seed: int, device: int = 0) -> np.ndarray:
     out = np.zeros(ctr.shape[0], np.float64)
     _check(load().mcinv_debug_gaussian(device, seed, ctr.shape[0], ctr.ctypes.data, out.ctypes.data))
     return out
-
-
-def debug_plan(csr, chains_per_warp: int, outputs=("diag",), q=None, pattern=None):
-    """Host-only v2 plan (no GPU): (tiles bytes, info dict). For CPU tests."""
-    cplx = np.iscomplexobj(csr.val)
-    rp = np.ascontiguousarray(csr.row_ptr, np.int64)
-    col = np.ascontiguousarray(csr.col, np.int32)
-    val = _doubles(csr.val, cplx)
-    args = [C128 if cplx else F64, csr.n, rp.ctypes.data, col.ctypes.data, val.ctypes.data]
-    keep = [rp, col, val]
-    if q is not None:
-        qa = [np.ascontiguousarray(q.row_ptr, np.int64), np.ascontiguousarray(q.col, np.int32), _doubles(q.val, cplx)]
-        keep += qa
-        args += [a.ctypes.data for a in qa]
-    else:
-        args += [None, None, None]
-    if pattern is not None:
-        pr = np.ascontiguousarray(pattern[0], np.int32)
-        pc = np.ascontiguousarray(pattern[1], np.int32)
-        keep += [pr, pc]
-        args += [pr.size, pr.ctypes.data, pc.ctypes.data]
-    else:
-        args += [0, None, None]
-    bits = 0
-    for o in outputs:
-        bits |= OUTPUTS[o]
-    info = np.zeros(8, np.int64)
-    L = load()
-    _check(L.mcinv_debug_plan(*args, bits, chains_per_warp, None, 0, info.ctypes.data))
-    buf = np.zeros(int(info[3]), np.uint8)
-    _check(L.mcinv_debug_plan(*args, bits, chains_per_warp, buf.ctypes.data, buf.size, info.ctypes.data))
-    names = ["steps", "tile_slot", "max_items", "bytes", "segments", "entries", "near", "items"]
-    return buf, dict(zip(names, (int(x) for x in info)))
 
 
 def debug_levels(csr, outputs=("diag",), q=None):

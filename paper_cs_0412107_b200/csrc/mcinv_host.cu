@@ -21,7 +21,6 @@
 #include "../../include/mcinv.h"
 #include "mcinv_internal.cuh"
 #include "levels.h"
-#include "plan.h"
 
 using mcinv::cd;
 using mcinv::ZW;
@@ -42,13 +41,6 @@ struct DevBuf {
 struct Entry {
     int j;
     std::complex<double> v;
-};
-
-struct PlanDev {
-    DevBuf tiles, tile_off;
-    int steps = 0, tile_slot = 0, max_items = 0, C = 32;
-    std::string error;  // non-empty: plan not usable, v1 kernel is used
-    mcinv::HostPlan stats;
 };
 
 // Device copy of the level schedule (levels.h) for the v3 kernel.
@@ -81,22 +73,21 @@ struct mcinv_ctx {
     std::string err;
     int64_t err_index = -1;
     bool valid = false;
-    bool host_only = false;  // mcinv_debug_plan: no device allocations
+    bool host_only = false;  // mcinv_debug_levels: no device allocations
 
     // host canonical C (rows sorted, duplicates summed), kept for the default pattern
     std::vector<int64_t> h_rp;
     std::vector<int> h_col;
-    // host copies for the v2 planner (plan.h)
+    // host copies for the level planner (levels.h)
     std::vector<int> h_u_ptr, h_u_col;
     std::vector<std::complex<double>> h_u_a, h_u_b, h_delta, h_sigma;
     std::vector<int> h_prow, h_pcol;
     std::vector<int64_t> h_q_ptr;
     std::vector<int> h_q_col;
     std::vector<std::complex<double>> h_q_val;
-    std::map<std::tuple<int, unsigned>, std::unique_ptr<PlanDev>> plans;  // (C, outputs) -> plan
     std::map<unsigned, std::unique_ptr<LevelDev>> levels;                 // outputs -> level schedule
     int nsm = 148;
-    int last_kernel = 0;  // 1 = v1, 2 = v2
+    int last_kernel = 0;  // 1 = v1 (row by row), 3 = v3 (level schedule)
     int last_C = 0;
     int64_t last_steps = 0;
     // device C
@@ -310,7 +301,6 @@ mcinv_status build_pattern(mcinv_ctx *ctx, int64_t count, const int32_t *rows, c
     idx.resize(std::max<int64_t>(count, 1));
     ctx->h_prow.assign(rows, rows + count);
     ctx->h_pcol.assign(cols, cols + count);
-    ctx->plans.clear();
     ctx->levels.clear();
     TRY(upload(ctx, ctx->p_ptr, ptr));
     TRY(upload(ctx, ctx->p_idx, idx));
@@ -343,7 +333,6 @@ mcinv_status build_q(mcinv_ctx *ctx, const std::vector<std::vector<Entry>> &rows
         }
         ctx->h_q_ptr[i + 1] = (int64_t)ctx->h_q_col.size();
     }
-    ctx->plans.clear();
     ctx->levels.clear();
     for (int64_t i = 0; i < n; ++i) {
         for (const Entry &e : rows[i]) {
@@ -419,11 +408,10 @@ mcinv_status check_args(const mcinv_ctx *ctx_c, const mcinv_run_args *a) {
     return MCINV_OK;
 }
 
-int kernel_pref() {  // 0 auto (v3), 1 force v1, 2 force v2, 3 force v3
+int kernel_pref() {  // 0 auto (v3), 1 force v1, 3 force v3
     const char *e = std::getenv("MCINV_KERNEL");
     if (!e) return 0;
     if (!std::strcmp(e, "v1")) return 1;
-    if (!std::strcmp(e, "v2")) return 2;
     if (!std::strcmp(e, "v3")) return 3;
     return 0;
 }
@@ -502,63 +490,6 @@ Layout make_layout(const mcinv_ctx *ctx, const mcinv_run_args *a) {
     return L;
 }
 
-int choose_C(int64_t ld) {
-    // rows of a step (R = 32 / C) give intra-chain parallelism when chains are
-    // few; many chains fill the GPU by themselves (C = 32, fully coalesced)
-    if (const char *e = std::getenv("MCINV_C")) return std::atoi(e);
-    if (ld >= 32 * 148) return 32;
-    if (ld >= 16 * 148) return 16;
-    return 8;
-}
-
-
-template <typename S>
-PlanDev *get_plan(mcinv_ctx *ctx, int C, unsigned outputs) {
-    const unsigned key_out = outputs & (MCINV_DIAG | MCINV_PATTERN | MCINV_TRACE);
-    auto key = std::make_tuple(C, key_out);
-    auto it = ctx->plans.find(key);
-    if (it != ctx->plans.end()) return it->second.get();
-    std::unique_ptr<PlanDev> pd(new PlanDev());
-    pd->C = C;
-    mcinv::PlanInput in;
-    in.n = ctx->n;
-    in.cplx = ctx->dtype == MCINV_C128;
-    in.u_ptr = &ctx->h_u_ptr;
-    in.u_col = &ctx->h_u_col;
-    in.u_a = &ctx->h_u_a;
-    in.u_b = &ctx->h_u_b;
-    in.delta = &ctx->h_delta;
-    in.sigma = &ctx->h_sigma;
-    in.want_diag = key_out & MCINV_DIAG;
-    in.want_pattern = key_out & MCINV_PATTERN;
-    in.want_trace = key_out & MCINV_TRACE;
-    in.p_row = &ctx->h_prow;
-    in.p_col = &ctx->h_pcol;
-    in.q_ptr = &ctx->h_q_ptr;
-    in.q_col = &ctx->h_q_col;
-    in.q_val = &ctx->h_q_val;
-    mcinv::HostPlan hp;
-    pd->error = mcinv::build_plan(in, 32 / C, C, hp);
-    if (pd->error.empty()) {
-        const size_t smem = mcinv::sweep2_smem<S>(hp.tile_slot_bytes, hp.max_parts);
-        if (smem > 227 * 1024) pd->error = "plan needs " + std::to_string(smem) + " B of shared memory";
-    }
-    if (pd->error.empty()) {
-        if (upload(ctx, pd->tiles, hp.tiles) != MCINV_OK || upload(ctx, pd->tile_off, hp.tile_off) != MCINV_OK)
-            pd->error = "plan upload failed";
-        pd->steps = hp.steps;
-        pd->tile_slot = hp.tile_slot_bytes;
-        pd->max_items = hp.max_parts;
-        if (!ctx->host_only) {
-            hp.tiles.clear();
-            hp.tiles.shrink_to_fit();
-        }
-        pd->stats = std::move(hp);
-    }
-    PlanDev *raw = pd.get();
-    ctx->plans[key] = std::move(pd);
-    return raw;
-}
 
 template <typename S>
 LevelDev *get_levels(mcinv_ctx *ctx, unsigned outputs) {
@@ -675,19 +606,13 @@ mcinv_status run_typed(mcinv_ctx *ctx, const mcinv_run_args *a, const Layout &L,
         if (a->outputs & MCINV_FULL) CK(cudaMemsetAsync(ws + L.slot_full, 0, (size_t)L.G * n * n * sizeof(S), st));
         if (a->outputs & MCINV_TRACE) CK(cudaMemsetAsync(p.slot_trace, 0, (size_t)L.Gs * sizeof(S), st));
     }
-    // kernel choice (Layout::ver): v3 level schedule (default), v2 step schedule, v1 row by row
-    const int C = choose_C(L.ld);
-    PlanDev *plan = L.ver == 2 ? get_plan<S>(ctx, C, a->outputs) : nullptr;
-    const bool v2 = plan && plan->error.empty() &&
-                    (int64_t)plan->steps * (a->burn_in + a->cycles) < (int64_t(1) << 31);
-    if (L.ver == 2 && !v2)
-        return fail(ctx, MCINV_E_INVALID, "v2 kernel unavailable: " + (plan ? plan->error : std::string("no plan")));
+    // kernel choice (Layout::ver): v3 level schedule (default), v1 row by row
     LevelDev *lv = L.ver == 3 ? get_levels<S>(ctx, a->outputs) : nullptr;
     if (lv && !lv->error.empty()) return fail(ctx, MCINV_E_INVALID, "level schedule: " + lv->error);
     if (lv && L.lgP > L.lgC) return fail(ctx, MCINV_E_INVALID, "layout: group lanes exceed chains per CTA");
     ctx->last_kernel = L.ver;
-    ctx->last_C = v2 ? plan->C : (lv ? (1 << L.lgC) : 32);
-    ctx->last_steps = v2 ? plan->steps : (lv ? lv->D : n);
+    ctx->last_C = lv ? (1 << L.lgC) : 32;
+    ctx->last_steps = lv ? lv->D : n;
     Sweep3Params<S> q3{};
     int threads3 = 0;
     if (lv) {
@@ -732,29 +657,6 @@ mcinv_status run_typed(mcinv_ctx *ctx, const mcinv_run_args *a, const Layout &L,
         want = std::min<int64_t>(1024, std::max<int64_t>(want, int64_t(1) << L.lgC));
         threads3 = (int)((want + 31) / 32 * 32);
     }
-    Sweep2Params<S> q2{};
-    if (v2) {
-        q2.tiles = (const unsigned char *)plan->tiles.p;
-        q2.tile_off = (const int64_t *)plan->tile_off.p;
-        q2.steps = plan->steps;
-        q2.tile_slot = plan->tile_slot;
-        q2.max_items = plan->max_items;
-        q2.zw = p.zw;
-        q2.n = (int)n;
-        q2.ld = L.ld;
-        q2.chains = p.chains;
-        q2.chain0 = p.chain0;
-        q2.key0 = p.key0;
-        q2.key1 = p.key1;
-        q2.noise = p.noise;
-        q2.sweep_abs0 = p.sweep_abs0;
-        q2.burn_in = p.burn_in;
-        q2.gs = p.gs;
-        q2.pcount = (int)ctx->pcount;
-        q2.slot_diag = p.slot_diag;
-        q2.slot_pat = p.slot_pat;
-        q2.slot_trace = p.slot_trace;
-    }
     cudaError_t lerr = cudaSuccess;
     auto sweep = [&](int s0, int s1, int snap_s0, unsigned outs) {
         if (lv) {
@@ -767,18 +669,6 @@ mcinv_status run_typed(mcinv_ctx *ctx, const mcinv_run_args *a, const Layout &L,
             q.snap_y = (S *)(ws + L.snap_y);
             timed(ctx, 0, st, [&] {
                 cudaError_t e = launch_sweep3<S>(q, threads3, st);
-                if (e != cudaSuccess) lerr = e;
-            });
-        } else if (v2) {
-            Sweep2Params<S> q = q2;
-            q.s_begin = s0;
-            q.s_end = s1;
-            q.snap_s0 = snap_s0;
-            q.outputs = outs;
-            q.snap_x = (S *)(ws + L.snap_x);
-            q.snap_y = (S *)(ws + L.snap_y);
-            timed(ctx, 0, st, [&] {
-                cudaError_t e = launch_sweep2<S>(q, plan->C, st);
                 if (e != cudaSuccess) lerr = e;
             });
         } else {
@@ -1008,19 +898,6 @@ mcinv_status mcinv_result(mcinv_ctx *ctx, unsigned output, int64_t total_chains,
     double bad = 0.0;
     CK(cudaMemcpyAsync(&bad, mom + L.mom_count - 1, sizeof(double), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    if (ctx->last_kernel == 2) {
-        unsigned int dbg[38] = {0};
-        if (mcinv::sweep2_debug(dbg)) {
-            std::fprintf(stderr,
-                         "mcinv: sweep2 protocol watchdog: block %u warp %u barrier +%u parity %u step %u\n",
-                         dbg[0], dbg[1], dbg[2] - dbg[5], dbg[3], dbg[4]);
-            for (int w = 0; w < 8; ++w)
-                if (dbg[6 + 4 * w + 3])
-                    std::fprintf(stderr, "mcinv:   warp %d waited on barrier +%u parity %u step %u\n", w,
-                                 dbg[6 + 4 * w] - dbg[5], dbg[6 + 4 * w + 1], dbg[6 + 4 * w + 2]);
-            return fail(ctx, MCINV_E_CUDA, "sweep kernel protocol watchdog fired", (int64_t)dbg[4]);
-        }
-    }
     if (bad > 0.0) return fail(ctx, MCINV_E_DIVERGED, "state non-finite or above 1e12", (int64_t)bad);
     return MCINV_OK;
 }
@@ -1067,51 +944,6 @@ mcinv_status mcinv_stats(mcinv_ctx *ctx, int64_t *launches, double *sweep_ms, in
     if (contract_ms) *contract_ms = ms[1];
     if (contract_launches) *contract_launches = cnt[1];
     ctx->launches = 0;
-    return MCINV_OK;
-}
-
-mcinv_status mcinv_debug_plan(mcinv_dtype dtype, int64_t n, const int64_t *row_ptr, const int32_t *col_idx,
-                              const void *values, const int64_t *q_row_ptr, const int32_t *q_col_idx,
-                              const void *q_values, int64_t pcount, const int32_t *p_rows, const int32_t *p_cols,
-                              unsigned outputs, int chains_per_warp, void *tiles, size_t capacity, int64_t *info) {
-    if (!info) return MCINV_E_INVALID;
-    if (chains_per_warp != 8 && chains_per_warp != 16 && chains_per_warp != 32) return MCINV_E_INVALID;
-    mcinv_ctx c;
-    mcinv_ctx *ctx = &c;
-    ctx->host_only = true;
-    ctx->dtype = dtype;
-    ctx->n = n;
-    if (dtype != MCINV_F64 && dtype != MCINV_C128) return MCINV_E_INVALID;
-    if (n < 1 || n >= (int64_t(1) << 31)) return MCINV_E_INVALID;
-    std::vector<std::vector<Entry>> rows;
-    TRY(read_csr(ctx, n, row_ptr, col_idx, (const double *)values, dtype == MCINV_C128, rows));
-    TRY(dtype == MCINV_C128 ? build_matrix<cd>(ctx, rows) : build_matrix<double>(ctx, rows));
-    if (p_rows) TRY(build_pattern(ctx, pcount, p_rows, p_cols));
-    else TRY(default_pattern(ctx));
-    if (q_row_ptr) {
-        std::vector<std::vector<Entry>> qrows;
-        TRY(read_csr(ctx, n, q_row_ptr, q_col_idx, (const double *)q_values, dtype == MCINV_C128, qrows));
-        TRY(dtype == MCINV_C128 ? build_q<cd>(ctx, qrows) : build_q<double>(ctx, qrows));
-    }
-    PlanDev *pd = dtype == MCINV_C128 ? get_plan<cd>(ctx, chains_per_warp, outputs)
-                                      : get_plan<double>(ctx, chains_per_warp, outputs);
-    if (!pd->error.empty()) {
-        std::fprintf(stderr, "mcinv_debug_plan: %s\n", pd->error.c_str());
-        return MCINV_E_INVALID;
-    }
-    const mcinv::HostPlan &hp = pd->stats;
-    info[0] = hp.steps;
-    info[1] = hp.tile_slot_bytes;
-    info[2] = hp.max_parts;
-    info[3] = (int64_t)hp.tiles.size();
-    info[4] = hp.segments;
-    info[5] = hp.entries;
-    info[6] = hp.near_entries;
-    info[7] = hp.parts;
-    if (tiles) {
-        if (capacity < hp.tiles.size()) return MCINV_E_BUFFER;
-        std::memcpy(tiles, hp.tiles.data(), hp.tiles.size());
-    }
     return MCINV_OK;
 }
 

@@ -85,34 +85,6 @@ template <typename S> struct SweepParams {
 template <typename S>
 void launch_sweep(const SweepParams<S> &p, cudaStream_t st);
 
-// v2 sweep kernel on a step schedule (plan.h / sweep2.cu)
-template <typename S>
-struct Sweep2Params {
-    const unsigned char *tiles;  // device tiles (global)
-    const int64_t *tile_off;     // [steps + 1]
-    int steps;                   // steps per sweep
-    int tile_slot;               // smem bytes per tile slot
-    int max_items;
-    ZW<S> *zw;
-    int n, ld, chains;
-    uint32_t chain0, key0, key1;
-    int noise;
-    uint32_t sweep_abs0;
-    int s_begin, s_end, burn_in;
-    unsigned outputs;
-    int gs;
-    int pcount;
-    double *slot_diag, *slot_pat, *slot_trace;
-    S *snap_x, *snap_y;
-    int snap_s0;
-};
-
-template <typename S>
-cudaError_t launch_sweep2(const Sweep2Params<S> &p, int C, cudaStream_t st);
-template <typename S>
-size_t sweep2_smem(int tile_slot, int max_items);
-int sweep2_debug(unsigned int *dbg);
-
 // v3 sweep kernel on the level schedule (levels.h / sweep3.cu). Arrays are in
 // level order; see LevelPlan for their meaning.
 template <typename S>

@@ -236,14 +236,13 @@ def test_errors(mc):
     assert e.value.code == 8
 
 
-@pytest.mark.parametrize("kernel", ["v1", "v2", "v3"])
+@pytest.mark.parametrize("kernel", ["v1", "v3"])
 def test_both_kernels(mc, orc, kernel, monkeypatch):
-    """The row-by-row kernel (v1), the step-scheduled kernel (v2) and the
-    level-scheduled kernel (v3) all match the oracle, for every chains-per-warp
-    (v2) / chains-per-CTA (v3) layout: C below, equal to and above the group
-    size (accumulator sub-slots) and above a warp."""
+    """The row-by-row kernel (v1) and the level-scheduled kernel (v3) both
+    match the oracle; v3 for every chains-per-CTA layout: C below, equal to
+    and above the group size and above a warp."""
     monkeypatch.setenv("MCINV_KERNEL", kernel)
-    Cs = {"v1": (32,), "v2": (8, 16, 32), "v3": (1, 4, 8, 32, 64)}[kernel]
+    Cs = {"v1": (32,), "v3": (1, 4, 8, 32, 64)}[kernel]
     for C in Cs:
         monkeypatch.setenv("MCINV_C", str(C))
         compare_run(mc, orc, W.pedigree(500, seed=21), seed=4, chains=64, burn_in=2, cycles=4,
