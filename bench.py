@@ -164,12 +164,14 @@ def algorithmic_bytes_per_chain_sweep(c) -> int:
 
 
 def committed_traffic(workload: str):
-    """dram bytes per sweep launch from the committed ncu --set full summary."""
+    """DRAM bytes (read + write) per site-update of the sweep kernel, from the
+    committed `ncu --set full` summary (profiles/ncu_summary.json; captured on a
+    shorter launch of the same shape, so it is stored per site-update)."""
     path = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(path) as f:
             d = json.load(f)
-        return d.get(workload, {}).get("dram_bytes_per_launch")
+        return d.get(workload, {}).get("dram_bytes_per_site")
     except (OSError, ValueError):
         return None
 
@@ -267,9 +269,11 @@ def ours_arm(args):
     if sweeps_per_launch:
         bytes_launch = b_chain_sweep * chains * sweeps_per_launch
         achieved = bytes_launch / (sweep_launch_ms / 1e3) / 1e9
-        tr = committed_traffic(name)
+        tps = committed_traffic(name)
+        tr = tps * chains * c.n * sweeps_per_launch if tps else None
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": tr, "kernel": "sweep_kernel (K1)", "peak_source": peak_src,
+                "traffic": tr, "traffic_bytes_per_site": tps, "kernel": "sweep3_kernel (K1/K2, v3)",
+                "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": bytes_launch,
                 "algorithmic_bytes_per_site": b_chain_sweep / c.n,
                 "sweep_ms_per_launch": sweep_launch_ms,
