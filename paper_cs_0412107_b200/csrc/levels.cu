@@ -43,10 +43,15 @@ std::string build_levels(const LevelInput &in, LevelPlan &P) {
     P.D = D;
     const int nph = D + 1;
 
-    // rows in level order (ascending i within a level)
+    // rows in level order; within a level (mutually independent rows, any order
+    // is exact) by decreasing entry count, so the rows sharing a warp have
+    // similar loop trip counts (less SIMT divergence); ties by ascending i
     std::vector<int> key(P.level.begin(), P.level.end());
     P.ord_row = bucket(key, nph, P.ph_row);
     P.ph_row.push_back(P.ph_row.back());  // [D+2]; phase D holds no rows
+    for (int l = 0; l < D; ++l)
+        std::stable_sort(P.ord_row.begin() + P.ph_row[l], P.ord_row.begin() + P.ph_row[l + 1],
+                         [&](int x, int y) { return up[x + 1] - up[x] > up[y + 1] - up[y]; });
 
     // pattern slots: fused at the update of max(i, j) when min(i, j) is a lower
     // neighbour (or i == j); the first occurrence of a pair is fused, the rest

@@ -43,7 +43,7 @@ struct LevelPlan {
     int D = 0;                       // update levels; phases 0..D
     std::vector<int> level;          // lev(i), for tests
     std::vector<int> ph_row;         // [D+2] level-order row range of phase p (phase D: empty)
-    std::vector<int> ord_row;        // [n] rows in level order (ascending i within a level)
+    std::vector<int> ord_row;        // [n] rows in level order (decreasing entry count within a level)
     std::vector<int> ord_eptr;       // [n+1] entry range of level-order row o
     std::vector<int> ent_col;        // [nnz_u] union entries in level order
     std::vector<std::complex<double>> ent_a, ent_b;
