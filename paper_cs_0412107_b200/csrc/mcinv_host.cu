@@ -48,8 +48,17 @@ struct LevelDev {
     DevBuf ph_row, ord_rec, ent_col, ent_ab, ent_pz, ord_dsg;
     DevBuf ph_tq, tq_row, tq_eptr, tq_col, tq_val, ph_pp, pp_i, pp_j, pp_slot;
     int D = 0, max_rows = 0;
+    bool deferred = false;                   // deferred items exist (v4 cannot run this plan)
     std::string error;
-    mcinv::LevelPlan host;  // kept only for mcinv_debug_levels
+    mcinv::LevelPlan host;                   // kept only for mcinv_debug_levels
+    std::vector<int4> h_rec;                 // level-order records, for the v4 slot arrays
+    std::vector<unsigned char> h_dsg;        // level-order {delta, sigma} (raw bytes of S)
+    std::vector<int> h_ph_row;
+    struct Slots {
+        DevBuf rec, dsg;
+        int nslots = 0;
+    };
+    std::map<int, std::unique_ptr<Slots>> slots;  // rows per warp group R -> padded slot arrays
 };
 
 struct Layout {
@@ -87,7 +96,8 @@ struct mcinv_ctx {
     std::vector<std::complex<double>> h_q_val;
     std::map<unsigned, std::unique_ptr<LevelDev>> levels;                 // outputs -> level schedule
     int nsm = 148;
-    int last_kernel = 0;  // 1 = v1 (row by row), 3 = v3 (level schedule)
+    int last_kernel = 0;  // 1 = v1 (row by row), 3 = v3 (level schedule), 4 = v4 (dataflow)
+    DevBuf err_flag;      // v4 watchdog flag (device unsigned)
     int last_C = 0;
     int64_t last_steps = 0;
     // device C
@@ -408,11 +418,12 @@ mcinv_status check_args(const mcinv_ctx *ctx_c, const mcinv_run_args *a) {
     return MCINV_OK;
 }
 
-int kernel_pref() {  // 0 auto (v3), 1 force v1, 3 force v3
+int kernel_pref() {  // 0 auto (v4 when eligible, else v3), 1 force v1, 3 force v3, 4 force v4
     const char *e = std::getenv("MCINV_KERNEL");
     if (!e) return 0;
     if (!std::strcmp(e, "v1")) return 1;
     if (!std::strcmp(e, "v3")) return 3;
+    if (!std::strcmp(e, "v4")) return 4;
     return 0;
 }
 
@@ -440,7 +451,7 @@ Layout make_layout(const mcinv_ctx *ctx, const mcinv_run_args *a) {
     L.ld = (int)((a->chains + 31) / 32 * 32);
     L.G = (int)(a->chains / a->group_size);
     const int pref = kernel_pref();
-    L.ver = pref == 0 ? 3 : pref;
+    L.ver = pref == 1 ? 1 : 3;  // v3 / v4 share the layout; run_typed picks v4 when eligible
     L.Gs = L.G;
     L.ksub = 1;
     if (L.ver == 3) {
@@ -562,10 +573,44 @@ LevelDev *get_levels(mcinv_ctx *ctx, unsigned outputs) {
         up(ld->pp_j, P.pp_j);
         up(ld->pp_slot, P.pp_slot);
         if (st != MCINV_OK && ld->error.empty()) ld->error = "level plan upload failed";
+        ld->deferred = !P.pp_i.empty() || !P.tq_row.empty();
+        ld->h_rec = rec;
+        ld->h_dsg.assign(reinterpret_cast<const unsigned char *>(dsg.data()),
+                         reinterpret_cast<const unsigned char *>(dsg.data() + dsg.size()));
+        ld->h_ph_row = P.ph_row;
         if (!ctx->host_only) P = mcinv::LevelPlan();  // device copy only
     }
     LevelDev *raw = ld.get();
     ctx->levels[key] = std::move(ld);
+    return raw;
+}
+
+// v4 slot arrays: level order with every level padded to a multiple of R rows
+// (a warp group of R rows never spans two levels, so its rows are independent)
+template <typename S>
+LevelDev::Slots *get_slots(mcinv_ctx *ctx, LevelDev *lv, int R) {
+    auto it = lv->slots.find(R);
+    if (it != lv->slots.end()) return it->second.get();
+    std::unique_ptr<LevelDev::Slots> sl(new LevelDev::Slots());
+    std::vector<int4> rec;
+    std::vector<S> dsg;
+    const S *hd = reinterpret_cast<const S *>(lv->h_dsg.data());
+    for (int l = 0; l < lv->D; ++l) {
+        for (int o = lv->h_ph_row[l]; o < lv->h_ph_row[l + 1]; ++o) {
+            rec.push_back(lv->h_rec[o]);
+            dsg.push_back(hd[2 * o]);
+            dsg.push_back(hd[2 * o + 1]);
+        }
+        while (rec.size() % R) {
+            rec.push_back(make_int4(-1, 0, 0, -1));
+            dsg.push_back(S{});
+            dsg.push_back(S{});
+        }
+    }
+    sl->nslots = (int)rec.size();
+    if (upload(ctx, sl->rec, rec) != MCINV_OK || upload(ctx, sl->dsg, dsg) != MCINV_OK) return nullptr;
+    LevelDev::Slots *raw = sl.get();
+    lv->slots[R] = std::move(sl);
     return raw;
 }
 
@@ -610,7 +655,20 @@ mcinv_status run_typed(mcinv_ctx *ctx, const mcinv_run_args *a, const Layout &L,
     LevelDev *lv = L.ver == 3 ? get_levels<S>(ctx, a->outputs) : nullptr;
     if (lv && !lv->error.empty()) return fail(ctx, MCINV_E_INVALID, "level schedule: " + lv->error);
     if (lv && L.lgP > L.lgC) return fail(ctx, MCINV_E_INVALID, "layout: group lanes exceed chains per CTA");
-    ctx->last_kernel = L.ver;
+    // v4 (dataflow) when the chains of a row fit one warp, the per-row counters fit
+    // shared memory and the plan has no deferred items (trace, non-neighbour pairs)
+    const int pref = kernel_pref();
+    const bool v4_ok = lv && L.lgC <= 5 && n <= 200000 && !lv->deferred;
+    if (pref == 4 && !v4_ok) return fail(ctx, MCINV_E_INVALID, "v4 kernel not applicable to this run");
+    const bool v4 = v4_ok && (pref == 0 || pref == 4);
+    LevelDev::Slots *sl = v4 ? get_slots<S>(ctx, lv, 32 >> L.lgC) : nullptr;
+    if (v4 && !sl) return fail(ctx, MCINV_E_NOMEM, "v4 slot arrays");
+    if (v4 && !ctx->err_flag.p) {
+        if (cudaMalloc(&ctx->err_flag.p, 16) != cudaSuccess) return fail(ctx, MCINV_E_NOMEM, "v4 flag");
+        ctx->err_flag.bytes = 16;
+    }
+    if (v4) CK(cudaMemsetAsync(ctx->err_flag.p, 0, 16, st));
+    ctx->last_kernel = v4 ? 4 : L.ver;
     ctx->last_C = lv ? (1 << L.lgC) : 32;
     ctx->last_steps = lv ? lv->D : n;
     Sweep3Params<S> q3{};
@@ -649,6 +707,12 @@ mcinv_status run_typed(mcinv_ctx *ctx, const mcinv_run_args *a, const Layout &L,
         q3.slot_diag = p.slot_diag;
         q3.slot_pat = p.slot_pat;
         q3.slot_trace = p.slot_trace;
+        if (sl) {
+            q3.slot_rec = (const int4 *)sl->rec.p;
+            q3.slot_dsg = (const S *)sl->dsg.p;
+            q3.nslots = sl->nslots;
+            q3.err = (unsigned *)ctx->err_flag.p;
+        }
         // threads: enough for the widest phase x C, a multiple of 32 and of C, <= 768 (85
         // registers per thread: measured best for configs 2-5)
         int64_t want = (int64_t)std::max(lv->max_rows, 1) << L.lgC;
@@ -668,7 +732,7 @@ mcinv_status run_typed(mcinv_ctx *ctx, const mcinv_run_args *a, const Layout &L,
             q.snap_x = (S *)(ws + L.snap_x);
             q.snap_y = (S *)(ws + L.snap_y);
             timed(ctx, 0, st, [&] {
-                cudaError_t e = launch_sweep3<S>(q, threads3, st);
+                cudaError_t e = v4 ? launch_sweep4<S>(q, threads3, st) : launch_sweep3<S>(q, threads3, st);
                 if (e != cudaSuccess) lerr = e;
             });
         } else {
@@ -898,6 +962,11 @@ mcinv_status mcinv_result(mcinv_ctx *ctx, unsigned output, int64_t total_chains,
     double bad = 0.0;
     CK(cudaMemcpyAsync(&bad, mom + L.mom_count - 1, sizeof(double), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    if (ctx->last_kernel == 4) {
+        unsigned wd = 0;
+        CK(cudaMemcpy(&wd, ctx->err_flag.p, sizeof(wd), cudaMemcpyDeviceToHost));
+        if (wd) return fail(ctx, MCINV_E_CUDA, "v4 dataflow watchdog: a dependency wait exceeded its bound");
+    }
     if (bad > 0.0) return fail(ctx, MCINV_E_DIVERGED, "state non-finite or above 1e12", (int64_t)bad);
     return MCINV_OK;
 }

@@ -114,10 +114,19 @@ struct Sweep3Params {
     double *slot_diag, *slot_pat, *slot_trace;  // [groups][count] (x e doubles)
     S *snap_x, *snap_y;
     int snap_s0;
+    // v4 (dataflow) only: level-order rows padded per level to whole warp groups of
+    // R = 32 / C rows; slot_rec.x = -1 marks padding
+    const int4 *slot_rec;
+    const S *slot_dsg;
+    int nslots;
+    unsigned *err;        // set (watchdog) if a dependency wait exceeds its bound
 };
 
 template <typename S>
 cudaError_t launch_sweep3(const Sweep3Params<S> &p, int threads, cudaStream_t st);
+// v4: per-row completion counters in shared memory instead of per-level barriers
+template <typename S>
+cudaError_t launch_sweep4(const Sweep3Params<S> &p, int threads, cudaStream_t st);
 
 // A_g[i][j] += sum_{t < T, c in group g} X[t][i][c] conj(Y[t][j][c]).
 template <typename S>

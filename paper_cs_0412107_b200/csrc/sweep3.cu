@@ -128,6 +128,61 @@ __device__ __forceinline__ void slot_red(double *slot, cd v) {
     red_add(slot + 1, v.im);
 }
 
+// Fused accumulation of row i's products in a sampling sweep (Eq. 1/C,
+// P:173-176): z_i w_i^* into the diag slot and the pattern slot of (i, i);
+// z_i w_j^* and z_j w_i^* for the lower neighbours j (final values, L1-hot
+// from the gathers) into their pattern slots. Called by all 32 lanes of a
+// converged warp (acc = false for lanes without a valid, active item).
+template <typename S, int P, int V>
+__device__ __forceinline__ void accumulate_row(const Sweep3Params<S> &p, const ZW<S> *zcol, int4 rec, S zi, S wi,
+                                               bool acc, int lane, bool gleader, bool towner, double *sd,
+                                               double *sp, bool want_diag, bool want_pat) {
+    constexpr int E = ScalarTraits<S>::kDoubles;
+    const int i = rec.x, beg = rec.y;
+    if (want_diag || want_pat) {
+        // z_i w_i^*: diag element i and pattern element (i, i)
+        const S d = group_sum<P>(acc ? zwc_s(zi, wi) : zero_s<S>());
+        if (acc && gleader) {
+            if (want_diag) slot_red(sd + (int64_t)i * E, d);
+            if (want_pat && rec.w >= 0) slot_red(sp + (int64_t)rec.w * E, d);
+        }
+    }
+    if (!want_pat) return;
+    // z_i w_j^* and z_j w_i^* for the lower neighbours j = col[beg + e], e < nlow
+    const int nlow = acc ? rec.z >> 16 : 0;
+    if constexpr (P == 1) {
+        for (int e = 0; e < nlow; ++e) {
+            const ZW<S> u = ld_zw(zcol + (int64_t)__ldg(p.ent_col + beg + e) * p.ld);
+            const int2 pz = __ldg(p.ent_pz + beg + e);
+            if (pz.x >= 0) slot_red(sp + (int64_t)pz.x * E, zwc_s(zi, u.w));
+            if (pz.y >= 0) slot_red(sp + (int64_t)pz.y * E, zwc_s(u.z, wi));
+        }
+    } else {
+        constexpr int VE = V / 2;  // entries per transpose-reduction
+        const int nb = (__reduce_max_sync(0xffffffffu, nlow) + VE - 1) / VE;
+        for (int b = 0; b < nb; ++b) {
+            S v[V];
+#pragma unroll
+            for (int q = 0; q < VE; ++q) {
+                const int e = b * VE + q;
+                const int jc = __ldg(p.ent_col + beg + e);  // padded: always in bounds
+                const bool ok = e < nlow;
+                const ZW<S> u = ld_zw(zcol + (int64_t)(ok ? jc : 0) * p.ld);
+                v[2 * q] = ok ? zwc_s(zi, u.w) : zero_s<S>();
+                v[2 * q + 1] = ok ? zwc_s(u.z, wi) : zero_s<S>();
+            }
+            int held;
+            const S x = transpose_sum<P, V>(v, lane, held);
+            const int e = b * VE + (held >> 1);
+            if (towner && e < nlow) {
+                const int2 pz = __ldg(p.ent_pz + beg + e);
+                const int slot = (held & 1) ? pz.y : pz.x;
+                if (slot >= 0) slot_red(sp + (int64_t)slot * E, x);
+            }
+        }
+    }
+}
+
 }  // namespace
 
 template <typename S, int KU, int NT, int LGP>
@@ -188,51 +243,8 @@ __global__ void __launch_bounds__(NT, 1) sweep3_kernel(const Sweep3Params<S> p) 
                     }
                 }
                 if (!sampling) continue;
-                const bool acc = valid && active;
-                if (want_diag || want_pat) {
-                    // z_i w_i^*: diag element i and pattern element (i, i)
-                    const S d = group_sum<P>(acc ? zwc_s(zi, wi) : zero_s<S>());
-                    if (acc && gleader) {
-                        if (want_diag) slot_red(sd + (int64_t)i * E, d);
-                        if (want_pat && rec.w >= 0) slot_red(sp + (int64_t)rec.w * E, d);
-                    }
-                }
-                if (want_pat) {
-                    // z_i w_j^* and z_j w_i^* for the lower neighbours j = col[beg + e], e < nlow
-                    // (values final and L1-hot from the gathers above)
-                    const int nlow = acc ? rec.z >> 16 : 0;
-                    if constexpr (P == 1) {
-                        for (int e = 0; e < nlow; ++e) {
-                            const ZW<S> u = ld_zw(zcol + (int64_t)__ldg(p.ent_col + beg + e) * p.ld);
-                            const int2 pz = __ldg(p.ent_pz + beg + e);
-                            if (pz.x >= 0) slot_red(sp + (int64_t)pz.x * E, zwc_s(zi, u.w));
-                            if (pz.y >= 0) slot_red(sp + (int64_t)pz.y * E, zwc_s(u.z, wi));
-                        }
-                    } else {
-                        constexpr int VE = V / 2;  // entries per transpose-reduction
-                        const int nb = (__reduce_max_sync(0xffffffffu, nlow) + VE - 1) / VE;
-                        for (int b = 0; b < nb; ++b) {
-                            S v[V];
-#pragma unroll
-                            for (int q = 0; q < VE; ++q) {
-                                const int e = b * VE + q;
-                                const int jc = __ldg(p.ent_col + beg + e);  // padded: always in bounds
-                                const bool ok = e < nlow;
-                                const ZW<S> u = ld_zw(zcol + (int64_t)(ok ? jc : 0) * p.ld);
-                                v[2 * q] = ok ? zwc_s(zi, u.w) : zero_s<S>();
-                                v[2 * q + 1] = ok ? zwc_s(u.z, wi) : zero_s<S>();
-                            }
-                            int held;
-                            const S x = transpose_sum<P, V>(v, lane, held);
-                            const int e = b * VE + (held >> 1);
-                            if (towner && e < nlow) {
-                                const int2 pz = __ldg(p.ent_pz + beg + e);
-                                const int slot = (held & 1) ? pz.y : pz.x;
-                                if (slot >= 0) slot_red(sp + (int64_t)slot * E, x);
-                            }
-                        }
-                    }
-                }
+                accumulate_row<S, P, V>(p, zcol, rec, zi, wi, valid && active, lane, gleader, towner, sd, sp,
+                                        want_diag, want_pat);
             }
             if (sampling) {
                 // ---- deferred trace items: conj(w_i) sum_j Q_ij z_j  (w^dagger Q z, reading R2);
@@ -287,6 +299,105 @@ __global__ void __launch_bounds__(NT, 1) sweep3_kernel(const Sweep3Params<S> p) 
     }
 }
 
+// ---------------------------------------------------------------- v4: dataflow
+//
+// The same row update and accumulation, without per-level barriers. Every row
+// j has a completion counter done[j] (shared memory, one byte, counted modulo
+// 256) = the number of sweeps of this launch's chains that have updated it.
+// Row i in sweep s may run once every lower neighbour j < i has done[j] >=
+// s + 1 (its new value, Eq. 4/5 read order) and every upper neighbour has
+// done[j] >= s: the upper neighbour has finished sweep s - 1, i.e. it has
+// read z_i of sweep s - 1 (write-after-read) and holds the value row i must
+// read. Neighbour counters differ by at most 2, so byte arithmetic is exact.
+// Each warp takes groups of R = 32 / C rows (never spanning a level: rows of
+// a group are independent) in increasing (sweep, level order); all
+// dependencies point to earlier groups, so the earliest unfinished group can
+// always run: no deadlock. A bounded wait (watchdog) reports instead of
+// hanging if that reasoning were ever violated.
+template <typename S, int KU, int NT, int LGP>
+__global__ void __launch_bounds__(NT, 1) sweep4_kernel(const Sweep3Params<S> p) {
+    constexpr int E = ScalarTraits<S>::kDoubles;
+    constexpr int P = 1 << LGP;
+    constexpr int V = P < 8 ? P : 8;
+    extern __shared__ __align__(16) unsigned char done[];  // [n]
+    const int tid = threadIdx.x;
+    const int B = blockDim.x;
+    const int lane = tid & 31;
+    const int lgC = p.lgC;  // C <= 32: the C lanes of a row are in one warp
+    const int C = 1 << lgC;
+    const int c = lane & (C - 1);
+    const int chain = (blockIdx.x << lgC) + c;
+    const bool active = chain < p.chains;
+    const uint32_t gchain = p.chain0 + static_cast<uint32_t>(chain);
+    const bool gleader = (c & (P - 1)) == 0;
+    const bool towner = (lane & ((P > V ? P / V : 1) - 1)) == 0;
+    const int64_t grp = chain >> p.lgG;
+    ZW<S> *__restrict__ zcol = p.zw + chain;
+    const bool want_diag = p.outputs & OUT_DIAG, want_pat = p.outputs & OUT_PATTERN;
+    const bool want_full = p.outputs & OUT_FULL;
+    double *const sd = p.slot_diag + grp * p.n * E;
+    double *const sp = p.slot_pat + grp * p.pcount * E;
+
+    for (int j = tid; j < p.n; j += B) done[j] = static_cast<unsigned char>(p.s_begin);
+    __syncthreads();
+
+    const int R = 32 >> lgC;
+    const int ngroups = p.nslots / R;
+    const int64_t total = (int64_t)(p.s_end - p.s_begin) * ngroups;
+    for (int64_t gi = tid >> 5; gi < total; gi += B >> 5) {
+        const int s = p.s_begin + (int)(gi / ngroups);
+        const int slot = (int)(gi % ngroups) * R + (lane >> lgC);
+        const uint32_t k = p.sweep_abs0 + static_cast<uint32_t>(s);
+        const bool sampling = s >= p.burn_in;
+        const int4 rec = __ldg(p.slot_rec + slot);
+        const bool valid = rec.x >= 0;
+        const int i = rec.x, beg = rec.y, cnt = valid ? rec.z & 0xffff : 0;
+        S zi = zero_s<S>(), wi = zero_s<S>();
+        if (valid) {
+            double phi;
+            if (p.noise == 0) phi = gaussian(static_cast<uint32_t>(i), k, gchain, p.key0, p.key1);
+            else phi = p.noise == 2 ? 1.0 : 0.0;
+            // dependency wait (all C lanes of the row read the same counters: smem broadcast)
+            const unsigned char lo = static_cast<unsigned char>(s + 1), hi = static_cast<unsigned char>(s);
+            for (int e = 0; e < cnt; ++e) {
+                const int j = __ldg(p.ent_col + beg + e);
+                const unsigned char need = j < i ? lo : hi;
+                const volatile unsigned char *f = done + j;
+                if (static_cast<signed char>(*f - need) < 0) {
+                    unsigned spins = 0;
+                    while (static_cast<signed char>(*f - need) < 0 && !*reinterpret_cast<volatile unsigned *>(p.err)) {
+                        __nanosleep(32);
+                        if (++spins > (1u << 26)) {  // ~seconds: report, do not hang
+                            atomicOr(p.err, 1u);
+                            break;
+                        }
+                    }
+                }
+            }
+            __threadfence_block();  // acquire: gathers after the counters
+            S az = zero_s<S>(), aw = zero_s<S>();
+            row_sums<S, KU>(p, zcol, beg, cnt, az, aw);
+            const S dl = ldg_s(p.slot_dsg + 2 * slot), sg = ldg_s(p.slot_dsg + 2 * slot + 1);
+            zi = fma_s(neg_s(dl), az, scale_s(sg, phi));
+            wi = fma_s(neg_s(conj_s(dl)), aw, scale_s(conj_s(sg), phi));
+            zcol[(int64_t)i * p.ld] = ZW<S>{zi, wi};
+            if (want_full && sampling) {
+                const int64_t ts = s - p.snap_s0;
+                p.snap_x[(ts * p.n + i) * p.ld + chain] = zi;
+                p.snap_y[(ts * p.n + i) * p.ld + chain] = wi;
+            }
+        }
+        __syncwarp();  // the row's C stores are ordered before its counter update
+        if (valid && c == 0) {
+            __threadfence_block();  // release
+            *reinterpret_cast<volatile unsigned char *>(done + i) = static_cast<unsigned char>(s + 1);
+        }
+        if (sampling)
+            accumulate_row<S, P, V>(p, zcol, rec, zi, wi, valid && active, lane, gleader, towner, sd, sp, want_diag,
+                                    want_pat);
+    }
+}
+
 namespace {
 
 template <typename S, int LGP>
@@ -305,6 +416,43 @@ cudaError_t launch3(const Sweep3Params<S> &p, int threads, cudaStream_t st) {
 
 }  // namespace
 
+template <typename S, int LGP>
+cudaError_t launch4(const Sweep3Params<S> &p, int threads, cudaStream_t st) {
+    constexpr int KS = ScalarTraits<S>::kDoubles == 1 ? 4 : 2;
+    const int C = 1 << p.lgC;
+    const int blocks = (p.chains + C - 1) / C;
+    const size_t smem = ((size_t)p.n + 15) / 16 * 16;
+    cudaError_t e;
+    if (threads <= 512) {
+        auto k = sweep4_kernel<S, 2 * KS, 512, LGP>;
+        e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e == cudaSuccess) k<<<blocks, threads, smem, st>>>(p);
+    } else if (threads <= 768) {
+        auto k = sweep4_kernel<S, KS, 768, LGP>;
+        e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e == cudaSuccess) k<<<blocks, threads, smem, st>>>(p);
+    } else {
+        auto k = sweep4_kernel<S, KS, 1024, LGP>;
+        e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e == cudaSuccess) k<<<blocks, threads, smem, st>>>(p);
+    }
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
+}
+
+template <typename S>
+cudaError_t launch_sweep4(const Sweep3Params<S> &p, int threads, cudaStream_t st) {
+    switch (p.lgP) {
+        case 0: return launch4<S, 0>(p, threads, st);
+        case 1: return launch4<S, 1>(p, threads, st);
+        case 2: return launch4<S, 2>(p, threads, st);
+        case 3: return launch4<S, 3>(p, threads, st);
+        case 4: return launch4<S, 4>(p, threads, st);
+        case 5: return launch4<S, 5>(p, threads, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
 template <typename S>
 cudaError_t launch_sweep3(const Sweep3Params<S> &p, int threads, cudaStream_t st) {
     switch (p.lgP) {
@@ -319,6 +467,8 @@ cudaError_t launch_sweep3(const Sweep3Params<S> &p, int threads, cudaStream_t st
 }
 
 template cudaError_t launch_sweep3<double>(const Sweep3Params<double> &, int, cudaStream_t);
+template cudaError_t launch_sweep4<double>(const Sweep3Params<double> &, int, cudaStream_t);
+template cudaError_t launch_sweep4<cd>(const Sweep3Params<cd> &, int, cudaStream_t);
 template cudaError_t launch_sweep3<cd>(const Sweep3Params<cd> &, int, cudaStream_t);
 
 }  // namespace mcinv

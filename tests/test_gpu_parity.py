@@ -252,6 +252,31 @@ def test_both_kernels(mc, orc, kernel, monkeypatch):
                     outputs=("diag", "trace", "full"), group_size=4, snapshot_sweeps=2)
 
 
+def test_v4_dataflow(mc, orc, monkeypatch):
+    """The dataflow kernel (v4: per-row completion counters, no level barriers)
+    matches the oracle for every chains-per-CTA layout up to a warp, real and
+    complex, with diag / pattern / full outputs, several launches (full-output
+    chunks) and forced block sizes; it is the default for the bench config."""
+    monkeypatch.setenv("MCINV_KERNEL", "v4")
+    for C in (1, 4, 8, 32):
+        monkeypatch.setenv("MCINV_C", str(C))
+        for th in ("64", "768"):
+            monkeypatch.setenv("MCINV_THREADS", th)
+            compare_run(mc, orc, W.pedigree(500, seed=21), seed=4, chains=64, burn_in=2, cycles=4,
+                        outputs=("diag", "pattern"), group_size=8)
+        c = W.lattice(4, 3, 0.15, seed=22)
+        compare_run(mc, orc, c, seed=5, chains=40, burn_in=2, cycles=3, outputs=("diag", "full"), group_size=4,
+                    snapshot_sweeps=2)
+    monkeypatch.delenv("MCINV_KERNEL")
+    monkeypatch.delenv("MCINV_C")
+    monkeypatch.delenv("MCINV_THREADS")
+    c, q, run = W.config(2)
+    inv = mc.Inverter(c)
+    inv.run(run.seed, run.chains, 0, 1, run.outputs, group_size=run.group_size)
+    assert inv.kernel_info()["version"] == 4
+    inv.close()
+
+
 def test_v3_custom_pattern_and_threads(mc, orc, monkeypatch):
     """v3 with a custom pattern (non-neighbour pairs, duplicates, diagonal
     elements: deferred items) and forced block sizes (several rounds of items
@@ -270,13 +295,13 @@ def test_v3_custom_pattern_and_threads(mc, orc, monkeypatch):
                     outputs=("pattern", "diag"), group_size=16)
 
 
-def test_bench_configs_use_v3(mc):
+def test_bench_configs_use_level_kernels(mc):
     for k in (2, 3, 5):
         c, q, run = W.config(k)
         inv = mc.Inverter(c, q=q)
         inv.run(run.seed, run.chains, 0, 1, tuple(o for o in run.outputs if o != "full") or ("diag",),
                 group_size=run.group_size)
-        assert inv.kernel_info()["version"] == 3, k
+        assert inv.kernel_info()["version"] in (3, 4), k
         inv.close()
 
 
