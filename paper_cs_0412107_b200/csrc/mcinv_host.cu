@@ -660,7 +660,9 @@ mcinv_status run_typed(mcinv_ctx *ctx, const mcinv_run_args *a, const Layout &L,
     const int pref = kernel_pref();
     const bool v4_ok = lv && L.lgC <= 5 && n <= 200000 && !lv->deferred;
     if (pref == 4 && !v4_ok) return fail(ctx, MCINV_E_INVALID, "v4 kernel not applicable to this run");
-    const bool v4 = v4_ok && (pref == 0 || pref == 4);
+    // auto: v4 whenever it applies (measured faster than v3 on configs 1-3: no per-level
+    // barrier; profiles/), else v3
+    const bool v4 = v4_ok && (pref == 4 || pref == 0);
     LevelDev::Slots *sl = v4 ? get_slots<S>(ctx, lv, 32 >> L.lgC) : nullptr;
     if (v4 && !sl) return fail(ctx, MCINV_E_NOMEM, "v4 slot arrays");
     if (v4 && !ctx->err_flag.p) {
@@ -701,8 +703,14 @@ mcinv_status run_typed(mcinv_ctx *ctx, const mcinv_run_args *a, const Layout &L,
         q3.sweep_abs0 = p.sweep_abs0;
         q3.burn_in = p.burn_in;
         q3.lgC = L.lgC;
-        q3.lgP = L.lgP;
         q3.lgG = ilog2(a->group_size);
+        // v3 register blocking: K = 2 adjacent chains per thread (real C; both in one SE
+        // group; no trace / deferred items, which run K = 1); MCINV_K=1 disables
+        int lgK = (ctx->dtype == MCINV_F64 && L.lgC >= 1 && a->group_size >= 2 && !lv->deferred) ? 1 : 0;
+        if (const char *e = std::getenv("MCINV_K")) lgK = std::atoi(e) >= 2 ? lgK : 0;
+        if (v4) lgK = 0;
+        q3.lgK = lgK;
+        q3.lgP = L.lgP - lgK;
         q3.pcount = (int)ctx->pcount;
         q3.slot_diag = p.slot_diag;
         q3.slot_pat = p.slot_pat;
@@ -715,10 +723,10 @@ mcinv_status run_typed(mcinv_ctx *ctx, const mcinv_run_args *a, const Layout &L,
         }
         // threads: enough for the widest phase x C, a multiple of 32 and of C, <= 768 (85
         // registers per thread: measured best for configs 2-5)
-        int64_t want = (int64_t)std::max(lv->max_rows, 1) << L.lgC;
-        want = std::min<int64_t>(768, want);
+        int64_t want = (int64_t)std::max(lv->max_rows, 1) << (L.lgC - q3.lgK);
+        want = std::min<int64_t>(v4 ? 1024 : 768, want);  // v4: more warps keep more rows in flight
         if (const char *e = std::getenv("MCINV_THREADS")) want = std::atoi(e);
-        want = std::min<int64_t>(1024, std::max<int64_t>(want, int64_t(1) << L.lgC));
+        want = std::min<int64_t>(1024, std::max<int64_t>(want, int64_t(1) << (L.lgC - q3.lgK)));
         threads3 = (int)((want + 31) / 32 * 32);
     }
     cudaError_t lerr = cudaSuccess;

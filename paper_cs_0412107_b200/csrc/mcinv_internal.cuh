@@ -108,8 +108,9 @@ struct Sweep3Params {
     int s_begin, s_end, burn_in;
     unsigned outputs;
     int lgC;              // log2 chains per CTA
-    int lgP;              // log2 lanes of one SE group inside a CTA: min(group size, C) (kernel template)
+    int lgP;              // log2 lanes of one SE group inside a CTA: min(group size, C) / K (kernel template)
     int lgG;              // log2 group size: chain c accumulates into group slot c >> lgG
+    int lgK;              // v3: log2 chains per thread (1 only for real runs without trace / deferred items)
     int pcount;
     double *slot_diag, *slot_pat, *slot_trace;  // [groups][count] (x e doubles)
     S *snap_x, *snap_y;

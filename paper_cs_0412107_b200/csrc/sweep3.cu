@@ -92,29 +92,72 @@ __device__ __forceinline__ ZW<S> ld_zw(const ZW<S> *p) {
     return *p;  // coherent load: values written by other threads of the CTA before __syncthreads
 }
 
-// fma chains of Eq. (4)/(5) over the cnt entries at beg, KU gathers in flight.
-// Branch-free: the entry arrays are padded by KU entries, so every load is
-// unconditional; slots past the row's end gather row 0 of this chain (an
-// L1-hot dummy) and their fma is predicated off, so the sums are exactly the
-// serial ones.
-template <typename S, int KU>
-__device__ __forceinline__ void row_sums(const Sweep3Params<S> &p, const ZW<S> *zcol, int beg, int cnt, S &az,
-                                         S &aw) {
+// K consecutive (z, w) state elements of one row (K chains of a thread) in
+// 256-bit accesses where they fill one (LDG.E.ENL2.256 on sm_100a).
+template <typename S, int K>
+struct ZWK {
+    ZW<S> v[K];
+};
+__device__ __forceinline__ void ld256(const void *p, double &a, double &b, double &c, double &d) {
+    asm volatile("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p) : "memory");
+}
+__device__ __forceinline__ void st256(void *p, double a, double b, double c, double d) {
+    asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
+}
+template <typename S, int K>
+__device__ __forceinline__ ZWK<S, K> ld_zwk(const ZW<S> *p) {
+    ZWK<S, K> r;
+    if constexpr (ScalarTraits<S>::kDoubles == 1 && K == 1) {
+        r.v[0] = *p;
+    } else if constexpr (ScalarTraits<S>::kDoubles == 1) {
+#pragma unroll
+        for (int q = 0; q < K; q += 2) ld256(p + q, r.v[q].z, r.v[q].w, r.v[q + 1].z, r.v[q + 1].w);
+    } else {
+#pragma unroll
+        for (int q = 0; q < K; ++q) ld256(p + q, r.v[q].z.re, r.v[q].z.im, r.v[q].w.re, r.v[q].w.im);
+    }
+    return r;
+}
+template <typename S, int K>
+__device__ __forceinline__ void st_zwk(ZW<S> *p, const ZWK<S, K> &r) {
+    if constexpr (ScalarTraits<S>::kDoubles == 1 && K == 1) {
+        *p = r.v[0];
+    } else if constexpr (ScalarTraits<S>::kDoubles == 1) {
+#pragma unroll
+        for (int q = 0; q < K; q += 2) st256(p + q, r.v[q].z, r.v[q].w, r.v[q + 1].z, r.v[q + 1].w);
+    } else {
+#pragma unroll
+        for (int q = 0; q < K; ++q) st256(p + q, r.v[q].z.re, r.v[q].z.im, r.v[q].w.re, r.v[q].w.im);
+    }
+}
+
+// fma chains of Eq. (4)/(5) over the cnt entries at beg for the K chains of
+// this thread, KU gathers in flight. Branch-free: the entry arrays are padded
+// by 8 entries, so every load is unconditional; slots past the row's end
+// gather row 0 of these chains (an L1-hot dummy) and their fma is predicated
+// off, so the sums are exactly the serial ones.
+template <typename S, int KU, int K>
+__device__ __forceinline__ void row_sums(const Sweep3Params<S> &p, const ZW<S> *zcol, int beg, int cnt,
+                                         S (&az)[K], S (&aw)[K]) {
     for (int e0 = 0; e0 < cnt; e0 += KU) {
         int j[KU];
-        ZW<S> v[KU], ab[KU];
+        ZWK<S, K> v[KU];
+        ZW<S> ab[KU];
 #pragma unroll
-        for (int k = 0; k < KU; ++k) j[k] = __ldg(p.ent_col + beg + e0 + k);
+        for (int q = 0; q < KU; ++q) j[q] = __ldg(p.ent_col + beg + e0 + q);
 #pragma unroll
-        for (int k = 0; k < KU; ++k) {
-            v[k] = ld_zw(zcol + (int64_t)(e0 + k < cnt ? j[k] : 0) * p.ld);
-            ab[k] = ldg_ab(reinterpret_cast<const ZW<S> *>(p.ent_ab) + beg + e0 + k);
+        for (int q = 0; q < KU; ++q) {
+            v[q] = ld_zwk<S, K>(zcol + (int64_t)(e0 + q < cnt ? j[q] : 0) * p.ld);
+            ab[q] = ldg_ab(reinterpret_cast<const ZW<S> *>(p.ent_ab) + beg + e0 + q);
         }
 #pragma unroll
-        for (int k = 0; k < KU; ++k)
-            if (e0 + k < cnt) {
-                az = fma_s(ab[k].z, v[k].z, az);
-                aw = fma_s(ab[k].w, v[k].w, aw);
+        for (int q = 0; q < KU; ++q)
+            if (e0 + q < cnt) {
+#pragma unroll
+                for (int h = 0; h < K; ++h) {
+                    az[h] = fma_s(ab[q].z, v[q].v[h].z, az[h]);
+                    aw[h] = fma_s(ab[q].w, v[q].v[h].w, aw[h]);
+                }
             }
     }
 }
@@ -131,31 +174,47 @@ __device__ __forceinline__ void slot_red(double *slot, cd v) {
 // Fused accumulation of row i's products in a sampling sweep (Eq. 1/C,
 // P:173-176): z_i w_i^* into the diag slot and the pattern slot of (i, i);
 // z_i w_j^* and z_j w_i^* for the lower neighbours j (final values, L1-hot
-// from the gathers) into their pattern slots. Called by all 32 lanes of a
-// converged warp (acc = false for lanes without a valid, active item).
-template <typename S, int P, int V>
-__device__ __forceinline__ void accumulate_row(const Sweep3Params<S> &p, const ZW<S> *zcol, int4 rec, S zi, S wi,
-                                               bool acc, int lane, bool gleader, bool towner, double *sd,
-                                               double *sp, bool want_diag, bool want_pat) {
+// from the gathers) into their pattern slots. The K chains of the thread are
+// summed in registers (they belong to one SE group), then the P lanes of the
+// group. Called by all 32 lanes of a converged warp; acc[h] = false for
+// chains without a valid, active item.
+template <typename S, int P, int V, int K>
+__device__ __forceinline__ void accumulate_row(const Sweep3Params<S> &p, const ZW<S> *zcol, int4 rec, const S (&zi)[K],
+                                               const S (&wi)[K], const bool (&acc)[K], int lane, bool gleader,
+                                               bool towner, double *sd, double *sp, bool want_diag, bool want_pat) {
     constexpr int E = ScalarTraits<S>::kDoubles;
     const int i = rec.x, beg = rec.y;
+    bool any = false;
+#pragma unroll
+    for (int h = 0; h < K; ++h) any = any || acc[h];
     if (want_diag || want_pat) {
         // z_i w_i^*: diag element i and pattern element (i, i)
-        const S d = group_sum<P>(acc ? zwc_s(zi, wi) : zero_s<S>());
-        if (acc && gleader) {
+        S d = zero_s<S>();
+#pragma unroll
+        for (int h = 0; h < K; ++h)
+            if (acc[h]) d = add_s(d, zwc_s(zi[h], wi[h]));
+        d = group_sum<P>(d);
+        if (any && gleader) {
             if (want_diag) slot_red(sd + (int64_t)i * E, d);
             if (want_pat && rec.w >= 0) slot_red(sp + (int64_t)rec.w * E, d);
         }
     }
     if (!want_pat) return;
     // z_i w_j^* and z_j w_i^* for the lower neighbours j = col[beg + e], e < nlow
-    const int nlow = acc ? rec.z >> 16 : 0;
+    const int nlow = any ? rec.z >> 16 : 0;
     if constexpr (P == 1) {
         for (int e = 0; e < nlow; ++e) {
-            const ZW<S> u = ld_zw(zcol + (int64_t)__ldg(p.ent_col + beg + e) * p.ld);
+            const ZWK<S, K> u = ld_zwk<S, K>(zcol + (int64_t)__ldg(p.ent_col + beg + e) * p.ld);
+            S x = zero_s<S>(), y = zero_s<S>();
+#pragma unroll
+            for (int h = 0; h < K; ++h)
+                if (acc[h]) {
+                    x = add_s(x, zwc_s(zi[h], u.v[h].w));
+                    y = add_s(y, zwc_s(u.v[h].z, wi[h]));
+                }
             const int2 pz = __ldg(p.ent_pz + beg + e);
-            if (pz.x >= 0) slot_red(sp + (int64_t)pz.x * E, zwc_s(zi, u.w));
-            if (pz.y >= 0) slot_red(sp + (int64_t)pz.y * E, zwc_s(u.z, wi));
+            if (pz.x >= 0) slot_red(sp + (int64_t)pz.x * E, x);
+            if (pz.y >= 0) slot_red(sp + (int64_t)pz.y * E, y);
         }
     } else {
         constexpr int VE = V / 2;  // entries per transpose-reduction
@@ -167,9 +226,16 @@ __device__ __forceinline__ void accumulate_row(const Sweep3Params<S> &p, const Z
                 const int e = b * VE + q;
                 const int jc = __ldg(p.ent_col + beg + e);  // padded: always in bounds
                 const bool ok = e < nlow;
-                const ZW<S> u = ld_zw(zcol + (int64_t)(ok ? jc : 0) * p.ld);
-                v[2 * q] = ok ? zwc_s(zi, u.w) : zero_s<S>();
-                v[2 * q + 1] = ok ? zwc_s(u.z, wi) : zero_s<S>();
+                const ZWK<S, K> u = ld_zwk<S, K>(zcol + (int64_t)(ok ? jc : 0) * p.ld);
+                S x = zero_s<S>(), y = zero_s<S>();
+#pragma unroll
+                for (int h = 0; h < K; ++h)
+                    if (acc[h]) {
+                        x = add_s(x, zwc_s(zi[h], u.v[h].w));
+                        y = add_s(y, zwc_s(u.v[h].z, wi[h]));
+                    }
+                v[2 * q] = ok ? x : zero_s<S>();
+                v[2 * q + 1] = ok ? y : zero_s<S>();
             }
             int held;
             const S x = transpose_sum<P, V>(v, lane, held);
@@ -185,30 +251,31 @@ __device__ __forceinline__ void accumulate_row(const Sweep3Params<S> &p, const Z
 
 }  // namespace
 
-template <typename S, int KU, int NT, int LGP>
+template <typename S, int KU, int NT, int LGP, int K>
 __global__ void __launch_bounds__(NT, 1) sweep3_kernel(const Sweep3Params<S> p) {
     constexpr int E = ScalarTraits<S>::kDoubles;
-    constexpr int P = 1 << LGP;        // lanes of one SE group inside this CTA (<= C)
+    constexpr int P = 1 << LGP;        // lanes of one SE group inside this CTA (K chains per lane)
     constexpr int V = P < 8 ? P : 8;   // products per transpose-reduction (pairs of one entry)
     const int tid = threadIdx.x;
-    const int B = blockDim.x;  // a multiple of 32 and of C
+    const int B = blockDim.x;  // a multiple of 32 and of C / K
     const int lane = tid & 31;
     const int wbase = tid - lane;
-    const int lgC = p.lgC;
-    const int C = 1 << lgC;
-    const int c = tid & (C - 1);
-    const int chain = (blockIdx.x << lgC) + c;
-    const bool active = chain < p.chains;
-    const uint32_t gchain = p.chain0 + static_cast<uint32_t>(chain);
-    const bool gleader = (c & (P - 1)) == 0;           // owner of a plain group sum
+    const int lgL = p.lgC - (K == 2 ? 1 : 0);  // log2 lanes per row: C / K
+    const int Lr = 1 << lgL;
+    const int cl = tid & (Lr - 1);
+    const int chain = (blockIdx.x << p.lgC) + cl * K;  // first of this lane's K chains
+    bool active[K];
+#pragma unroll
+    for (int h = 0; h < K; ++h) active[h] = chain + h < p.chains;
+    const bool gleader = (cl & (P - 1)) == 0;                     // owner of a plain group sum
     const bool towner = (lane & ((P > V ? P / V : 1) - 1)) == 0;  // owner of a transposed value
-    const int64_t grp = chain >> p.lgG;                // SE group of this chain = its accumulator slot
+    const int64_t grp = chain >> p.lgG;  // SE group of these chains = their accumulator slot
     ZW<S> *__restrict__ zcol = p.zw + chain;
     const bool want_diag = p.outputs & OUT_DIAG, want_pat = p.outputs & OUT_PATTERN;
     const bool want_tr = p.outputs & OUT_TRACE, want_full = p.outputs & OUT_FULL;
     double *const sd = p.slot_diag + grp * p.n * E;
     double *const sp = p.slot_pat + grp * p.pcount * E;
-    S tr = zero_s<S>();
+    S tr = zero_s<S>();  // K == 1 only (trace runs use K = 1)
 
     for (int s = p.s_begin; s < p.s_end; ++s) {
         const uint32_t k = p.sweep_abs0 + static_cast<uint32_t>(s);
@@ -217,65 +284,88 @@ __global__ void __launch_bounds__(NT, 1) sweep3_kernel(const Sweep3Params<S> p) 
         for (int ph = 0; ph < nph; ++ph) {
             // ---- row updates of level ph; warp-uniform trip count (shuffles below)
             const int r0 = __ldg(p.ph_row + ph);
-            const int nu = (__ldg(p.ph_row + ph + 1) - r0) << lgC;
+            const int nu = (__ldg(p.ph_row + ph + 1) - r0) << lgL;
             for (int base = wbase; base < nu; base += B) {
                 const int t = base + lane;
                 const bool valid = t < nu;
-                const int o = r0 + (t >> lgC);
+                const int o = r0 + (t >> lgL);
                 const int4 rec = valid ? __ldg(p.ord_rec + o) : make_int4(0, 0, 0, -1);
                 const int i = rec.x, beg = rec.y, cnt = rec.z & 0xffff;
-                S zi = zero_s<S>(), wi = zero_s<S>();
+                S zi[K], wi[K];
+#pragma unroll
+                for (int h = 0; h < K; ++h) zi[h] = wi[h] = zero_s<S>();
                 if (valid) {
                     // noise first: its temporaries are dead before the gathers are in flight
-                    double phi;
-                    if (p.noise == 0) phi = gaussian(static_cast<uint32_t>(i), k, gchain, p.key0, p.key1);
-                    else phi = p.noise == 2 ? 1.0 : 0.0;
-                    S az = zero_s<S>(), aw = zero_s<S>();
-                    row_sums<S, KU>(p, zcol, beg, cnt, az, aw);
+                    double phi[K];
+#pragma unroll
+                    for (int h = 0; h < K; ++h) {
+                        if (p.noise == 0)
+                            phi[h] = gaussian(static_cast<uint32_t>(i), k, p.chain0 + static_cast<uint32_t>(chain + h),
+                                              p.key0, p.key1);
+                        else phi[h] = p.noise == 2 ? 1.0 : 0.0;
+                    }
+                    S az[K], aw[K];
+#pragma unroll
+                    for (int h = 0; h < K; ++h) az[h] = aw[h] = zero_s<S>();
+                    row_sums<S, KU, K>(p, zcol, beg, cnt, az, aw);
                     const S dl = ldg_s(p.ord_dsg + 2 * o), sg = ldg_s(p.ord_dsg + 2 * o + 1);
-                    zi = fma_s(neg_s(dl), az, scale_s(sg, phi));
-                    wi = fma_s(neg_s(conj_s(dl)), aw, scale_s(conj_s(sg), phi));
-                    zcol[(int64_t)i * p.ld] = ZW<S>{zi, wi};
+                    ZWK<S, K> out;
+#pragma unroll
+                    for (int h = 0; h < K; ++h) {
+                        zi[h] = fma_s(neg_s(dl), az[h], scale_s(sg, phi[h]));
+                        wi[h] = fma_s(neg_s(conj_s(dl)), aw[h], scale_s(conj_s(sg), phi[h]));
+                        out.v[h] = ZW<S>{zi[h], wi[h]};
+                    }
+                    st_zwk<S, K>(zcol + (int64_t)i * p.ld, out);
                     if (want_full && sampling) {
                         const int64_t ts = s - p.snap_s0;
-                        p.snap_x[(ts * p.n + i) * p.ld + chain] = zi;
-                        p.snap_y[(ts * p.n + i) * p.ld + chain] = wi;
+#pragma unroll
+                        for (int h = 0; h < K; ++h) {
+                            p.snap_x[(ts * p.n + i) * p.ld + chain + h] = zi[h];
+                            p.snap_y[(ts * p.n + i) * p.ld + chain + h] = wi[h];
+                        }
                     }
                 }
                 if (!sampling) continue;
-                accumulate_row<S, P, V>(p, zcol, rec, zi, wi, valid && active, lane, gleader, towner, sd, sp,
-                                        want_diag, want_pat);
+                bool acc[K];
+#pragma unroll
+                for (int h = 0; h < K; ++h) acc[h] = valid && active[h];
+                accumulate_row<S, P, V, K>(p, zcol, rec, zi, wi, acc, lane, gleader, towner, sd, sp, want_diag,
+                                           want_pat);
             }
-            if (sampling) {
-                // ---- deferred trace items: conj(w_i) sum_j Q_ij z_j  (w^dagger Q z, reading R2);
-                // per-thread register sums, no shuffles
-                if (want_tr) {
-                    const int q0 = __ldg(p.ph_tq + ph);
-                    const int nq = (__ldg(p.ph_tq + ph + 1) - q0) << lgC;
-                    for (int t = tid; t < nq; t += B) {
-                        const int o = q0 + (t >> lgC);
-                        const int i = __ldg(p.tq_row + o);
-                        S qz = zero_s<S>();
-                        for (int e = __ldg(p.tq_eptr + o); e < __ldg(p.tq_eptr + o + 1); ++e)
-                            qz = add_s(qz, mul_s(ldg_s(p.tq_val + e),
-                                                 ld_zw(zcol + (int64_t)__ldg(p.tq_col + e) * p.ld).z));
-                        tr = add_s(tr, zwc_s(qz, ld_zw(zcol + (int64_t)i * p.ld).w));
+            if constexpr (K == 1) {
+                if (sampling) {
+                    // ---- deferred trace items: conj(w_i) sum_j Q_ij z_j  (w^dagger Q z, reading R2);
+                    // per-thread register sums, no shuffles
+                    if (want_tr) {
+                        const int q0 = __ldg(p.ph_tq + ph);
+                        const int nq = (__ldg(p.ph_tq + ph + 1) - q0) << lgL;
+                        for (int t = tid; t < nq; t += B) {
+                            const int o = q0 + (t >> lgL);
+                            const int i = __ldg(p.tq_row + o);
+                            S qz = zero_s<S>();
+                            for (int e = __ldg(p.tq_eptr + o); e < __ldg(p.tq_eptr + o + 1); ++e)
+                                qz = add_s(qz, mul_s(ldg_s(p.tq_val + e),
+                                                     ld_zw(zcol + (int64_t)__ldg(p.tq_col + e) * p.ld).z));
+                            tr = add_s(tr, zwc_s(qz, ld_zw(zcol + (int64_t)i * p.ld).w));
+                        }
                     }
-                }
-                // ---- deferred pattern pairs z_i w_j^*
-                if (want_pat) {
-                    const int q0 = __ldg(p.ph_pp + ph);
-                    const int nq = (__ldg(p.ph_pp + ph + 1) - q0) << lgC;
-                    for (int base = wbase; base < nq; base += B) {
-                        const int t = base + lane;
-                        const bool valid = t < nq;
-                        const int o = q0 + (t >> lgC);
-                        S x = zero_s<S>();
-                        if (valid && active)
-                            x = zwc_s(ld_zw(zcol + (int64_t)__ldg(p.pp_i + o) * p.ld).z,
-                                      ld_zw(zcol + (int64_t)__ldg(p.pp_j + o) * p.ld).w);
-                        x = group_sum<P>(x);
-                        if (valid && active && gleader) slot_red(sp + (int64_t)__ldg(p.pp_slot + o) * E, x);
+                    // ---- deferred pattern pairs z_i w_j^*
+                    if (want_pat) {
+                        const int q0 = __ldg(p.ph_pp + ph);
+                        const int nq = (__ldg(p.ph_pp + ph + 1) - q0) << lgL;
+                        for (int base = wbase; base < nq; base += B) {
+                            const int t = base + lane;
+                            const bool valid = t < nq;
+                            const int o = q0 + (t >> lgL);
+                            S x = zero_s<S>();
+                            if (valid && active[0])
+                                x = zwc_s(ld_zw(zcol + (int64_t)__ldg(p.pp_i + o) * p.ld).z,
+                                          ld_zw(zcol + (int64_t)__ldg(p.pp_j + o) * p.ld).w);
+                            x = group_sum<P>(x);
+                            if (valid && active[0] && gleader)
+                                slot_red(sp + (int64_t)__ldg(p.pp_slot + o) * E, x);
+                        }
                     }
                 }
             }
@@ -283,37 +373,42 @@ __global__ void __launch_bounds__(NT, 1) sweep3_kernel(const Sweep3Params<S> p) 
         }
     }
 
-    if (want_tr) {
-        // per-chain trace: sum over the threads of each chain, then over the P chains of a group
-        extern __shared__ __align__(16) unsigned char red_raw[];
-        S *red = reinterpret_cast<S *>(red_raw);
-        red[tid] = active ? tr : zero_s<S>();
-        __syncthreads();
-        if (wbase < C) {  // whole warps (C < 32: lanes >= C hold zeros and are not leaders)
-            S v = zero_s<S>();
-            if (tid < C)
-                for (int h = tid; h < B; h += C) v = add_s(v, red[h]);
-            v = group_sum<P>(v);
-            if (tid < C && gleader && active) slot_red(p.slot_trace + grp * E, v);
+    if constexpr (K == 1) {
+        if (want_tr) {
+            // per-chain trace: sum over the threads of each chain, then over the P chains of a group
+            extern __shared__ __align__(16) unsigned char red_raw[];
+            S *red = reinterpret_cast<S *>(red_raw);
+            const int C = 1 << p.lgC;
+            red[tid] = active[0] ? tr : zero_s<S>();
+            __syncthreads();
+            if (wbase < C) {  // whole warps (C < 32: lanes >= C hold zeros and are not leaders)
+                S v = zero_s<S>();
+                if (tid < C)
+                    for (int h = tid; h < B; h += C) v = add_s(v, red[h]);
+                v = group_sum<P>(v);
+                if (tid < C && gleader && active[0]) slot_red(p.slot_trace + grp * E, v);
+            }
         }
     }
 }
 
 // ---------------------------------------------------------------- v4: dataflow
 //
-// The same row update and accumulation, without per-level barriers. Every row
-// j has a completion counter done[j] (shared memory, one byte, counted modulo
-// 256) = the number of sweeps of this launch's chains that have updated it.
-// Row i in sweep s may run once every lower neighbour j < i has done[j] >=
-// s + 1 (its new value, Eq. 4/5 read order) and every upper neighbour has
-// done[j] >= s: the upper neighbour has finished sweep s - 1, i.e. it has
-// read z_i of sweep s - 1 (write-after-read) and holds the value row i must
-// read. Neighbour counters differ by at most 2, so byte arithmetic is exact.
-// Each warp takes groups of R = 32 / C rows (never spanning a level: rows of
-// a group are independent) in increasing (sweep, level order); all
-// dependencies point to earlier groups, so the earliest unfinished group can
-// always run: no deadlock. A bounded wait (watchdog) reports instead of
-// hanging if that reasoning were ever violated.
+// The same row update and accumulation, without per-level barriers: one CTA
+// barrier per sweep, and within a sweep every row j has a completion counter
+// done[j] (shared memory, one byte, counted modulo 256) = the number of
+// sweeps that have updated it. Row i in sweep s may run once every lower
+// neighbour j < i (a prefix of its ascending entry list) has done[j] = s + 1:
+// it then reads their new values (Eq. 4/5 order). Upper neighbours hold their
+// sweep s - 1 values until the sweep barrier (they are updated after row i in
+// every order the counters allow, being at higher levels), and every read of
+// row i's sweep s - 1 value happened before that barrier, so the sweep
+// barrier covers all write-after-read hazards; the counter is published right
+// after the store. Each warp takes groups of R = 32 / C rows (never spanning
+// a level: rows of a group are independent) in level order; every dependency
+// points to an earlier group, so the earliest unfinished group can always
+// run: no deadlock. A bounded wait (watchdog) reports instead of hanging if
+// that reasoning were ever violated.
 template <typename S, int KU, int NT, int LGP>
 __global__ void __launch_bounds__(NT, 1) sweep4_kernel(const Sweep3Params<S> p) {
     constexpr int E = ScalarTraits<S>::kDoubles;
@@ -343,75 +438,88 @@ __global__ void __launch_bounds__(NT, 1) sweep4_kernel(const Sweep3Params<S> p) 
 
     const int R = 32 >> lgC;
     const int ngroups = p.nslots / R;
-    const int64_t total = (int64_t)(p.s_end - p.s_begin) * ngroups;
-    for (int64_t gi = tid >> 5; gi < total; gi += B >> 5) {
-        const int s = p.s_begin + (int)(gi / ngroups);
-        const int slot = (int)(gi % ngroups) * R + (lane >> lgC);
+    const int W = B >> 5;
+    for (int s = p.s_begin; s < p.s_end; ++s) {
         const uint32_t k = p.sweep_abs0 + static_cast<uint32_t>(s);
         const bool sampling = s >= p.burn_in;
-        const int4 rec = __ldg(p.slot_rec + slot);
-        const bool valid = rec.x >= 0;
-        const int i = rec.x, beg = rec.y, cnt = valid ? rec.z & 0xffff : 0;
-        S zi = zero_s<S>(), wi = zero_s<S>();
-        if (valid) {
-            double phi;
-            if (p.noise == 0) phi = gaussian(static_cast<uint32_t>(i), k, gchain, p.key0, p.key1);
-            else phi = p.noise == 2 ? 1.0 : 0.0;
-            // dependency wait (all C lanes of the row read the same counters: smem broadcast)
-            const unsigned char lo = static_cast<unsigned char>(s + 1), hi = static_cast<unsigned char>(s);
-            for (int e = 0; e < cnt; ++e) {
-                const int j = __ldg(p.ent_col + beg + e);
-                const unsigned char need = j < i ? lo : hi;
-                const volatile unsigned char *f = done + j;
-                if (static_cast<signed char>(*f - need) < 0) {
-                    unsigned spins = 0;
-                    while (static_cast<signed char>(*f - need) < 0 && !*reinterpret_cast<volatile unsigned *>(p.err)) {
-                        __nanosleep(32);
-                        if (++spins > (1u << 26)) {  // ~seconds: report, do not hang
-                            atomicOr(p.err, 1u);
-                            break;
+        const unsigned char need = static_cast<unsigned char>(s + 1);
+        for (int g = tid >> 5; g < ngroups; g += W) {
+            const int slot = g * R + (lane >> lgC);
+            const int4 rec = __ldg(p.slot_rec + slot);
+            const bool valid = rec.x >= 0;
+            const int i = rec.x, beg = rec.y, cnt = valid ? rec.z & 0xffff : 0;
+            S zi = zero_s<S>(), wi = zero_s<S>();
+            if (valid) {
+                double phi;
+                if (p.noise == 0) phi = gaussian(static_cast<uint32_t>(i), k, gchain, p.key0, p.key1);
+                else phi = p.noise == 2 ? 1.0 : 0.0;
+                // wait for the lower neighbours (the first nlow entries; all C lanes of the
+                // row read the same counters: smem broadcast), then acquire
+                const int nlow = rec.z >> 16;
+                for (int e = 0; e < nlow; ++e) {
+                    const volatile unsigned char *f = done + __ldg(p.ent_col + beg + e);
+                    if (*f != need) {
+                        unsigned spins = 0;
+                        while (*f != need && !*reinterpret_cast<volatile unsigned *>(p.err)) {
+                            __nanosleep(32);
+                            if (++spins > (1u << 26)) {  // ~seconds: report, do not hang
+                                atomicOr(p.err, 1u);
+                                break;
+                            }
                         }
                     }
                 }
+                __threadfence_block();
+                S az[1] = {zero_s<S>()}, aw[1] = {zero_s<S>()};
+                row_sums<S, KU, 1>(p, zcol, beg, cnt, az, aw);
+                const S dl = ldg_s(p.slot_dsg + 2 * slot), sg = ldg_s(p.slot_dsg + 2 * slot + 1);
+                zi = fma_s(neg_s(dl), az[0], scale_s(sg, phi));
+                wi = fma_s(neg_s(conj_s(dl)), aw[0], scale_s(conj_s(sg), phi));
+                zcol[(int64_t)i * p.ld] = ZW<S>{zi, wi};
+                if (want_full && sampling) {
+                    const int64_t ts = s - p.snap_s0;
+                    p.snap_x[(ts * p.n + i) * p.ld + chain] = zi;
+                    p.snap_y[(ts * p.n + i) * p.ld + chain] = wi;
+                }
             }
-            __threadfence_block();  // acquire: gathers after the counters
-            S az = zero_s<S>(), aw = zero_s<S>();
-            row_sums<S, KU>(p, zcol, beg, cnt, az, aw);
-            const S dl = ldg_s(p.slot_dsg + 2 * slot), sg = ldg_s(p.slot_dsg + 2 * slot + 1);
-            zi = fma_s(neg_s(dl), az, scale_s(sg, phi));
-            wi = fma_s(neg_s(conj_s(dl)), aw, scale_s(conj_s(sg), phi));
-            zcol[(int64_t)i * p.ld] = ZW<S>{zi, wi};
-            if (want_full && sampling) {
-                const int64_t ts = s - p.snap_s0;
-                p.snap_x[(ts * p.n + i) * p.ld + chain] = zi;
-                p.snap_y[(ts * p.n + i) * p.ld + chain] = wi;
+            __syncwarp();  // the row's C stores are ordered before its counter update
+            if (valid && c == 0) {
+                __threadfence_block();  // release
+                *reinterpret_cast<volatile unsigned char *>(done + i) = need;
+            }
+            if (sampling) {
+                const S zk[1] = {zi}, wk[1] = {wi};
+                const bool ak[1] = {valid && active};
+                accumulate_row<S, P, V, 1>(p, zcol, rec, zk, wk, ak, lane, gleader, towner, sd, sp, want_diag,
+                                           want_pat);
             }
         }
-        __syncwarp();  // the row's C stores are ordered before its counter update
-        if (valid && c == 0) {
-            __threadfence_block();  // release
-            *reinterpret_cast<volatile unsigned char *>(done + i) = static_cast<unsigned char>(s + 1);
-        }
-        if (sampling)
-            accumulate_row<S, P, V>(p, zcol, rec, zi, wi, valid && active, lane, gleader, towner, sd, sp, want_diag,
-                                    want_pat);
+        __syncthreads();  // sweep boundary: all reads of sweep s values are done
     }
 }
 
 namespace {
 
-template <typename S, int LGP>
-cudaError_t launch3(const Sweep3Params<S> &p, int threads, cudaStream_t st) {
+template <typename S, int LGP, int K>
+cudaError_t launch3k(const Sweep3Params<S> &p, int threads, cudaStream_t st) {
     // gathers in flight per row chunk: 64 registers at 1024 threads, 85 at 768, 128 at 512
     // (the entry arrays are padded by 8 entries: KU <= 8)
-    constexpr int KS = ScalarTraits<S>::kDoubles == 1 ? 4 : 2;
+    constexpr int KS = ScalarTraits<S>::kDoubles == 1 && K == 1 ? 4 : 2;
     const int C = 1 << p.lgC;
     const int blocks = (p.chains + C - 1) / C;
     const size_t smem = (p.outputs & OUT_TRACE) ? (size_t)threads * sizeof(S) : 0;
-    if (threads <= 512) sweep3_kernel<S, 2 * KS, 512, LGP><<<blocks, threads, smem, st>>>(p);
-    else if (threads <= 768) sweep3_kernel<S, KS, 768, LGP><<<blocks, threads, smem, st>>>(p);
-    else sweep3_kernel<S, KS, 1024, LGP><<<blocks, threads, smem, st>>>(p);
+    if (threads <= 512) sweep3_kernel<S, 2 * KS, 512, LGP, K><<<blocks, threads, smem, st>>>(p);
+    else if (threads <= 768) sweep3_kernel<S, KS, 768, LGP, K><<<blocks, threads, smem, st>>>(p);
+    else sweep3_kernel<S, KS, 1024, LGP, K><<<blocks, threads, smem, st>>>(p);
     return cudaGetLastError();
+}
+
+template <typename S, int LGP>
+cudaError_t launch3(const Sweep3Params<S> &p, int threads, cudaStream_t st) {
+    if constexpr (ScalarTraits<S>::kDoubles == 1) {
+        if (p.lgK == 1) return launch3k<S, LGP, 2>(p, threads, st);
+    }
+    return launch3k<S, LGP, 1>(p, threads, st);
 }
 
 }  // namespace

@@ -270,11 +270,29 @@ def test_v4_dataflow(mc, orc, monkeypatch):
     monkeypatch.delenv("MCINV_KERNEL")
     monkeypatch.delenv("MCINV_C")
     monkeypatch.delenv("MCINV_THREADS")
-    c, q, run = W.config(2)
-    inv = mc.Inverter(c)
-    inv.run(run.seed, run.chains, 0, 1, run.outputs, group_size=run.group_size)
-    assert inv.kernel_info()["version"] == 4
-    inv.close()
+    # automatic choice: v4 where it applies (configs 2, 3), v3 for C > 32 or trace (configs 4, 5)
+    for k, ver in ((3, 4), (2, 4), (5, 3)):
+        c, q, run = W.config(k)
+        inv = mc.Inverter(c)
+        inv.run(run.seed, run.chains, 0, 1, tuple(o for o in run.outputs if o != "full") or ("diag",),
+                group_size=run.group_size)
+        assert inv.kernel_info()["version"] == ver, k
+        inv.close()
+
+
+@pytest.mark.parametrize("K", ["1", "2"])
+def test_v3_chains_per_thread(mc, orc, monkeypatch, K):
+    """v3 with one or two adjacent chains per thread (256-bit state accesses,
+    in-thread pre-summed accumulation) for several chains-per-CTA layouts and
+    group sizes, including an inactive tail chain."""
+    monkeypatch.setenv("MCINV_KERNEL", "v3")
+    monkeypatch.setenv("MCINV_K", K)
+    for C, gs, chains in ((2, 2, 62), (8, 8, 64), (16, 4, 60), (64, 32, 96)):
+        monkeypatch.setenv("MCINV_C", str(C))
+        compare_run(mc, orc, W.pedigree(400, seed=23), seed=7, chains=chains, burn_in=2, cycles=3,
+                    outputs=("diag", "pattern"), group_size=gs)
+        compare_run(mc, orc, W.dense_config1(24, seed=24), seed=8, chains=chains, burn_in=1, cycles=3,
+                    outputs=("diag", "full"), group_size=gs, snapshot_sweeps=2)
 
 
 def test_v3_custom_pattern_and_threads(mc, orc, monkeypatch):
