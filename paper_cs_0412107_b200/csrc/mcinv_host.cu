@@ -663,7 +663,13 @@ mcinv_status run_typed(mcinv_ctx *ctx, const mcinv_run_args *a, const Layout &L,
     // auto: v4 whenever it applies (measured faster than v3 on configs 1-3: no per-level
     // barrier; profiles/), else v3
     const bool v4 = v4_ok && (pref == 4 || pref == 0);
-    LevelDev::Slots *sl = v4 ? get_slots<S>(ctx, lv, 32 >> L.lgC) : nullptr;
+    // chains per thread K (register blocking; real C, both chains in one SE group, no
+    // trace / deferred items): default 2 for v3 (config 4 +19%), 1 for v4 (config 2 measured
+    // faster with more threads than with blocking, profiles/); MCINV_K=1|2 overrides
+    int lgK = (lv && ctx->dtype == MCINV_F64 && L.lgC >= 1 && a->group_size >= 2 && !lv->deferred) ? 1 : 0;
+    if (const char *e = std::getenv("MCINV_K")) lgK = std::atoi(e) >= 2 ? lgK : 0;
+    else if (v4) lgK = 0;
+    LevelDev::Slots *sl = v4 ? get_slots<S>(ctx, lv, 32 >> (L.lgC - lgK)) : nullptr;
     if (v4 && !sl) return fail(ctx, MCINV_E_NOMEM, "v4 slot arrays");
     if (v4 && !ctx->err_flag.p) {
         if (cudaMalloc(&ctx->err_flag.p, 16) != cudaSuccess) return fail(ctx, MCINV_E_NOMEM, "v4 flag");
@@ -704,11 +710,6 @@ mcinv_status run_typed(mcinv_ctx *ctx, const mcinv_run_args *a, const Layout &L,
         q3.burn_in = p.burn_in;
         q3.lgC = L.lgC;
         q3.lgG = ilog2(a->group_size);
-        // v3 register blocking: K = 2 adjacent chains per thread (real C; both in one SE
-        // group; no trace / deferred items, which run K = 1); MCINV_K=1 disables
-        int lgK = (ctx->dtype == MCINV_F64 && L.lgC >= 1 && a->group_size >= 2 && !lv->deferred) ? 1 : 0;
-        if (const char *e = std::getenv("MCINV_K")) lgK = std::atoi(e) >= 2 ? lgK : 0;
-        if (v4) lgK = 0;
         q3.lgK = lgK;
         q3.lgP = L.lgP - lgK;
         q3.pcount = (int)ctx->pcount;

@@ -409,22 +409,23 @@ __global__ void __launch_bounds__(NT, 1) sweep3_kernel(const Sweep3Params<S> p) 
 // points to an earlier group, so the earliest unfinished group can always
 // run: no deadlock. A bounded wait (watchdog) reports instead of hanging if
 // that reasoning were ever violated.
-template <typename S, int KU, int NT, int LGP>
+template <typename S, int KU, int NT, int LGP, int K>
 __global__ void __launch_bounds__(NT, 1) sweep4_kernel(const Sweep3Params<S> p) {
     constexpr int E = ScalarTraits<S>::kDoubles;
-    constexpr int P = 1 << LGP;
+    constexpr int P = 1 << LGP;        // lanes of one SE group (K chains per lane)
     constexpr int V = P < 8 ? P : 8;
     extern __shared__ __align__(16) unsigned char done[];  // [n]
     const int tid = threadIdx.x;
     const int B = blockDim.x;
     const int lane = tid & 31;
-    const int lgC = p.lgC;  // C <= 32: the C lanes of a row are in one warp
-    const int C = 1 << lgC;
-    const int c = lane & (C - 1);
-    const int chain = (blockIdx.x << lgC) + c;
-    const bool active = chain < p.chains;
-    const uint32_t gchain = p.chain0 + static_cast<uint32_t>(chain);
-    const bool gleader = (c & (P - 1)) == 0;
+    const int lgL = p.lgC - (K == 2 ? 1 : 0);  // log2 lanes per row (C / K <= 32: one warp)
+    const int Lr = 1 << lgL;
+    const int cl = lane & (Lr - 1);
+    const int chain = (blockIdx.x << p.lgC) + cl * K;
+    bool active[K];
+#pragma unroll
+    for (int h = 0; h < K; ++h) active[h] = chain + h < p.chains;
+    const bool gleader = (cl & (P - 1)) == 0;
     const bool towner = (lane & ((P > V ? P / V : 1) - 1)) == 0;
     const int64_t grp = chain >> p.lgG;
     ZW<S> *__restrict__ zcol = p.zw + chain;
@@ -436,7 +437,7 @@ __global__ void __launch_bounds__(NT, 1) sweep4_kernel(const Sweep3Params<S> p) 
     for (int j = tid; j < p.n; j += B) done[j] = static_cast<unsigned char>(p.s_begin);
     __syncthreads();
 
-    const int R = 32 >> lgC;
+    const int R = 32 >> lgL;  // rows per warp group
     const int ngroups = p.nslots / R;
     const int W = B >> 5;
     for (int s = p.s_begin; s < p.s_end; ++s) {
@@ -444,16 +445,23 @@ __global__ void __launch_bounds__(NT, 1) sweep4_kernel(const Sweep3Params<S> p) 
         const bool sampling = s >= p.burn_in;
         const unsigned char need = static_cast<unsigned char>(s + 1);
         for (int g = tid >> 5; g < ngroups; g += W) {
-            const int slot = g * R + (lane >> lgC);
+            const int slot = g * R + (lane >> lgL);
             const int4 rec = __ldg(p.slot_rec + slot);
             const bool valid = rec.x >= 0;
             const int i = rec.x, beg = rec.y, cnt = valid ? rec.z & 0xffff : 0;
-            S zi = zero_s<S>(), wi = zero_s<S>();
+            S zi[K], wi[K];
+#pragma unroll
+            for (int h = 0; h < K; ++h) zi[h] = wi[h] = zero_s<S>();
             if (valid) {
-                double phi;
-                if (p.noise == 0) phi = gaussian(static_cast<uint32_t>(i), k, gchain, p.key0, p.key1);
-                else phi = p.noise == 2 ? 1.0 : 0.0;
-                // wait for the lower neighbours (the first nlow entries; all C lanes of the
+                double phi[K];
+#pragma unroll
+                for (int h = 0; h < K; ++h) {
+                    if (p.noise == 0)
+                        phi[h] = gaussian(static_cast<uint32_t>(i), k, p.chain0 + static_cast<uint32_t>(chain + h),
+                                          p.key0, p.key1);
+                    else phi[h] = p.noise == 2 ? 1.0 : 0.0;
+                }
+                // wait for the lower neighbours (the first nlow entries; all lanes of the
                 // row read the same counters: smem broadcast), then acquire
                 const int nlow = rec.z >> 16;
                 for (int e = 0; e < nlow; ++e) {
@@ -470,27 +478,38 @@ __global__ void __launch_bounds__(NT, 1) sweep4_kernel(const Sweep3Params<S> p) 
                     }
                 }
                 __threadfence_block();
-                S az[1] = {zero_s<S>()}, aw[1] = {zero_s<S>()};
-                row_sums<S, KU, 1>(p, zcol, beg, cnt, az, aw);
+                S az[K], aw[K];
+#pragma unroll
+                for (int h = 0; h < K; ++h) az[h] = aw[h] = zero_s<S>();
+                row_sums<S, KU, K>(p, zcol, beg, cnt, az, aw);
                 const S dl = ldg_s(p.slot_dsg + 2 * slot), sg = ldg_s(p.slot_dsg + 2 * slot + 1);
-                zi = fma_s(neg_s(dl), az[0], scale_s(sg, phi));
-                wi = fma_s(neg_s(conj_s(dl)), aw[0], scale_s(conj_s(sg), phi));
-                zcol[(int64_t)i * p.ld] = ZW<S>{zi, wi};
+                ZWK<S, K> out;
+#pragma unroll
+                for (int h = 0; h < K; ++h) {
+                    zi[h] = fma_s(neg_s(dl), az[h], scale_s(sg, phi[h]));
+                    wi[h] = fma_s(neg_s(conj_s(dl)), aw[h], scale_s(conj_s(sg), phi[h]));
+                    out.v[h] = ZW<S>{zi[h], wi[h]};
+                }
+                st_zwk<S, K>(zcol + (int64_t)i * p.ld, out);
                 if (want_full && sampling) {
                     const int64_t ts = s - p.snap_s0;
-                    p.snap_x[(ts * p.n + i) * p.ld + chain] = zi;
-                    p.snap_y[(ts * p.n + i) * p.ld + chain] = wi;
+#pragma unroll
+                    for (int h = 0; h < K; ++h) {
+                        p.snap_x[(ts * p.n + i) * p.ld + chain + h] = zi[h];
+                        p.snap_y[(ts * p.n + i) * p.ld + chain + h] = wi[h];
+                    }
                 }
             }
-            __syncwarp();  // the row's C stores are ordered before its counter update
-            if (valid && c == 0) {
+            __syncwarp();  // the row's stores are ordered before its counter update
+            if (valid && cl == 0) {
                 __threadfence_block();  // release
                 *reinterpret_cast<volatile unsigned char *>(done + i) = need;
             }
             if (sampling) {
-                const S zk[1] = {zi}, wk[1] = {wi};
-                const bool ak[1] = {valid && active};
-                accumulate_row<S, P, V, 1>(p, zcol, rec, zk, wk, ak, lane, gleader, towner, sd, sp, want_diag,
+                bool acc[K];
+#pragma unroll
+                for (int h = 0; h < K; ++h) acc[h] = valid && active[h];
+                accumulate_row<S, P, V, K>(p, zcol, rec, zi, wi, acc, lane, gleader, towner, sd, sp, want_diag,
                                            want_pat);
             }
         }
@@ -524,28 +543,36 @@ cudaError_t launch3(const Sweep3Params<S> &p, int threads, cudaStream_t st) {
 
 }  // namespace
 
-template <typename S, int LGP>
-cudaError_t launch4(const Sweep3Params<S> &p, int threads, cudaStream_t st) {
-    constexpr int KS = ScalarTraits<S>::kDoubles == 1 ? 4 : 2;
+template <typename S, int LGP, int K>
+cudaError_t launch4k(const Sweep3Params<S> &p, int threads, cudaStream_t st) {
+    constexpr int KS = ScalarTraits<S>::kDoubles == 1 && K == 1 ? 4 : 2;
     const int C = 1 << p.lgC;
     const int blocks = (p.chains + C - 1) / C;
     const size_t smem = ((size_t)p.n + 15) / 16 * 16;
     cudaError_t e;
     if (threads <= 512) {
-        auto k = sweep4_kernel<S, 2 * KS, 512, LGP>;
+        auto k = sweep4_kernel<S, 2 * KS, 512, LGP, K>;
         e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e == cudaSuccess) k<<<blocks, threads, smem, st>>>(p);
     } else if (threads <= 768) {
-        auto k = sweep4_kernel<S, KS, 768, LGP>;
+        auto k = sweep4_kernel<S, KS, 768, LGP, K>;
         e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e == cudaSuccess) k<<<blocks, threads, smem, st>>>(p);
     } else {
-        auto k = sweep4_kernel<S, KS, 1024, LGP>;
+        auto k = sweep4_kernel<S, KS, 1024, LGP, K>;
         e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e == cudaSuccess) k<<<blocks, threads, smem, st>>>(p);
     }
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
+}
+
+template <typename S, int LGP>
+cudaError_t launch4(const Sweep3Params<S> &p, int threads, cudaStream_t st) {
+    if constexpr (ScalarTraits<S>::kDoubles == 1) {
+        if (p.lgK == 1) return launch4k<S, LGP, 2>(p, threads, st);
+    }
+    return launch4k<S, LGP, 1>(p, threads, st);
 }
 
 template <typename S>

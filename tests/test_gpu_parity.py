@@ -273,21 +273,22 @@ def test_v4_dataflow(mc, orc, monkeypatch):
     # automatic choice: v4 where it applies (configs 2, 3), v3 for C > 32 or trace (configs 4, 5)
     for k, ver in ((3, 4), (2, 4), (5, 3)):
         c, q, run = W.config(k)
-        inv = mc.Inverter(c)
+        inv = mc.Inverter(c, q=q)
         inv.run(run.seed, run.chains, 0, 1, tuple(o for o in run.outputs if o != "full") or ("diag",),
                 group_size=run.group_size)
         assert inv.kernel_info()["version"] == ver, k
         inv.close()
 
 
+@pytest.mark.parametrize("kernel", ["v3", "v4"])
 @pytest.mark.parametrize("K", ["1", "2"])
-def test_v3_chains_per_thread(mc, orc, monkeypatch, K):
-    """v3 with one or two adjacent chains per thread (256-bit state accesses,
-    in-thread pre-summed accumulation) for several chains-per-CTA layouts and
-    group sizes, including an inactive tail chain."""
-    monkeypatch.setenv("MCINV_KERNEL", "v3")
+def test_chains_per_thread(mc, orc, monkeypatch, K, kernel):
+    """v3 and v4 with one or two adjacent chains per thread (256-bit state
+    accesses, in-thread pre-summed accumulation) for several chains-per-CTA
+    layouts and group sizes, including an inactive tail chain."""
+    monkeypatch.setenv("MCINV_KERNEL", kernel)
     monkeypatch.setenv("MCINV_K", K)
-    for C, gs, chains in ((2, 2, 62), (8, 8, 64), (16, 4, 60), (64, 32, 96)):
+    for C, gs, chains in ((2, 2, 62), (8, 8, 64), (16, 4, 60)) + (((64, 32, 96),) if kernel == "v3" else ()):
         monkeypatch.setenv("MCINV_C", str(C))
         compare_run(mc, orc, W.pedigree(400, seed=23), seed=7, chains=chains, burn_in=2, cycles=3,
                     outputs=("diag", "pattern"), group_size=gs)
