@@ -272,7 +272,9 @@ def ours_arm(args):
         tps = committed_traffic(name)
         tr = tps * chains * c.n * sweeps_per_launch if tps else None
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": tr, "traffic_bytes_per_site": tps, "kernel": "sweep3_kernel (K1/K2, v3)",
+                "traffic": tr, "traffic_bytes_per_site": tps,
+                "kernel": {3: "sweep3_kernel (v3, level barriers)", 4: "sweep4_kernel (v4, dataflow)",
+                           1: "sweep_kernel (v1)"}.get(kinfo["version"], str(kinfo)),
                 "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": bytes_launch,
                 "algorithmic_bytes_per_site": b_chain_sweep / c.n,
