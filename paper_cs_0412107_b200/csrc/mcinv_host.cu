@@ -54,6 +54,7 @@ struct LevelDev {
     std::vector<int4> h_rec;                 // level-order records, for the v4 slot arrays
     std::vector<unsigned char> h_dsg;        // level-order {delta, sigma} (raw bytes of S)
     std::vector<int> h_ph_row;
+    std::vector<int> h_ent_col;              // level-order entry columns (v4 slot ordering)
     struct Slots {
         DevBuf rec, dsg;
         int nslots = 0;
@@ -578,6 +579,7 @@ LevelDev *get_levels(mcinv_ctx *ctx, unsigned outputs) {
         ld->h_dsg.assign(reinterpret_cast<const unsigned char *>(dsg.data()),
                          reinterpret_cast<const unsigned char *>(dsg.data() + dsg.size()));
         ld->h_ph_row = P.ph_row;
+        ld->h_ent_col = P.ent_col;
         if (!ctx->host_only) P = mcinv::LevelPlan();  // device copy only
     }
     LevelDev *raw = ld.get();
@@ -595,8 +597,25 @@ LevelDev::Slots *get_slots(mcinv_ctx *ctx, LevelDev *lv, int R) {
     std::vector<int4> rec;
     std::vector<S> dsg;
     const S *hd = reinterpret_cast<const S *>(lv->h_dsg.data());
+    // optional (MCINV_SLOT_ORDER=1): within a level, rows whose lower neighbours got the
+    // earliest slots first (fewer counter waits); measured neutral on config 2 (dependency
+    // waits are rare), so the default keeps the planner's order (decreasing entry count)
+    const char *so = std::getenv("MCINV_SLOT_ORDER");
+    const bool by_ready = so && std::atoi(so) != 0;
+    std::vector<int> slot_of(ctx->n, -1);
     for (int l = 0; l < lv->D; ++l) {
+        std::vector<std::pair<int, int>> rows;  // (ready slot, level-order index)
         for (int o = lv->h_ph_row[l]; o < lv->h_ph_row[l + 1]; ++o) {
+            const int4 r = lv->h_rec[o];
+            int ready = -1;
+            for (int e = 0; e < (r.z >> 16); ++e) ready = std::max(ready, slot_of[lv->h_ent_col[r.y + e]]);
+            rows.push_back({by_ready ? ready : 0, o});
+        }
+        std::stable_sort(rows.begin(), rows.end(),
+                         [](const std::pair<int, int> &x, const std::pair<int, int> &y) { return x.first < y.first; });
+        for (const auto &ro : rows) {
+            const int o = ro.second;
+            slot_of[lv->h_rec[o].x] = (int)rec.size();
             rec.push_back(lv->h_rec[o]);
             dsg.push_back(hd[2 * o]);
             dsg.push_back(hd[2 * o + 1]);
