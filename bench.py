@@ -152,6 +152,16 @@ def load_peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+def load_fp64_peak():
+    """FP64 tensor-core yardstick measured on this pool's B200 (tools/fp64_peak.py)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "fp64_peak.json")) as f:
+            d = json.load(f)
+        return float(d["zgemm_4096x1024_conjT_tflops"]), "measured cuBLAS ZGEMM (profiles/fp64_peak.json)"
+    except (OSError, KeyError, ValueError):
+        return 35.0, "fallback (cuBLAS DGEMM measured in round 1)"
+
+
 def algorithmic_bytes_per_chain_sweep(c) -> int:
     """per site-update, the z gathers of row i (nnz of R_i),
     the w gathers of column i (nnz of K_i) and the two stores, e bytes each:
@@ -280,6 +290,19 @@ def ours_arm(args):
                 "algorithmic_bytes_per_site": b_chain_sweep / c.n,
                 "sweep_ms_per_launch": sweep_launch_ms,
                 "sweep_share_of_step": st["sweep_ms"] / (ms * args.steps)}
+
+    if "full" in outputs and st["contract_launches"]:
+        # the full-inverse contraction dominates (config 3): FP64 tensor-core (DMMA) bound;
+        # peak = cuBLAS ZGEMM measured on this box (profiles/fp64_peak.json), else cuBLAS DGEMM
+        flops = (8.0 if np.iscomplexobj(c.val) else 2.0) * c.n * c.n * chains * run.cycles
+        cms = st["contract_ms"] / args.steps
+        fp = load_fp64_peak()
+        achieved_tf = flops / (cms / 1e3) / 1e12
+        roof = {"bound": "tensor", "achieved": achieved_tf, "peak": fp[0], "unit": "TFLOP/s",
+                "frac": achieved_tf / fp[0] if fp[0] else None, "traffic": None, "peak_source": fp[1],
+                "kernel": "contract_kernel (K3, DMMA mma.sync.m8n8k4.f64)", "contract_ms_per_step": cms,
+                "contract_share_of_step": st["contract_ms"] / (ms * args.steps),
+                "algorithmic_flops_per_step": flops}
 
     # e2e: the public API from host CSR to host estimates, every step
     e2e = None

@@ -6,7 +6,14 @@
 // error group g (gs consecutive chains) this kernel adds
 //     A_g[i][j] += sum_{t < T} sum_{c in g} X[t][i][c] * conj(Y[t][j][c])
 // i.e. sum_k z^(k) w^(k)dagger of Eq. (1/C), as a GEMM with
-// K = T * gs. Complex: Re A += Xr Yr^T + Xi Yi^T, Im A += Xi Yr^T - Xr Yi^T.
+// K = T * gs. Complex: Re A += Xr Yr^T + Xi Yi^T, Im A += Xi Yr^T - Xr Yi^T
+// (four real DMMA products per complex 8x8x4 step).
+//
+// CTA tile 64 x 64 outputs (4 warps, 32 x 32 each), K staged in chunks of
+// KC = 16 by cp.async into a double-buffered shared-memory pipeline, k-major
+// with a padded row stride so the m8n8k4 fragment loads (lane -> row = lane/4,
+// k = lane%4) are bank-conflict free; complex values stay interleaved (one
+// 16-B shared load gives both parts of a fragment element).
 #include "mcinv_internal.cuh"
 #include "scalar.cuh"
 
@@ -14,7 +21,7 @@ namespace mcinv {
 
 namespace {
 
-constexpr int BM = 64, BN = 64, KC = 16, PADK = KC + 1;
+constexpr int BM = 64, BN = 64, KC = 16;
 
 __device__ __forceinline__ void dmma(double &d0, double &d1, double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -22,89 +29,133 @@ __device__ __forceinline__ void dmma(double &d0, double &d1, double a, double b)
                  : "d"(a), "d"(b));
 }
 
-__device__ __forceinline__ double re_of(double v) { return v; }
-__device__ __forceinline__ double im_of(double) { return 0.0; }
-__device__ __forceinline__ double re_of(cd v) { return v.re; }
-__device__ __forceinline__ double im_of(cd v) { return v.im; }
+__device__ __forceinline__ void cp_async(void *smem, const void *gmem, bool pred) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    const int bytes = pred ? 16 : 0;  // src-size 0: zero-fill (rows past n, k past K)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void *smem, const void *gmem, bool pred) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    const int bytes = pred ? 8 : 0;
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(s), "l"(gmem), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// shared tile: [KC][row stride] elements; stride chosen conflict-free for the fragment pattern
+template <typename S> struct Tile;
+template <> struct Tile<double> { static constexpr int LD = BM + 4; };  // 8-B elements
+template <> struct Tile<cd> { static constexpr int LD = BM + 2; };      // 16-B elements
+
+template <typename S>
+__device__ __forceinline__ void stage(S *sm, const S *g, int t0k, int i0, int n, int ld, int gs, int c0, int K,
+                                     int tid) {
+    // element (k, r) of the chunk = g[((t) * n + i0 + r) * ld + c0 + c], k = t0k + kk, t = k / gs, c = k % gs
+    constexpr int LDS = Tile<S>::LD;
+    for (int e = tid; e < KC * BM; e += 128) {
+        const int r = e / KC, kk = e % KC;  // consecutive threads: consecutive chains (contiguous in gmem)
+        const int k = t0k + kk;
+        const bool ok = k < K && i0 + r < n;
+        const int t = ok ? k / gs : 0, c = ok ? k % gs : 0;
+        const S *src = g + ((int64_t)t * n + (ok ? i0 + r : 0)) * ld + c0 + c;
+        if constexpr (ScalarTraits<S>::kDoubles == 2) cp_async(sm + kk * LDS + r, src, ok);
+        else cp_async8(sm + kk * LDS + r, src, ok);
+    }
+}
 
 template <typename S, bool CPLX>
 __global__ void __launch_bounds__(128) contract_kernel(const S *__restrict__ x, const S *__restrict__ y,
                                                       double *__restrict__ acc, int n, int ld, int gs, int T) {
-    __shared__ double xr[BM][PADK], yr[BN][PADK];
-    __shared__ double xi[CPLX ? BM : 1][PADK], yi[CPLX ? BN : 1][PADK];
+    constexpr int LDS = Tile<S>::LD;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    S *xs = reinterpret_cast<S *>(smem_raw);  // [2][KC][LDS]
+    S *ys = xs + 2 * KC * LDS;                // [2][KC][LDS]
     const int g = blockIdx.z;
     const int i0 = blockIdx.y * BM, j0 = blockIdx.x * BN;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
-    const int K = T * gs;
+    const int K = T * gs, c0 = g * gs;
     double cr[4][4][2], ci[4][4][2];
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
         for (int b = 0; b < 4; ++b) cr[a][b][0] = cr[a][b][1] = ci[a][b][0] = ci[a][b][1] = 0.0;
 
-    for (int k0 = 0; k0 < K; k0 += KC) {
-        // stage X[i0:i0+64, k0:k0+KC] and Y[j0:j0+64, k0:k0+KC]
-        for (int e = threadIdx.x; e < BM * KC; e += blockDim.x) {
-            const int r = e / KC, kk = e % KC, k = k0 + kk;
-            const int t = k / gs, c = g * gs + k % gs;
-            S vx = zero_s<S>(), vy = zero_s<S>();
-            if (k < K) {
-                if (i0 + r < n) vx = x[((int64_t)t * n + i0 + r) * ld + c];
-                if (j0 + r < n) vy = y[((int64_t)t * n + j0 + r) * ld + c];
-            }
-            xr[r][kk] = re_of(vx);
-            yr[r][kk] = re_of(vy);
-            if constexpr (CPLX) {
-                xi[r][kk] = im_of(vx);
-                yi[r][kk] = im_of(vy);
-            }
+    const int nk = (K + KC - 1) / KC;
+    stage<S>(xs, x, 0, i0, n, ld, gs, c0, K, tid);
+    stage<S>(ys, y, 0, j0, n, ld, gs, c0, K, tid);
+    cp_commit();
+    for (int kc = 0; kc < nk; ++kc) {
+        const int buf = kc & 1;
+        if (kc + 1 < nk) {
+            stage<S>(xs + (buf ^ 1) * KC * LDS, x, (kc + 1) * KC, i0, n, ld, gs, c0, K, tid);
+            stage<S>(ys + (buf ^ 1) * KC * LDS, y, (kc + 1) * KC, j0, n, ld, gs, c0, K, tid);
         }
+        cp_commit();
+        cp_wait<1>();
         __syncthreads();
+        const S *xb = xs + buf * KC * LDS, *yb = ys + buf * KC * LDS;
 #pragma unroll
         for (int ks = 0; ks < KC; ks += 4) {
-            const int ka = ks + (lane & 3);
-            double ar[4], br[4], ai[4], bi[4];
+            const int kk = ks + (lane & 3);
+            S av[4], bv[4];
 #pragma unroll
             for (int a = 0; a < 4; ++a) {
-                ar[a] = xr[wm + a * 8 + (lane >> 2)][ka];
-                br[a] = yr[wn + a * 8 + (lane >> 2)][ka];
-                if constexpr (CPLX) {
-                    ai[a] = xi[wm + a * 8 + (lane >> 2)][ka];
-                    bi[a] = yi[wn + a * 8 + (lane >> 2)][ka];
-                }
+                av[a] = xb[kk * LDS + wm + a * 8 + (lane >> 2)];
+                bv[a] = yb[kk * LDS + wn + a * 8 + (lane >> 2)];
             }
 #pragma unroll
             for (int a = 0; a < 4; ++a)
 #pragma unroll
                 for (int b = 0; b < 4; ++b) {
-                    dmma(cr[a][b][0], cr[a][b][1], ar[a], br[b]);
                     if constexpr (CPLX) {
-                        dmma(cr[a][b][0], cr[a][b][1], ai[a], bi[b]);
-                        dmma(ci[a][b][0], ci[a][b][1], ai[a], br[b]);
-                        dmma(ci[a][b][0], ci[a][b][1], -ar[a], bi[b]);
+                        dmma(cr[a][b][0], cr[a][b][1], av[a].re, bv[b].re);
+                        dmma(cr[a][b][0], cr[a][b][1], av[a].im, bv[b].im);
+                        dmma(ci[a][b][0], ci[a][b][1], av[a].im, bv[b].re);
+                        dmma(ci[a][b][0], ci[a][b][1], -av[a].re, bv[b].im);
+                    } else {
+                        dmma(cr[a][b][0], cr[a][b][1], av[a], bv[b]);
                     }
                 }
         }
         __syncthreads();
     }
-    // accumulate into A_g (layout [G][n][n] x e doubles)
+    // accumulate into A_g (layout [G][n][n] x e doubles): each lane owns 2 adjacent columns
     const int e = CPLX ? 2 : 1;
     double *out = acc + (int64_t)g * n * n * e;
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
-        for (int b = 0; b < 4; ++b)
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int i = i0 + wm + a * 8 + (lane >> 2);
-                const int j = j0 + wn + b * 8 + (lane & 3) * 2 + h;
-                if (i < n && j < n) {
-                    double *p = out + ((int64_t)i * n + j) * e;
-                    p[0] += cr[a][b][h];
-                    if (CPLX) p[1] += ci[a][b][h];
+        for (int b = 0; b < 4; ++b) {
+            const int i = i0 + wm + a * 8 + (lane >> 2);
+            const int j = j0 + wn + b * 8 + (lane & 3) * 2;
+            if (i >= n) continue;
+            double *p = out + ((int64_t)i * n + j) * e;
+            if (CPLX) {
+                if (j + 1 < n) {
+                    double4 v = *reinterpret_cast<double4 *>(p);
+                    v.x += cr[a][b][0];
+                    v.y += ci[a][b][0];
+                    v.z += cr[a][b][1];
+                    v.w += ci[a][b][1];
+                    *reinterpret_cast<double4 *>(p) = v;
+                } else if (j < n) {
+                    p[0] += cr[a][b][0];
+                    p[1] += ci[a][b][0];
+                }
+            } else {
+                if (j + 1 < n && ((reinterpret_cast<uintptr_t>(p) & 15) == 0)) {
+                    double2 v = *reinterpret_cast<double2 *>(p);
+                    v.x += cr[a][b][0];
+                    v.y += cr[a][b][1];
+                    *reinterpret_cast<double2 *>(p) = v;
+                } else {
+                    if (j < n) p[0] += cr[a][b][0];
+                    if (j + 1 < n) p[1] += cr[a][b][1];
                 }
             }
+        }
 }
 
 }  // namespace
@@ -114,7 +165,10 @@ void launch_contract(const S *x, const S *y, double *acc, int n, int ld, int cha
                      cudaStream_t st) {
     const int G = chains / gs;
     dim3 grid((n + BN - 1) / BN, (n + BM - 1) / BM, G);
-    contract_kernel<S, ScalarTraits<S>::kDoubles == 2><<<grid, 128, 0, st>>>(x, y, acc, n, ld, gs, T);
+    const size_t smem = 2 * 2 * KC * Tile<S>::LD * sizeof(S);
+    auto k = contract_kernel<S, ScalarTraits<S>::kDoubles == 2>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k<<<grid, 128, smem, st>>>(x, y, acc, n, ld, gs, T);
 }
 
 template void launch_contract<double>(const double *, const double *, double *, int, int, int, int, int,

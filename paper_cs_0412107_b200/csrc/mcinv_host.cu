@@ -469,9 +469,12 @@ Layout make_layout(const mcinv_ctx *ctx, const mcinv_run_args *a) {
     if (a->outputs & MCINV_FULL) {
         int T = a->snapshot_sweeps;
         if (T <= 0) {
-            // K = T * gs >= 256 per contraction, bounded by cycles
-            T = (int)std::max<int64_t>(1, 256 / a->group_size);
+            // K = T * gs >= 1024 per contraction (the A_g tiles are read and written once per
+            // launch), at most 64 sweeps and 16 GB of snapshots, bounded by cycles
+            T = (int)std::max<int64_t>(1, 1024 / a->group_size);
             if (T > 64) T = 64;
+            const int64_t per = 2 * n * (int64_t)L.ld * (int64_t)sz;
+            while (T > 1 && T * per > (int64_t(16) << 30)) T /= 2;
         }
         if (a->cycles > 0 && T > a->cycles) T = (int)a->cycles;
         L.T = std::max(T, 1);
