@@ -57,9 +57,11 @@ typedef enum { MCINV_F64 = 1, MCINV_C128 = 2 } mcinv_dtype;
 
 enum { MCINV_DIAG = 1u, MCINV_PATTERN = 2u, MCINV_FULL = 4u, MCINV_TRACE = 8u };
 
-/* Noise source for Eq. (4)/(5): Gaussian (production), or the constants 0 and
- * 1 (test modes: zero noise reduces CC to Gauss-Seidel, Eq. 12). */
-enum { MCINV_NOISE_GAUSS = 0, MCINV_NOISE_ZERO = 1, MCINV_NOISE_ONE = 2 };
+/* Noise source for Eq. (4)/(5): Gaussian (BASELINE north_star; DESIGN.md
+ * reading R4), Z2 = +-1 (the paper's preferred bounded noise phi = 2B - 1,
+ * P:123-126; reading R21), or the constants 0 and 1 (test modes: zero
+ * noise reduces CC to Gauss-Seidel, Eq. 12). */
+enum { MCINV_NOISE_GAUSS = 0, MCINV_NOISE_ZERO = 1, MCINV_NOISE_ONE = 2, MCINV_NOISE_Z2 = 3 };
 
 /* Build a context for C on CUDA device `device`: validates the CSR, splits
  * C = L + D + U, builds the row lists of Eq. (4) and the

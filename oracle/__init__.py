@@ -23,7 +23,7 @@ _SO = os.path.join(_HERE, "liboracle.so")
 _lib = None
 
 DIAG, PATTERN, FULL, TRACE = 1, 2, 4, 8
-NOISE_GAUSS, NOISE_ZERO, NOISE_ONE = 0, 1, 2
+NOISE_GAUSS, NOISE_ZERO, NOISE_ONE, NOISE_Z2 = 0, 1, 2, 3
 OUT_BITS = {"diag": DIAG, "pattern": PATTERN, "full": FULL, "trace": TRACE}
 ERRORS = {1: "invalid", 2: "zero diagonal", 3: "diagonal domain", 4: "diverged", 5: "no memory"}
 
@@ -59,6 +59,8 @@ def lib():
         L.orc_gaussian_from_words.restype = ctypes.c_double
         L.orc_gaussian.argtypes = [ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32]
         L.orc_gaussian.restype = ctypes.c_double
+        L.orc_z2.argtypes = [ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32]
+        L.orc_z2.restype = ctypes.c_double
         L.orc_matrix_build.argtypes = [ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                        ctypes.c_int, P(ctypes.c_void_p), P(ctypes.c_int64)]
         L.orc_matrix_free.argtypes = [ctypes.c_void_p]
@@ -95,6 +97,10 @@ def gaussian_from_words(r) -> float:
 
 def gaussian(seed: int, row: int, sweep: int, chain: int) -> float:
     return lib().orc_gaussian(seed, row, sweep, chain)
+
+
+def z2(seed: int, row: int, sweep: int, chain: int) -> float:
+    return lib().orc_z2(seed, row, sweep, chain)
 
 
 def _as_doubles(val: np.ndarray, cplx: bool) -> np.ndarray:

@@ -73,6 +73,20 @@ double orc_gaussian(uint64_t seed, uint32_t row, uint32_t sweep, uint32_t chain)
     return orc_gaussian_from_words(r);
 }
 
+/* Z2 noise, the paper's preferred bounded noise "phi = 2B - 1" with B a
+ * Bernoulli(1/2) variable: E(phi) = 0, E(phi^2) = 1 as
+ * Eq. (5a/5b) require. B is the top bit of word 0 of the Philox block of
+ * counter {row, sweep, chain, 1} (4th word 1: a stream disjoint from the
+ * Gaussian one; reading R21). */
+double orc_z2(uint64_t seed, uint32_t row, uint32_t sweep, uint32_t chain)
+{
+    uint32_t ctr[4], key[2], r[4];
+    ctr[0] = row; ctr[1] = sweep; ctr[2] = chain; ctr[3] = 1u;
+    key[0] = (uint32_t)seed; key[1] = (uint32_t)(seed >> 32);
+    orc_philox4x32_10(ctr, key, r);
+    return (r[0] >> 31) ? -1.0 : 1.0;
+}
+
 /* ----------------------------------------------------------- matrix ----- */
 
 typedef struct { double re, im; } cx;
@@ -274,6 +288,7 @@ static double noise(const orc_args *a, int64_t i, int64_t k, int64_t c)
 {
     if (a->noise == ORC_NOISE_ZERO) return 0.0;
     if (a->noise == ORC_NOISE_ONE) return 1.0;
+    if (a->noise == ORC_NOISE_Z2) return orc_z2(a->seed, (uint32_t)i, (uint32_t)k, (uint32_t)c);
     return orc_gaussian(a->seed, (uint32_t)i, (uint32_t)k, (uint32_t)c);
 }
 

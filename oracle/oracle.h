@@ -22,7 +22,7 @@ extern "C" {
 enum { ORC_OK = 0, ORC_E_INVALID = 1, ORC_E_ZERO_DIAG = 2, ORC_E_DIAG_DOMAIN = 3,
        ORC_E_DIVERGED = 4, ORC_E_NOMEM = 5 };
 enum { ORC_DIAG = 1u, ORC_PATTERN = 2u, ORC_FULL = 4u, ORC_TRACE = 8u };
-enum { ORC_NOISE_GAUSS = 0, ORC_NOISE_ZERO = 1, ORC_NOISE_ONE = 2 };
+enum { ORC_NOISE_GAUSS = 0, ORC_NOISE_ZERO = 1, ORC_NOISE_ONE = 2, ORC_NOISE_Z2 = 3 };
 
 typedef struct orc_matrix orc_matrix;
 
@@ -34,6 +34,10 @@ double orc_gaussian_from_words(const uint32_t r[4]);
 
 /* phi(c,k,i) = Gaussian(Philox(ctr={row, sweep, chain, 0}, key=seed)). */
 double orc_gaussian(uint64_t seed, uint32_t row, uint32_t sweep, uint32_t chain);
+
+/* Z2 noise phi = +-1 (reading R21): the top bit of
+ * word 0 of Philox(ctr={row, sweep, chain, 1}, key=seed); 1 -> -1, 0 -> +1. */
+double orc_z2(uint64_t seed, uint32_t row, uint32_t sweep, uint32_t chain);
 
 /* Build the split C = L + D + U.  values: n_nz doubles (real) or
  * 2*n_nz doubles (complex, interleaved re,im). Duplicates are summed.

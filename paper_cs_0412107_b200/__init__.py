@@ -25,7 +25,7 @@ _lib = None
 
 DIAG, PATTERN, FULL, TRACE = 1, 2, 4, 8
 OUTPUTS = {"diag": DIAG, "pattern": PATTERN, "full": FULL, "trace": TRACE}
-NOISE = {"gauss": 0, "zero": 1, "one": 2}
+NOISE = {"gauss": 0, "zero": 1, "one": 2, "z2": 3}
 F64, C128 = 1, 2
 
 __all__ = ["Inverter", "MCInvError", "load", "philox", "gaussian", "OUTPUTS"]

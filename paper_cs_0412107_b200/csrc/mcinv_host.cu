@@ -414,7 +414,7 @@ mcinv_status check_args(const mcinv_ctx *ctx_c, const mcinv_run_args *a) {
         return fail(ctx, MCINV_E_INVALID, "chain or sweep index exceeds the 32-bit noise counter");
     if (a->outputs & ~15u) return fail(ctx, MCINV_E_INVALID, "unknown output bit");
     if ((a->outputs & MCINV_TRACE) && !ctx->have_q) return fail(ctx, MCINV_E_STATE, "TRACE needs mcinv_set_trace_q");
-    if (a->noise < 0 || a->noise > 2) return fail(ctx, MCINV_E_INVALID, "noise mode");
+    if (a->noise < 0 || a->noise > 3) return fail(ctx, MCINV_E_INVALID, "noise mode");
     if (a->chains > (int64_t(1) << 30)) return fail(ctx, MCINV_E_INVALID, "too many chains for one call");
     return MCINV_OK;
 }

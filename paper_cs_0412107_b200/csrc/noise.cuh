@@ -94,4 +94,20 @@ __device__ __forceinline__ double gaussian(uint32_t row, uint32_t sweep, uint32_
     return box_muller(philox4x32_10(row, sweep, chain, 0u, k0, k1));
 }
 
+// Z2 noise phi = 2B - 1 (reading R21): B = top bit
+// of word 0 of Philox(counter {row, sweep, chain, 1}): a stream disjoint from
+// the Gaussian one. 1 -> -1, 0 -> +1.
+__device__ __forceinline__ double z2_noise(uint32_t row, uint32_t sweep, uint32_t chain, uint32_t k0, uint32_t k1) {
+    return (philox4x32_10(row, sweep, chain, 1u, k0, k1).x >> 31) ? -1.0 : 1.0;
+}
+
+// phi(chain, sweep, row) for the run's noise mode: 0 Gaussian, 3 Z2, 1/2 the
+// test constants 0/1 (MCINV_NOISE_*)
+__device__ __forceinline__ double noise_phi(int mode, uint32_t row, uint32_t sweep, uint32_t chain, uint32_t k0,
+                                            uint32_t k1) {
+    if (mode == 0) return gaussian(row, sweep, chain, k0, k1);
+    if (mode == 3) return z2_noise(row, sweep, chain, k0, k1);
+    return mode == 2 ? 1.0 : 0.0;
+}
+
 }  // namespace mcinv

@@ -58,9 +58,7 @@ __global__ void __launch_bounds__(128) sweep_kernel(const SweepParams<S> p) {
                 az = fma_s(ldg_s(p.A.u_a + e), v.z, az);
                 aw = fma_s(ldg_s(p.A.u_b + e), v.w, aw);
             }
-            double phi;
-            if (p.noise == 0) phi = gaussian(static_cast<uint32_t>(i), k, gchain, p.key0, p.key1);
-            else phi = p.noise == 2 ? 1.0 : 0.0;
+            const double phi = noise_phi(p.noise, static_cast<uint32_t>(i), k, gchain, p.key0, p.key1);
             const S dl = ldg_s(p.A.delta + i), sg = ldg_s(p.A.sigma + i);
             const S zi = fma_s(neg_s(dl), az, scale_s(sg, phi));
             const S wi = fma_s(neg_s(conj_s(dl)), aw, scale_s(conj_s(sg), phi));

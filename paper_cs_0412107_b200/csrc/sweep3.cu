@@ -299,10 +299,8 @@ __global__ void __launch_bounds__(NT, 1) sweep3_kernel(const Sweep3Params<S> p) 
                     double phi[K];
 #pragma unroll
                     for (int h = 0; h < K; ++h) {
-                        if (p.noise == 0)
-                            phi[h] = gaussian(static_cast<uint32_t>(i), k, p.chain0 + static_cast<uint32_t>(chain + h),
-                                              p.key0, p.key1);
-                        else phi[h] = p.noise == 2 ? 1.0 : 0.0;
+                        phi[h] = noise_phi(p.noise, static_cast<uint32_t>(i), k,
+                                           p.chain0 + static_cast<uint32_t>(chain + h), p.key0, p.key1);
                     }
                     S az[K], aw[K];
 #pragma unroll
@@ -456,10 +454,8 @@ __global__ void __launch_bounds__(NT, 1) sweep4_kernel(const Sweep3Params<S> p) 
                 double phi[K];
 #pragma unroll
                 for (int h = 0; h < K; ++h) {
-                    if (p.noise == 0)
-                        phi[h] = gaussian(static_cast<uint32_t>(i), k, p.chain0 + static_cast<uint32_t>(chain + h),
-                                          p.key0, p.key1);
-                    else phi[h] = p.noise == 2 ? 1.0 : 0.0;
+                    phi[h] = noise_phi(p.noise, static_cast<uint32_t>(i), k,
+                                       p.chain0 + static_cast<uint32_t>(chain + h), p.key0, p.key1);
                 }
                 // wait for the lower neighbours (the first nlow entries; all lanes of the
                 // row read the same counters: smem broadcast), then acquire

@@ -54,15 +54,16 @@ def est_match(eg, eo, tol=TOL_EST, what=""):
 
 
 def compare_run(mc, orc, c, q=None, pattern=None, seed=1, chains=64, burn_in=5, cycles=10, outputs=("diag",),
-                group_size=32, chain_begin=0, snapshot_sweeps=0):
+                group_size=32, chain_begin=0, snapshot_sweeps=0, noise="gauss"):
     inv = mc.Inverter(c, q=q, pattern=pattern)
     inv.run(seed, chains, burn_in, cycles, outputs, chain_begin=chain_begin, group_size=group_size,
-            snapshot_sweeps=snapshot_sweeps)
+            snapshot_sweeps=snapshot_sweeps, noise=noise)
     res = {o: inv.result(o) for o in outputs}
     zg, wg = inv.get_state()
     om = orc.Matrix(c, q=q, pattern=pattern if pattern is not None else
                     (np.repeat(np.arange(c.n), np.diff(c.row_ptr)).astype(np.int32), c.col))
-    r = om.run(seed, chains, burn_in, cycles, outputs, chain_begin=chain_begin)
+    r = om.run(seed, chains, burn_in, cycles, outputs, chain_begin=chain_begin,
+               noise={"gauss": orc.NOISE_GAUSS, "z2": orc.NOISE_Z2}[noise])
     states_match(zg, wg, r["z"], r["w"])
     for o in outputs:
         eo, so = orc.estimate(r[o], cycles, group_size=group_size, chain_begin=chain_begin)
@@ -294,6 +295,19 @@ def test_chains_per_thread(mc, orc, monkeypatch, K, kernel):
                     outputs=("diag", "pattern"), group_size=gs)
         compare_run(mc, orc, W.dense_config1(24, seed=24), seed=8, chains=chains, burn_in=1, cycles=3,
                     outputs=("diag", "full"), group_size=gs, snapshot_sweeps=2)
+
+
+@pytest.mark.parametrize("kernel", ["v1", "v3", "v4"])
+def test_z2_noise_parity(mc, orc, kernel, monkeypatch):
+    """NEXT-1 Z2 noise (reading R21) on every sweep kernel:
+    states and estimates vs the oracle on the same seed."""
+    monkeypatch.setenv("MCINV_KERNEL", kernel)
+    compare_run(mc, orc, W.pedigree(400, seed=51), seed=11, chains=64, burn_in=2, cycles=4,
+                outputs=("diag", "pattern"), group_size=8, noise="z2")
+    c = W.lattice(4, 3, 0.15, seed=52)
+    outs = ("diag", "trace") if kernel != "v4" else ("diag", "full")
+    compare_run(mc, orc, c, q=W.random_q(c.n, 53, 3) if "trace" in outs else None, seed=12, chains=40, burn_in=2,
+                cycles=3, outputs=outs, group_size=4, noise="z2", snapshot_sweeps=2)
 
 
 def test_v3_custom_pattern_and_threads(mc, orc, monkeypatch):

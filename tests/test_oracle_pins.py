@@ -455,3 +455,42 @@ def test_errors(orc):
     with pytest.raises(orc.OracleError) as e:
         m.run(seed=1, chains=1, burn_in=100, cycles=0)
     assert e.value.code == 4
+
+
+# ------------------------------------------------------------------ Z2 noise (NEXT-1)
+
+def test_z2_noise_bits_and_moments(orc):
+    """Reading R21: phi = +1 / -1 from the top bit of word 0 of
+    Philox({row, sweep, chain, 1}) (Philox pinned above); E(phi) = 0,
+    E(phi^2) = 1 (Eq. 5a/5b, P:166-169; phi = 2B - 1, P:123-126)."""
+    seed = 0x5EED00AA
+    for (i, k, c) in [(0, 0, 0), (5, 7, 3), (19999, 2199, 1023), (2**31, 1, 2**32 - 1)]:
+        w = orc.philox([i, k, c, 1], [seed & 0xFFFFFFFF, seed >> 32])
+        assert orc.z2(seed, i, k, c) == (-1.0 if (w[0] >> 31) else 1.0)
+    x = np.array([orc.z2(seed, i, k, c) for c in range(4) for k in range(50) for i in range(250)])
+    assert set(np.unique(x)) == {-1.0, 1.0}
+    assert abs(x.mean()) < 4 / np.sqrt(x.size)
+
+
+def test_z2_diagonal_is_exact(orc):
+    """P:1044-1048 with Z2 noise: z_i = phi sigma_i, w_i = phi conj(sigma_i), so
+    every sample z_i conj(w_i) = phi^2 / c_ii = 1/c_ii exactly: the estimate of
+    diag(C^-1) is exact with zero variance (the paper's reason to prefer Z2
+    noise, P:141)."""
+    d = np.array([2.0, 4.0, 0.5, 3.0])
+    c = W.diagonal(d)
+    r = orc.Matrix(c).run(seed=3, chains=8, burn_in=1, cycles=5, outputs=("diag",), noise=orc.NOISE_Z2)
+    est, se = orc.estimate(r["diag"], 5, group_size=2)
+    # every sample is the same number fl(sigma_i)^2: zero spread, the value 1/c_ii up to rounding
+    assert np.allclose(est, 1.0 / d, rtol=1e-15, atol=0) and np.all(se == 0)
+
+
+def test_z2_dense_lu_statistics(orc):
+    """Eq. (1/C) with Z2 noise (E(phi phi^T) = I) converges to the dense-LU
+    inverse: aggregate 4-SE rule (reading R14)."""
+    from tests import _stats
+    c = W.random_dense(10, seed=41)
+    inv = np.linalg.inv(c.to_dense())
+    r = orc.Matrix(c).run(seed=9, chains=256, burn_in=20, cycles=200, outputs=("full",), noise=orc.NOISE_Z2)
+    est, se = orc.estimate(r["full"], 200, group_size=8)
+    _stats.check(est.ravel(), inv.ravel(), se.ravel(), G=32, what="z2 full")
