@@ -1,5 +1,7 @@
 // levels.cu -- host planner of the level schedule (levels.h). Host code only.
 #include <algorithm>
+#include <queue>
+#include <tuple>
 #include <unordered_map>
 
 #include "levels.h"
@@ -167,6 +169,74 @@ std::string build_levels(const LevelInput &in, LevelPlan &P) {
         P.max_rows = std::max(P.max_rows, w);
     }
     return "";
+}
+
+std::vector<int> schedule_slots(int64_t n, const std::vector<int4> &rec, const std::vector<int> &ent_col, int R,
+                                int L) {
+    // row i -> level-order index o; lower neighbours (the first nlow entries) and the
+    // reverse edges (upper neighbours)
+    std::vector<int> ord_of(n);
+    for (int64_t o = 0; o < n; ++o) ord_of[rec[o].x] = (int)o;
+    std::vector<int> up_cnt(n + 1, 0);
+    for (int64_t o = 0; o < n; ++o)
+        for (int e = 0; e < (rec[o].z >> 16); ++e) up_cnt[ord_of[ent_col[rec[o].y + e]] + 1]++;
+    for (int64_t o = 0; o < n; ++o) up_cnt[o + 1] += up_cnt[o];
+    std::vector<int> up(up_cnt[n]), fill(up_cnt.begin(), up_cnt.end() - 1);
+    for (int64_t o = 0; o < n; ++o)
+        for (int e = 0; e < (rec[o].z >> 16); ++e) up[fill[ord_of[ent_col[rec[o].y + e]]]++] = (int)o;
+    // height = longest path to a sink (level order is topological: reverse sweep)
+    std::vector<int> height(n, 0);
+    for (int64_t o = n - 1; o >= 0; --o)
+        for (int q = up_cnt[o]; q < up_cnt[o + 1]; ++q) height[o] = std::max(height[o], height[up[q]] + 1);
+    // list scheduling
+    std::vector<int> pending(n), ready_at(n, 0), group_of(n, -1);
+    for (int64_t o = 0; o < n; ++o) pending[o] = rec[o].z >> 16;
+    // candidates keyed by (ready group, -height): rows whose lower neighbours are all placed
+    using Key = std::tuple<int, int, int>;  // (ready group, -height, o)
+    std::priority_queue<Key, std::vector<Key>, std::greater<Key>> waiting;  // by ready group
+    std::priority_queue<std::pair<int, int>> ready;                          // (height, -o) among ready
+    for (int64_t o = 0; o < n; ++o)
+        if (pending[o] == 0) waiting.push(Key(0, -height[o], (int)o));
+    std::vector<int> slots;
+    slots.reserve(n + n / 4);
+    int64_t placed = 0;
+    for (int G = 0; placed < n; ++G) {
+        while (!waiting.empty() && std::get<0>(waiting.top()) <= G) {
+            ready.push({-std::get<1>(waiting.top()), -std::get<2>(waiting.top())});
+            waiting.pop();
+        }
+        int taken = 0;
+        std::vector<int> now;
+        while (taken < R) {
+            int o;
+            if (!ready.empty()) {
+                o = -ready.top().second;
+                ready.pop();
+            } else if (!waiting.empty() && taken == 0) {
+                o = std::get<2>(waiting.top());  // nothing ready: earliest-ready row (it will wait)
+                waiting.pop();
+            } else {
+                break;
+            }
+            now.push_back(o);
+            ++taken;
+        }
+        for (int o : now) {
+            group_of[o] = G;
+            slots.push_back(o);
+            ++placed;
+        }
+        while ((int)slots.size() % R) slots.push_back(-1);
+        // rows of this group release their upper neighbours (not into this group: they
+        // become candidates from group G + L, or G + 1 at the least)
+        for (int o : now)
+            for (int q = up_cnt[o]; q < up_cnt[o + 1]; ++q) {
+                const int u = up[q];
+                ready_at[u] = std::max(ready_at[u], G + std::max(L, 1));
+                if (--pending[u] == 0) waiting.push(Key(ready_at[u], -height[u], u));
+            }
+    }
+    return slots;
 }
 
 }  // namespace mcinv

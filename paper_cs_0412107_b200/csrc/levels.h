@@ -24,6 +24,8 @@
 #include <string>
 #include <vector>
 
+#include <vector_types.h>
+
 namespace mcinv {
 
 struct LevelInput {
@@ -63,5 +65,17 @@ struct LevelPlan {
 
 // Build the plan; returns "" on success or an error message.
 std::string build_levels(const LevelInput &in, LevelPlan &out);
+
+// v4 slot schedule: a topological order of the
+// lower-neighbour DAG cut into warp groups of R rows, where every row is placed
+// at least L groups after the groups of all its lower neighbours when possible
+// (L ~ the groups a CTA has in flight, so the counters it waits for are
+// usually published already), longest remaining path first; a group that
+// cannot be filled with such rows is completed with the rows that become ready
+// earliest, and padded (-1) only when no row is left. Input: the level-order
+// records (i, entry begin, count | lower << 16) and entry columns of the plan.
+// Output: slot -> level-order index (or -1 for padding); size a multiple of R.
+std::vector<int> schedule_slots(int64_t n, const std::vector<int4> &rec, const std::vector<int> &ent_col, int R,
+                                int L);
 
 }  // namespace mcinv

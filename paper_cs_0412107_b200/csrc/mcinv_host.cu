@@ -59,7 +59,7 @@ struct LevelDev {
         DevBuf rec, dsg;
         int nslots = 0;
     };
-    std::map<int, std::unique_ptr<Slots>> slots;  // rows per warp group R -> padded slot arrays
+    std::map<int, std::unique_ptr<Slots>> slots;  // (rows per warp group R, warps W) -> slot arrays
 };
 
 struct Layout {
@@ -593,46 +593,47 @@ LevelDev *get_levels(mcinv_ctx *ctx, unsigned outputs) {
 // v4 slot arrays: level order with every level padded to a multiple of R rows
 // (a warp group of R rows never spans two levels, so its rows are independent)
 template <typename S>
-LevelDev::Slots *get_slots(mcinv_ctx *ctx, LevelDev *lv, int R) {
-    auto it = lv->slots.find(R);
+LevelDev::Slots *get_slots(mcinv_ctx *ctx, LevelDev *lv, int R, int W) {
+    auto it = lv->slots.find(R * 4096 + W);
     if (it != lv->slots.end()) return it->second.get();
     std::unique_ptr<LevelDev::Slots> sl(new LevelDev::Slots());
     std::vector<int4> rec;
     std::vector<S> dsg;
     const S *hd = reinterpret_cast<const S *>(lv->h_dsg.data());
-    // optional (MCINV_SLOT_ORDER=1): within a level, rows whose lower neighbours got the
-    // earliest slots first (fewer counter waits); measured neutral on config 2 (dependency
-    // waits are rare), so the default keeps the planner's order (decreasing entry count)
+    // slot order: the list schedule (levels.h schedule_slots) with a slack of L = W groups
+    // (the warps of a CTA); MCINV_SLOT_ORDER=level keeps plain level order (each level padded)
     const char *so = std::getenv("MCINV_SLOT_ORDER");
-    const bool by_ready = so && std::atoi(so) != 0;
-    std::vector<int> slot_of(ctx->n, -1);
-    for (int l = 0; l < lv->D; ++l) {
-        std::vector<std::pair<int, int>> rows;  // (ready slot, level-order index)
-        for (int o = lv->h_ph_row[l]; o < lv->h_ph_row[l + 1]; ++o) {
-            const int4 r = lv->h_rec[o];
-            int ready = -1;
-            for (int e = 0; e < (r.z >> 16); ++e) ready = std::max(ready, slot_of[lv->h_ent_col[r.y + e]]);
-            rows.push_back({by_ready ? ready : 0, o});
+    std::vector<int> order;
+    if (so && !std::strcmp(so, "level")) {
+        for (int l = 0; l < lv->D; ++l) {
+            for (int o = lv->h_ph_row[l]; o < lv->h_ph_row[l + 1]; ++o) order.push_back(o);
+            while (order.size() % R) order.push_back(-1);
         }
-        std::stable_sort(rows.begin(), rows.end(),
-                         [](const std::pair<int, int> &x, const std::pair<int, int> &y) { return x.first < y.first; });
-        for (const auto &ro : rows) {
-            const int o = ro.second;
-            slot_of[lv->h_rec[o].x] = (int)rec.size();
-            rec.push_back(lv->h_rec[o]);
-            dsg.push_back(hd[2 * o]);
-            dsg.push_back(hd[2 * o + 1]);
+    } else if (const char *e = std::getenv("MCINV_SLACK")) {
+        order = mcinv::schedule_slots(ctx->n, lv->h_rec, lv->h_ent_col, R, std::atoi(e));
+    } else {
+        // the largest slack (W, W/2, W/4 groups) whose schedule pads at most 3% of the
+        // slots: wide DAGs (config 2) take the full slack, narrow ones (lattices) less
+        for (int L = W;; L /= 2) {
+            order = mcinv::schedule_slots(ctx->n, lv->h_rec, lv->h_ent_col, R, L);
+            if (L <= std::max(1, W / 4) || (int64_t)order.size() <= ctx->n + ctx->n * 3 / 100) break;
         }
-        while (rec.size() % R) {
+    }
+    for (int o : order) {
+        if (o < 0) {
             rec.push_back(make_int4(-1, 0, 0, -1));
             dsg.push_back(S{});
             dsg.push_back(S{});
+        } else {
+            rec.push_back(lv->h_rec[o]);
+            dsg.push_back(hd[2 * o]);
+            dsg.push_back(hd[2 * o + 1]);
         }
     }
     sl->nslots = (int)rec.size();
     if (upload(ctx, sl->rec, rec) != MCINV_OK || upload(ctx, sl->dsg, dsg) != MCINV_OK) return nullptr;
     LevelDev::Slots *raw = sl.get();
-    lv->slots[R] = std::move(sl);
+    lv->slots[R * 4096 + W] = std::move(sl);
     return raw;
 }
 
@@ -691,7 +692,18 @@ mcinv_status run_typed(mcinv_ctx *ctx, const mcinv_run_args *a, const Layout &L,
     int lgK = (lv && ctx->dtype == MCINV_F64 && L.lgC >= 1 && a->group_size >= 2 && !lv->deferred) ? 1 : 0;
     if (const char *e = std::getenv("MCINV_K")) lgK = std::atoi(e) >= 2 ? lgK : 0;
     else if (v4) lgK = 0;
-    LevelDev::Slots *sl = v4 ? get_slots<S>(ctx, lv, 32 >> (L.lgC - lgK)) : nullptr;
+    // threads: v3 enough for the widest phase x C/K (<= 768: 85 registers, measured best
+    // for configs 2-5); v4 1024 real / 768 complex (more warps keep more rows in flight;
+    // measured best for configs 2 / 3), fewer for tiny n; a multiple of 32 and of C/K
+    int threads3 = 0;
+    if (lv) {
+        int64_t want = v4 ? std::min<int64_t>(ctx->dtype == MCINV_C128 ? 768 : 1024, (int64_t)n << (L.lgC - lgK))
+                          : std::min<int64_t>(768, (int64_t)std::max(lv->max_rows, 1) << (L.lgC - lgK));
+        if (const char *e = std::getenv("MCINV_THREADS")) want = std::atoi(e);
+        want = std::min<int64_t>(1024, std::max<int64_t>(want, int64_t(1) << (L.lgC - lgK)));
+        threads3 = (int)((want + 31) / 32 * 32);
+    }
+    LevelDev::Slots *sl = v4 ? get_slots<S>(ctx, lv, 32 >> (L.lgC - lgK), threads3 / 32) : nullptr;
     if (v4 && !sl) return fail(ctx, MCINV_E_NOMEM, "v4 slot arrays");
     if (v4 && !ctx->err_flag.p) {
         if (cudaMalloc(&ctx->err_flag.p, 16) != cudaSuccess) return fail(ctx, MCINV_E_NOMEM, "v4 flag");
@@ -702,7 +714,6 @@ mcinv_status run_typed(mcinv_ctx *ctx, const mcinv_run_args *a, const Layout &L,
     ctx->last_C = lv ? (1 << L.lgC) : 32;
     ctx->last_steps = lv ? lv->D : n;
     Sweep3Params<S> q3{};
-    int threads3 = 0;
     if (lv) {
         q3.ph_row = (const int *)lv->ph_row.p;
         q3.ord_rec = (const int4 *)lv->ord_rec.p;
@@ -744,13 +755,6 @@ mcinv_status run_typed(mcinv_ctx *ctx, const mcinv_run_args *a, const Layout &L,
             q3.nslots = sl->nslots;
             q3.err = (unsigned *)ctx->err_flag.p;
         }
-        // threads: enough for the widest phase x C, a multiple of 32 and of C, <= 768 (85
-        // registers per thread: measured best for configs 2-5)
-        int64_t want = (int64_t)std::max(lv->max_rows, 1) << (L.lgC - q3.lgK);
-        want = std::min<int64_t>(v4 ? 1024 : 768, want);  // v4: more warps keep more rows in flight
-        if (const char *e = std::getenv("MCINV_THREADS")) want = std::atoi(e);
-        want = std::min<int64_t>(1024, std::max<int64_t>(want, int64_t(1) << (L.lgC - q3.lgK)));
-        threads3 = (int)((want + 31) / 32 * 32);
     }
     cudaError_t lerr = cudaSuccess;
     auto sweep = [&](int s0, int s1, int snap_s0, unsigned outs) {
