@@ -411,3 +411,30 @@ def test_config4_sampled_sweeps(mc, orc):
     zg, wg = inv.get_state(62, 2)
     r = orc.Matrix(c).run(run.seed, 2, 2, 0, chain_begin=8192 - 2)
     states_match(zg, wg, r["z"], r["w"])
+
+
+# ------------------------------------------------------------- NEXT-3: free Wilson-Dirac
+
+def test_dirac_parity(mc, orc):
+    """Dirac 3^4 lattice (complex non-hermitian, 14 nnz/row): states, diag and
+    tr(Q L^-1) with Q = I vs the oracle on the same seed."""
+    c = W.dirac(3)
+    compare_run(mc, orc, c, q=W.identity_q(c.n), seed=21, chains=64, burn_in=3, cycles=4,
+                outputs=("diag", "trace"), group_size=16)
+
+
+@pytest.mark.slow
+def test_dirac18_trace_matches_paper(mc):
+    """The paper's Dirac case 1 (Tables 3/4: N = 18, K = 0.1, n = 419,904,
+    Q = I): the GPU estimate of tr(L^-1) agrees with the exact value
+    (closed form 413007.825; the paper prints 413007.84) within 4
+    standard errors (scalar rule, reading R14)."""
+    c = W.dirac(18)
+    inv = mc.Inverter(c, q=W.identity_q(c.n))
+    inv.run(0x5EED0012, 2048, 30, 200, ("trace",), group_size=32)
+    est, se = inv.result("trace")
+    exact = W.dirac_trace_closed(18)
+    r = (est.real - exact) / se.real
+    assert abs(r) < 4, (est, se, exact)
+    assert abs(est.imag) < 4 * se.imag + 1e-9
+    inv.close()

@@ -20,11 +20,16 @@ def main():
     ap.add_argument("--repeat", type=int, default=1)
     ap.add_argument("--outputs", default="")
     ap.add_argument("--noise", default="gauss", choices=["gauss", "z2"])
+    ap.add_argument("--dirac", type=int, default=0, help="free Wilson-Dirac N^4 lattice (trace, Q = I) instead")
     a = ap.parse_args()
     import torch
     import workloads as W
     import paper_cs_0412107_b200 as M
     c, q, run = W.config(a.config)
+    if a.dirac:
+        c = W.dirac(a.dirac)
+        q = W.identity_q(c.n)
+        run = W.RunSpec(chains=2048, burn_in=30, cycles=200, outputs=("trace",), seed=0x5EED0012, group_size=32)
     chains = a.chains or run.chains
     outs = tuple(a.outputs.split(",")) if a.outputs else run.outputs
     inv = M.Inverter(c, q=q)

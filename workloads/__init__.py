@@ -23,7 +23,8 @@ import scipy.sparse as sp
 
 __all__ = [
     "CSR", "RunSpec", "dense_config1", "pedigree", "lattice", "random_q",
-    "random_dense", "diagonal", "config", "CONFIGS", "RUN_SEED_BASE",
+    "random_dense", "diagonal", "config", "CONFIGS", "RUN_SEED_BASE", "dirac", "dirac_gammas",
+    "dirac_trace_closed", "identity_q",
 ]
 
 RUN_SEED_BASE = 0x5EED0000
@@ -197,6 +198,80 @@ def lattice_pure_gauge_diag(L: int, d: int, kappa: float, back: float = 0.6) -> 
     lam = 1.0 - kappa * sum(np.exp(1j * p) + back * np.exp(-1j * p) for p in grids)
     v = np.mean(1.0 / lam)
     return float(v.real)
+
+
+# Hermitian Euclidean gamma matrices (Dirac basis): the paper's printed gamma^i =
+# [[0, sigma^i], [sigma^i, 0]] with the Pauli matrices, and gamma^4 =
+# diag(1, 1, -1, -1) instead of the printed [[0, 1], [1, 0]], which commutes
+# with the gamma^i and violates the anticommutator of PAPER.md:731 (finding
+# F5; reading R22). This set satisfies it and gives the paper's
+# "fourteen non zero elements per row".
+_SIGMA = [np.array([[0, 1], [1, 0]], np.complex128), np.array([[0, -1j], [1j, 0]], np.complex128),
+          np.array([[1, 0], [0, -1]], np.complex128)]
+
+
+def dirac_gammas():
+    g = []
+    for s_ in _SIGMA:
+        m = np.zeros((4, 4), np.complex128)
+        m[:2, 2:] = s_
+        m[2:, :2] = s_
+        g.append(m)
+    g.append(np.diag([1.0, 1.0, -1.0, -1.0]).astype(np.complex128))
+    return g
+
+
+def dirac(N: int, K: float = 0.1) -> CSR:
+    """Free Wilson-Dirac matrix of PAPER.md Eq. (disDirac), P:784-796 (NEXT-3):
+    L = 1 + K sum_mu [(1 + gamma^mu) delta_{m+mu, n} + (1 - gamma^mu) delta_{m-mu, n}]
+    on a periodic N^4 lattice, with the index map of P:826-833: row = site +
+    N^4 * spinor, site = x1 + N (x2 + N (x3 + N x0)) (spinor slowest);
+    direction mu = 1, 2, 3, 4 hops along x1, x2, x3, x0 (gamma^1 pairs with
+    the first index). Complex, non-hermitian, n = 4 N^4, 14 nnz/row.
+    """
+    V = N ** 4
+    site = np.arange(V, dtype=np.int64)
+    coord = [(site // N ** k) % N for k in range(4)]
+    gam = dirac_gammas()
+    one = np.eye(4)
+    rows, cols, vals = [], [], []
+    for r in range(4):  # the diagonal
+        rows.append(site + V * r)
+        cols.append(site + V * r)
+        vals.append(np.ones(V, np.complex128))
+    for mu in range(4):
+        for sgn in (+1, -1):
+            nb = site + (((coord[mu] + sgn) % N) - coord[mu]) * N ** mu
+            m = K * (one + sgn * gam[mu])
+            for r in range(4):
+                for rp in range(4):
+                    if m[r, rp] != 0:
+                        rows.append(site + V * r)
+                        cols.append(nb + V * rp)
+                        vals.append(np.full(V, m[r, rp], np.complex128))
+    n = 4 * V
+    mat = sp.coo_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))),
+                        shape=(n, n)).tocsr()
+    return CSR.from_scipy(mat)
+
+
+def dirac_trace_closed(N: int, K: float = 0.1) -> float:
+    """tr(L^-1) of the free Wilson-Dirac matrix: L(p) = a + i gamma.b with a =
+    1 + 2K sum cos p_mu, b_mu = 2K sin p_mu, p_mu = 2 pi k / N, so the spinor
+    trace of L(p)^-1 is 4a / (a^2 + |b|^2) (Clifford relations), summed over
+    momenta (finding F5). A property of the INPUT, not of the method; the paper
+    prints 413007.84 (N = 18) and 629489.14 (N = 20)."""
+    p = 2.0 * np.pi * np.arange(N) / N
+    P = np.meshgrid(p, p, p, p, indexing="ij")
+    a = 1.0 + 2.0 * K * sum(np.cos(x) for x in P)
+    b2 = sum((2.0 * K * np.sin(x)) ** 2 for x in P)
+    return float(np.sum(4.0 * a / (a * a + b2)))
+
+
+def identity_q(n: int, complex_: bool = True) -> CSR:
+    """Q = I: tr(Q C^-1) = tr(C^-1), the paper's Dirac experiments."""
+    v = np.ones(n, np.complex128 if complex_ else np.float64)
+    return CSR(n, np.arange(n + 1, dtype=np.int64), np.arange(n, dtype=np.int32), v)
 
 
 def random_q(n: int, seed: int = 2005, per_row: int = 4, complex_: bool = True) -> CSR:
