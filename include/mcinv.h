@@ -117,6 +117,32 @@ mcinv_status mcinv_workspace_size(const mcinv_ctx *ctx, const mcinv_run_args *ar
  * reported by mcinv_result. */
 mcinv_status mcinv_run(mcinv_ctx *ctx, const mcinv_run_args *args);
 
+/* Coupled burn-in (Alg. 1 steps 1-5; NEXT-2): the number of sweeps
+ * after which two paths started at z = w = 0 and z*_i = w*_i = i (1-based) and
+ * driven by the same noise agree to `tol` in max modulus over all rows of z and
+ * w (reading R23). By Eq. (12) their difference is a noise-free
+ * Gauss-Seidel iterate of C d = 0 and C^dagger d = 0, so it is computed on one
+ * noise-free path from d0 (exact, and the same for every chain). *sweeps
+ * receives that count (use it as burn_in), *diff (may be NULL) the final max
+ * difference. Uses a temporary workspace and replaces the context's last-run
+ * state (call before mcinv_run). Synchronizes `stream`. Errors: E_INVALID (tol
+ * <= 0, max_sweeps < 1), E_DIVERGED (difference non-finite or above 1e12, or
+ * tol not reached within max_sweeps: sp(T) or sp(S) >= 1). */
+mcinv_status mcinv_coupled_burn_in(mcinv_ctx *ctx, double tol, int64_t max_sweeps, void *stream, int64_t *sweeps,
+                                   double *diff);
+
+/* Adaptive stopping (NEXT-2; the paper determines M - N during the run,
+ * P:359-377, Tables 2/4/5): run `args` (burn_in included, args->cycles
+ * ignored) with check_cycles sampling sweeps, then resume in blocks of
+ * check_cycles until max over the elements of |SE| / |estimate| (moduli for
+ * complex elements) of `output` (one
+ * MCINV_* bit present in args->outputs) is below rel_se, or max_cycles sampling
+ * sweeps are done (reading R24). *cycles_done receives the sampling sweeps run,
+ * *rel_se_out (may be NULL) the final relative SE. Needs >= 2 SE groups.
+ * Synchronizes; mcinv_result then reads the final estimate. */
+mcinv_status mcinv_run_until(mcinv_ctx *ctx, const mcinv_run_args *args, unsigned output, double rel_se,
+                             int64_t check_cycles, int64_t max_cycles, int64_t *cycles_done, double *rel_se_out);
+
 /* Borrowed device pointer to the moment vector of the last run, for an
  * all-reduce (SUM, float64) across GPUs that ran disjoint chain ranges:
  *   for each output in the order DIAG, PATTERN, FULL, TRACE present:
@@ -127,7 +153,8 @@ mcinv_status mcinv_run(mcinv_ctx *ctx, const mcinv_run_args *args);
 mcinv_status mcinv_accumulators(mcinv_ctx *ctx, double **dev_ptr, size_t *count);
 
 /* Estimate and standard error of one output from the (possibly all-reduced)
- * moments: estimate = S1 / (total_chains * cycles) (Eq. 1/C); SE =
+ * moments: estimate = S1 / (total_chains * cycles) (Eq. 1/C), cycles =
+ * all sampling sweeps since the last non-resume run; SE =
  * sd(group means)/sqrt(G), G = total_chains / group_size (R15).
  * estimate / std_error receive count*e doubles each (std_error may be NULL);
  * capacity is in doubles. on_device != 0: both are device pointers, written

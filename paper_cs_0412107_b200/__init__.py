@@ -58,6 +58,11 @@ SYMBOLS = {
                                           ctypes.POINTER(ctypes.c_size_t)]),
     "mcinv_result": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_uint, ctypes.c_int64, ctypes.c_void_p,
                                     ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int]),
+    "mcinv_coupled_burn_in": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_double, ctypes.c_int64, ctypes.c_void_p,
+                                             ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_double)]),
+    "mcinv_run_until": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(_RunArgs), ctypes.c_uint, ctypes.c_double,
+                                       ctypes.c_int64, ctypes.c_int64, ctypes.POINTER(ctypes.c_int64),
+                                       ctypes.POINTER(ctypes.c_double)]),
     "mcinv_status_string": (ctypes.c_char_p, [ctypes.c_int]),
     "mcinv_error_detail": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64),
                                           ctypes.POINTER(ctypes.c_char_p)]),
@@ -246,6 +251,49 @@ class Inverter:
         self.cycles = cycles
         self.group_size = group_size
         return self
+
+    def coupled_burn_in(self, tol: float, max_sweeps: int = 100000, stream=None):
+        """Coupled burn-in of Alg. 1 (mcinv_coupled_burn_in): (sweeps, final max difference).
+        Replaces the last-run state (call before run)."""
+        torch = self._torch
+        if stream is None:
+            stream = torch.cuda.current_stream(self.device)
+        sp = stream.cuda_stream if hasattr(stream, "cuda_stream") else stream
+        n = ctypes.c_int64()
+        d = ctypes.c_double()
+        _check(load().mcinv_coupled_burn_in(self._h, tol, max_sweeps, sp, ctypes.byref(n), ctypes.byref(d)), self._h)
+        self._ws = None
+        return n.value, d.value
+
+    def run_until(self, seed: int, chains: int, burn_in: int, outputs: Sequence[str], target: str, rel_se: float,
+                  check_cycles: int = 100, max_cycles: int = 100000, group_size: int = 32, chain_begin: int = 0,
+                  noise: str = "gauss", stream=None):
+        """Adaptive stopping (mcinv_run_until): sampling sweeps in blocks of check_cycles until
+        the relative SE of output `target` is below rel_se. Returns (cycles run, relative SE)."""
+        torch = self._torch
+        if stream is None:
+            stream = torch.cuda.current_stream(self.device)
+        sp = stream.cuda_stream if hasattr(stream, "cuda_stream") else stream
+        a = self._make_args(seed, chains, burn_in, check_cycles, tuple(outputs), chain_begin, 0, group_size, noise,
+                            False, 0, sp)
+        b = ctypes.c_size_t()
+        _check(load().mcinv_workspace_size(self._h, ctypes.byref(a), ctypes.byref(b)), self._h)
+        need = max(int(b.value), 256)
+        if self._ws is None or self._ws.numel() < need:
+            self._ws = None
+            self._ws = torch.empty(need, dtype=torch.uint8, device=f"cuda:{self.device}")
+        a.workspace = self._ws.data_ptr()
+        a.workspace_bytes = self._ws.numel()
+        done = ctypes.c_int64()
+        rse = ctypes.c_double()
+        _check(load().mcinv_run_until(self._h, ctypes.byref(a), OUTPUTS[target], rel_se, check_cycles, max_cycles,
+                                      ctypes.byref(done), ctypes.byref(rse)), self._h)
+        self._args = a
+        self.outputs = tuple(outputs)
+        self.chains = chains
+        self.cycles = done.value
+        self.group_size = group_size
+        return done.value, rse.value
 
     def accumulators(self):
         """Device moment vector (torch float64 view) for an all-reduce."""

@@ -112,6 +112,7 @@ struct mcinv_ctx {
     DevBuf qr_ptr, qr_col, qr_val, qc_ptr, qc_row, qc_val;
     // last run
     bool have_run = false;
+    int64_t acc_cycles = 0;  // sampling sweeps accumulated since the last fresh (non-resume) run
     mcinv_run_args last{};
     Layout lay;
     DevBuf own_ws;
@@ -930,6 +931,7 @@ mcinv_status mcinv_run(mcinv_ctx *ctx, const mcinv_run_args *args) {
     ctx->have_run = false;
     TRY(ctx->dtype == MCINV_C128 ? run_typed<cd>(ctx, args, L, ws, st) : run_typed<double>(ctx, args, L, ws, st));
     ctx->have_run = true;
+    ctx->acc_cycles = args->resume ? ctx->acc_cycles + args->cycles : args->cycles;
     ctx->last = *args;
     ctx->lay = L;
     ctx->ws = ws;
@@ -967,7 +969,7 @@ mcinv_status mcinv_result(mcinv_ctx *ctx, unsigned output, int64_t total_chains,
     const int64_t comps = count * L.e;
     if (capacity < (size_t)comps) return fail(ctx, MCINV_E_BUFFER, "result buffer too small", comps);
     const double *mom = (const double *)(ctx->ws + L.mom);
-    const double cyc = (double)a.cycles;
+    const double cyc = (double)ctx->acc_cycles;  // all sampling sweeps, resumed runs included
     const double G = (double)(total_chains / a.group_size);
     cudaStream_t st = ctx->stream;
     if (on_device) {
@@ -1048,6 +1050,126 @@ mcinv_status mcinv_stats(mcinv_ctx *ctx, int64_t *launches, double *sweep_ms, in
     if (contract_ms) *contract_ms = ms[1];
     if (contract_launches) *contract_launches = cnt[1];
     ctx->launches = 0;
+    return MCINV_OK;
+}
+
+mcinv_status mcinv_coupled_burn_in(mcinv_ctx *ctx, double tol, int64_t max_sweeps, void *stream, int64_t *sweeps,
+                                   double *diff) {
+    // Alg. 1 steps 1-5 by Eq. (12): two paths with the same
+    // noise differ by a Gauss-Seidel iterate of C d = 0 (z) and C^dagger d = 0 (w),
+    // whatever the noise, so the coupled burn-in is the number of noise-free sweeps that
+    // take the start difference d0_i = i + 1 (Alg. 1: z_i = 0, z*_i = i, 1-based) below
+    // tol in max modulus (reading R23). Runs on one 32-chain group with noise 0.
+    if (!ctx || !ctx->valid || !sweeps || !(tol > 0.0) || max_sweeps < 1) return MCINV_E_INVALID;
+    CK(cudaSetDevice(ctx->device));
+    const int64_t n = ctx->n;
+    const int e = ctx->dtype == MCINV_C128 ? 2 : 1;
+    mcinv_run_args a{};
+    a.seed = 0;
+    a.chains = 32;
+    a.burn_in = 0;
+    a.cycles = 0;
+    a.outputs = 0;
+    a.noise = MCINV_NOISE_ZERO;
+    a.group_size = 32;
+    a.stream = stream;
+    size_t bytes = 0;
+    TRY(mcinv_workspace_size(ctx, &a, &bytes));
+    DevBuf tmp;
+    if (cudaMalloc(&tmp.p, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        tmp.p = nullptr;
+        return fail(ctx, MCINV_E_NOMEM, "burn-in workspace");
+    }
+    tmp.bytes = bytes;
+    a.workspace = tmp.p;
+    a.workspace_bytes = bytes;
+    TRY(mcinv_run(ctx, &a));
+    std::vector<double> d0((size_t)32 * n * e, 0.0);
+    for (int64_t c = 0; c < 32; ++c)
+        for (int64_t i = 0; i < n; ++i) d0[(c * n + i) * e] = (double)(i + 1);
+    TRY(mcinv_debug_set_state(ctx, 0, 32, d0.data(), d0.data()));
+    double *dmax = nullptr;
+    CK(cudaMalloc(&dmax, sizeof(double)));
+    const Layout L = ctx->lay;
+    cudaStream_t st = (cudaStream_t)stream;
+    mcinv_status result = MCINV_OK;
+    double last = 0.0;
+    int64_t p = 0;
+    for (p = 1; p <= max_sweeps; ++p) {
+        a.resume = 1;
+        a.burn_in = 1;
+        a.sweep_begin = p - 1;
+        result = mcinv_run(ctx, &a);
+        if (result != MCINV_OK) break;
+        if (ctx->dtype == MCINV_C128)
+            mcinv::launch_max_modulus<cd>((const ZW<cd> *)(ctx->ws + L.zw), (int)n, L.ld, dmax, st);
+        else
+            mcinv::launch_max_modulus<double>((const ZW<double> *)(ctx->ws + L.zw), (int)n, L.ld, dmax, st);
+        if (cudaMemcpyAsync(&last, dmax, sizeof(double), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+            cudaStreamSynchronize(st) != cudaSuccess) {
+            result = fail(ctx, MCINV_E_CUDA, "burn-in reduction");
+            break;
+        }
+        if (!(last <= 1e12)) {
+            result = fail(ctx, MCINV_E_DIVERGED, "coupled paths diverge (sp(T) or sp(S) >= 1)", p);
+            break;
+        }
+        if (last < tol) break;
+    }
+    cudaFree(dmax);
+    ctx->have_run = false;  // the temporary workspace is released
+    if (result != MCINV_OK) return result;
+    if (diff) *diff = last;
+    if (p > max_sweeps) return fail(ctx, MCINV_E_DIVERGED, "burn-in did not reach tol within max_sweeps", max_sweeps);
+    *sweeps = p;
+    return MCINV_OK;
+}
+
+mcinv_status mcinv_run_until(mcinv_ctx *ctx, const mcinv_run_args *args, unsigned output, double rel_se,
+                             int64_t check_cycles, int64_t max_cycles, int64_t *cycles_done, double *rel_se_out) {
+    // Adaptive stopping (the paper determines M - N "by inserting the
+    // calculation of the effective number of cycles during the iteration process"):
+    // run args (burn-in included) with check_cycles sampling sweeps, then resume in
+    // blocks of check_cycles until max |SE / estimate| of `output` is below rel_se
+    // (reading R24; the SE is the group SE of reading R15), or max_cycles.
+    if (!ctx || !ctx->valid || !args || !cycles_done || !(rel_se > 0.0) || check_cycles < 1 ||
+        max_cycles < check_cycles || !(args->outputs & output) || (output & (output - 1)))
+        return MCINV_E_INVALID;
+    if (args->chains / args->group_size < 2) return fail(ctx, MCINV_E_INVALID, "run_until needs >= 2 SE groups");
+    mcinv_run_args a = *args;
+    a.cycles = check_cycles;
+    a.resume = 0;
+    TRY(mcinv_run(ctx, &a));
+    const int64_t count = output == MCINV_DIAG ? ctx->n : output == MCINV_PATTERN ? ctx->pcount
+                          : output == MCINV_FULL ? ctx->n * ctx->n : 1;
+    const int64_t comps = count * (ctx->dtype == MCINV_C128 ? 2 : 1);
+    std::vector<double> est(comps), se(comps);
+    int64_t done = check_cycles;
+    double worst = 0.0;
+    for (;;) {
+        TRY(mcinv_result(ctx, output, a.chains, est.data(), se.data(), comps, 0));
+        // complex elements: moduli of SE and estimate (the paper's Dirac tolerance is
+        // "with respect to the absolute value rather than for real and imaginary part
+        // independently")
+        worst = 0.0;
+        const int e = ctx->dtype == MCINV_C128 ? 2 : 1;
+        for (int64_t c = 0; c < count; ++c) {
+            const double m = e == 2 ? std::hypot(est[2 * c], est[2 * c + 1]) : std::fabs(est[c]);
+            const double s_ = e == 2 ? std::hypot(se[2 * c], se[2 * c + 1]) : se[c];
+            worst = std::max(worst, s_ / (m > 0.0 ? m : 1.0));
+        }
+        if (worst < rel_se || done >= max_cycles) break;
+        mcinv_run_args r = a;
+        r.resume = 1;
+        r.burn_in = 0;
+        r.sweep_begin = a.sweep_begin + a.burn_in + done;
+        r.cycles = std::min(check_cycles, max_cycles - done);
+        TRY(mcinv_run(ctx, &r));
+        done += r.cycles;
+    }
+    *cycles_done = done;
+    if (rel_se_out) *rel_se_out = worst;
     return MCINV_OK;
 }
 

@@ -140,6 +140,8 @@ void launch_finalize(const double *s1, const double *s2, int64_t comps, double m
                      double G, double *est, double *se, cudaStream_t st);
 template <typename S>
 void launch_check(const ZW<S> *zw, int n, int ld, int chains, double *flag, cudaStream_t st);
+template <typename S>
+void launch_max_modulus(const ZW<S> *zw, int n, int ld, double *out, cudaStream_t st);
 void launch_philox(const uint32_t *ctr, int64_t count, uint32_t k0, uint32_t k1, uint32_t *out,
                    double *gauss, cudaStream_t st);
 

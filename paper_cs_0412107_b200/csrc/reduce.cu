@@ -60,6 +60,41 @@ __global__ void check_kernel(const ZW<S> *__restrict__ zw, int n, int ld, int ch
     if ((threadIdx.x & 31) == 0 && bad) atomicAdd(flag, (double)bad);
 }
 
+// max over rows of the (z, w) moduli of chain 0 (the coupled-burn-in difference)
+template <typename S>
+__global__ void max_modulus_kernel(const ZW<S> *__restrict__ zw, int n, int ld, double *out) {
+    double m = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const ZW<S> v = zw[(int64_t)i * ld];
+        double a, b;
+        if constexpr (ScalarTraits<S>::kDoubles == 1) {
+            a = fabs(v.z);
+            b = fabs(v.w);
+        } else {
+            a = hypot(v.z.re, v.z.im);
+            b = hypot(v.w.re, v.w.im);
+        }
+        m = fmax(m, fmax(a, b));
+        if (!(a <= 1e300) || !(b <= 1e300)) m = INFINITY;  // non-finite: diverged
+    }
+    for (int off = 16; off > 0; off >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, off));
+    __shared__ double part[32];
+    if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double r = 0.0;
+        for (int w = 0; w < (int)(blockDim.x + 31) / 32; ++w) r = fmax(r, part[w]);
+        *out = r;
+    }
+}
+
+template <typename S>
+void launch_max_modulus(const ZW<S> *zw, int n, int ld, double *out, cudaStream_t st) {
+    max_modulus_kernel<S><<<1, 1024, 0, st>>>(zw, n, ld, out);
+}
+template void launch_max_modulus<double>(const ZW<double> *, int, int, double *, cudaStream_t);
+template void launch_max_modulus<cd>(const ZW<cd> *, int, int, double *, cudaStream_t);
+
 __global__ void philox_kernel(const uint32_t *__restrict__ ctr, int64_t count, uint32_t k0, uint32_t k1,
                               uint32_t *__restrict__ out, double *__restrict__ gauss) {
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < count;

@@ -438,3 +438,37 @@ def test_dirac18_trace_matches_paper(mc):
     assert abs(r) < 4, (est, se, exact)
     assert abs(est.imag) < 4 * se.imag + 1e-9
     inv.close()
+
+
+# ------------------------------------------------------------- NEXT-2: coupled burn-in, adaptive stopping
+
+@pytest.mark.parametrize("cplx", [False, True])
+def test_coupled_burn_in_matches_gauss_seidel(mc, cplx):
+    """mcinv_coupled_burn_in (Alg. 1 steps 1-5 via Eq. 12) equals the plain
+    Gauss-Seidel count on the start difference (which the oracle's literal
+    four-chain run also reproduces, test_oracle_pins)."""
+    from tests.test_oracle_pins import gs_difference_sweeps
+    c = W.lattice(4, 2, 0.2, seed=61) if cplx else W.pedigree(60, seed=62)
+    inv = mc.Inverter(c)
+    n, d = inv.coupled_burn_in(1e-5)
+    assert n == gs_difference_sweeps(c, 1e-5) and d < 1e-5
+    inv.close()
+
+
+def test_run_until_adaptive(mc, orc):
+    """Adaptive stopping (mcinv_run_until): blocks of sampling sweeps until the
+    relative SE of the trace is below the target; the estimate equals the oracle
+    run with the same total sweeps (resume is exact), and the SE target holds."""
+    c = W.lattice(3, 2, 0.2, seed=63)
+    q = W.identity_q(c.n)
+    inv = mc.Inverter(c, q=q)
+    burn, _ = inv.coupled_burn_in(1e-6)
+    done, rse = inv.run_until(17, 64, burn, ("trace", "diag"), "trace", 2e-3, check_cycles=20, max_cycles=2000,
+                              group_size=8)
+    assert done % 20 == 0 and rse < 2e-3
+    est, se = inv.result("trace")
+    assert abs(se) / abs(est) < 2e-3
+    r = orc.Matrix(c, q=q).run(17, 64, burn, done, ("trace",))
+    eo, so = orc.estimate(r["trace"], done, group_size=8)
+    assert abs(est - eo) < 1e-10 * abs(eo)
+    inv.close()

@@ -494,3 +494,48 @@ def test_z2_dense_lu_statistics(orc):
     r = orc.Matrix(c).run(seed=9, chains=256, burn_in=20, cycles=200, outputs=("full",), noise=orc.NOISE_Z2)
     est, se = orc.estimate(r["full"], 200, group_size=8)
     _stats.check(est.ravel(), inv.ravel(), se.ravel(), G=32, what="z2 full")
+
+
+# ------------------------------------------------------------------ NEXT-2: coupled burn-in (Alg. 1)
+
+def gs_difference_sweeps(c, tol, max_sweeps=10000):
+    """Plain Gauss-Seidel on C d = 0 and C^dagger d = 0 from d0_i = i + 1
+    (numpy, row by row): the first sweep p with max |d| < tol in both."""
+    A = c.to_dense()
+    n = A.shape[0]
+    dz = np.arange(1, n + 1).astype(A.dtype)
+    dw = dz.copy()
+    Ah = A.conj().T
+    for p in range(1, max_sweeps + 1):
+        for i in range(n):
+            dz[i] = -(A[i, :i] @ dz[:i] + A[i, i + 1:] @ dz[i + 1:]) / A[i, i]
+            dw[i] = -(Ah[i, :i] @ dw[:i] + Ah[i, i + 1:] @ dw[i + 1:]) / Ah[i, i]
+        if max(np.max(np.abs(dz)), np.max(np.abs(dw))) < tol:
+            return p
+    raise AssertionError("no convergence")
+
+
+@pytest.mark.parametrize("cplx", [False, True])
+def test_coupled_burn_in_four_chains(orc, cplx):
+    """Algorithm 1 steps 1-5 run literally in the oracle: the pair
+    (z, w) from 0 and (z*, w*) from i + 1 with the same noise; the first sweep
+    where both differences are below tol equals the noise-free Gauss-Seidel
+    count of Eq. (12) that mcinv_coupled_burn_in uses (reading R23)."""
+    c = W.lattice(4, 2, 0.2, seed=61) if cplx else W.pedigree(60, seed=62)
+    tol = 1e-5
+    p_gs = gs_difference_sweeps(c, tol)
+    m = orc.Matrix(c)
+    dt = np.complex128 if cplx else np.float64
+    start = np.arange(1, c.n + 1).astype(dt)
+    snaps = list(range(p_gs + 2))
+    a = m.run(seed=5, chains=1, burn_in=p_gs + 2, cycles=0, snap_sweeps=snaps, chain_begin=3)
+    b = m.run(seed=5, chains=1, burn_in=p_gs + 2, cycles=0, snap_sweeps=snaps, chain_begin=3, z_init=start,
+              w_init=start)
+    first = None
+    for k in snaps:
+        dz = np.max(np.abs(b["z_snap"][k, 0] - a["z_snap"][k, 0]))
+        dw = np.max(np.abs(b["w_snap"][k, 0] - a["w_snap"][k, 0]))
+        if max(dz, dw) < tol:
+            first = k + 1  # snapshot k is taken after sweep k + 1
+            break
+    assert first == p_gs
