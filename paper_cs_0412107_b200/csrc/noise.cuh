@@ -105,9 +105,11 @@ __device__ __forceinline__ double z2_noise(uint32_t row, uint32_t sweep, uint32_
 // test constants 0/1 (MCINV_NOISE_*)
 __device__ __forceinline__ double noise_phi(int mode, uint32_t row, uint32_t sweep, uint32_t chain, uint32_t k0,
                                             uint32_t k1) {
-    if (mode == 0) return gaussian(row, sweep, chain, k0, k1);
-    if (mode == 3) return z2_noise(row, sweep, chain, k0, k1);
-    return mode == 2 ? 1.0 : 0.0;
+    if (mode == 1 || mode == 2) return mode == 2 ? 1.0 : 0.0;
+    // one Philox block: counter word 3 selects the stream (0 Gaussian, 1 Z2)
+    const PhiloxOut r = philox4x32_10(row, sweep, chain, mode == 3 ? 1u : 0u, k0, k1);
+    if (mode == 3) return (r.x >> 31) ? -1.0 : 1.0;
+    return box_muller(r);
 }
 
 }  // namespace mcinv
