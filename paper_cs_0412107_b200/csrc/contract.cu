@@ -105,19 +105,34 @@ __global__ void __launch_bounds__(128) contract_kernel(const S *__restrict__ x, 
                 av[a] = xb[kk * LDS + wm + a * 8 + (lane >> 2)];
                 bv[a] = yb[kk * LDS + wn + a * 8 + (lane >> 2)];
             }
+            // four passes over the 16 tiles: consecutive DMMAs never share an accumulator
+            // (15 independent DMMAs between two updates of the same tile)
+            if constexpr (CPLX) {
+                double na[4];
 #pragma unroll
-            for (int a = 0; a < 4; ++a)
+                for (int a = 0; a < 4; ++a) na[a] = -av[a].re;
 #pragma unroll
-                for (int b = 0; b < 4; ++b) {
-                    if constexpr (CPLX) {
-                        dmma(cr[a][b][0], cr[a][b][1], av[a].re, bv[b].re);
-                        dmma(cr[a][b][0], cr[a][b][1], av[a].im, bv[b].im);
-                        dmma(ci[a][b][0], ci[a][b][1], av[a].im, bv[b].re);
-                        dmma(ci[a][b][0], ci[a][b][1], -av[a].re, bv[b].im);
-                    } else {
-                        dmma(cr[a][b][0], cr[a][b][1], av[a], bv[b]);
-                    }
-                }
+                for (int a = 0; a < 4; ++a)
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) dmma(cr[a][b][0], cr[a][b][1], av[a].re, bv[b].re);
+#pragma unroll
+                for (int a = 0; a < 4; ++a)
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) dmma(ci[a][b][0], ci[a][b][1], av[a].im, bv[b].re);
+#pragma unroll
+                for (int a = 0; a < 4; ++a)
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) dmma(cr[a][b][0], cr[a][b][1], av[a].im, bv[b].im);
+#pragma unroll
+                for (int a = 0; a < 4; ++a)
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) dmma(ci[a][b][0], ci[a][b][1], na[a], bv[b].im);
+            } else {
+#pragma unroll
+                for (int a = 0; a < 4; ++a)
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) dmma(cr[a][b][0], cr[a][b][1], av[a], bv[b]);
+            }
         }
         __syncthreads();
     }

@@ -472,3 +472,25 @@ def test_run_until_adaptive(mc, orc):
     eo, so = orc.estimate(r["trace"], done, group_size=8)
     assert abs(est - eo) < 1e-10 * abs(eo)
     inv.close()
+
+
+@pytest.mark.slow
+def test_config3_full_size_dense_lu(mc, orc):
+    """Config 3 exactly as specified (BASELINE configs[2]: 64^2 complex lattice,
+    2048 chains, 200 + 2000 sweeps, full C^-1 through the DMMA contraction):
+    all 16.7M elements vs the dense LU inverse with the aggregate rule of
+    reading R14 (G = 64 groups), and sampled chains' final states vs the
+    oracle."""
+    c, _, run = W.config(3)
+    inv = mc.Inverter(c)
+    inv.run(run.seed, run.chains, run.burn_in, run.cycles, ("full",), group_size=run.group_size)
+    est, se = inv.result("full")
+    exact = np.linalg.inv(c.to_dense())
+    G = run.chains // run.group_size
+    _stats.check(est.real.ravel(), exact.real.ravel(), se.real.ravel(), G=G, what="config3 full re")
+    _stats.check(est.imag.ravel(), exact.imag.ravel(), se.imag.ravel(), G=G, what="config3 full im")
+    for ch in (0, 2047):
+        r = orc.Matrix(c).run(run.seed, 1, run.burn_in + run.cycles, 0, chain_begin=ch)
+        zg, wg = inv.get_state(ch, 1)
+        states_match(zg, wg, r["z"], r["w"])
+    inv.close()
