@@ -442,9 +442,13 @@ __global__ void __launch_bounds__(NT, 1) sweep4_kernel(const Sweep3Params<S> p) 
         const uint32_t k = p.sweep_abs0 + static_cast<uint32_t>(s);
         const bool sampling = s >= p.burn_in;
         const unsigned char need = static_cast<unsigned char>(s + 1);
+        // the next group's record is loaded one item ahead (off the item's critical path)
+        int4 rec_next = (tid >> 5) < ngroups ? __ldg(p.slot_rec + (tid >> 5) * R + (lane >> lgL))
+                                             : make_int4(-1, 0, 0, -1);
         for (int g = tid >> 5; g < ngroups; g += W) {
             const int slot = g * R + (lane >> lgL);
-            const int4 rec = __ldg(p.slot_rec + slot);
+            const int4 rec = rec_next;
+            if (g + W < ngroups) rec_next = __ldg(p.slot_rec + (g + W) * R + (lane >> lgL));
             const bool valid = rec.x >= 0;
             const int i = rec.x, beg = rec.y, cnt = valid ? rec.z & 0xffff : 0;
             S zi[K], wi[K];
