@@ -200,10 +200,14 @@ def reference_arm(args):
         if s >= args.warmup:
             vals.append(rate)
     value = statistics.mean(vals)
+    c, _, run = W.config(args.config)
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": W.CONFIGS[args.config]["dtype"], "data": "synthetic",
-            "config": {"workload": W.CONFIGS[args.config]["name"]},
+            "config": {"workload": W.CONFIGS[args.config]["name"], "n": c.n, "nnz": c.nnz,
+                       "chains_per_gpu": run.chains, "burn_in": run.burn_in, "cycles": run.cycles,
+                       "outputs": list(run.outputs), "group_size": run.group_size,
+                       "matrix_sha256": c.sha256()[:16]},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
