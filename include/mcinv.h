@@ -199,12 +199,16 @@ mcinv_status mcinv_debug_gaussian(int device, uint64_t seed, int64_t count, cons
 /* Host-only (no GPU needed): mcinv_create's preprocessing and the level
  * planner of the v3 sweep kernel for C, with the
  * default pattern and an optional Q, for the accumulation of `outputs`.
- * level[n] (may be NULL) receives lev(i); info[6] = {levels D, max items of a
+ * level[n] (may be NULL) receives lev(i); info[7] = {levels D, max items of a
  * phase, fused pattern pairs, deferred pattern pairs, trace items, union
- * entries}. For CPU tests of the planner. */
+ * entries, slots}. With slots != NULL also the v4 slot schedule for warp
+ * groups of slot_R rows and slack slot_L groups:
+ * slots[t] = row at slot t or -1 (padding), info[6] = number of slots (E_BUFFER
+ * if above slots_capacity). For CPU tests of the planner. */
 mcinv_status mcinv_debug_levels(mcinv_dtype dtype, int64_t n, const int64_t *row_ptr, const int32_t *col_idx,
                                 const void *values, const int64_t *q_row_ptr, const int32_t *q_col_idx,
-                                const void *q_values, unsigned outputs, int32_t *level, int64_t *info);
+                                const void *q_values, unsigned outputs, int32_t *level, int64_t *info,
+                                int slot_R, int slot_L, int32_t *slots, int64_t slots_capacity);
 /* Copy the state of chains [chain_begin, chain_begin+chains) (relative to the
  * last run's chain_begin) to host arrays z, w of shape [chains][n] (x2 doubles
  * for C128). Synchronizes. */

@@ -78,7 +78,8 @@ SYMBOLS = {
     "mcinv_debug_gaussian": (ctypes.c_int, [ctypes.c_int, ctypes.c_uint64, ctypes.c_int64, ctypes.c_void_p,
                                             ctypes.c_void_p]),
     "mcinv_debug_levels": (ctypes.c_int, [ctypes.c_int, ctypes.c_int64] + [ctypes.c_void_p] * 6 +
-                           [ctypes.c_uint, ctypes.c_void_p, ctypes.c_void_p]),
+                           [ctypes.c_uint, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
+                            ctypes.c_void_p, ctypes.c_int64]),
     "mcinv_debug_get_state": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p,
                                              ctypes.c_void_p]),
     "mcinv_debug_set_state": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p,
@@ -133,8 +134,9 @@ def gaussian(ctr: np.ndarray, seed: int, device: int = 0) -> np.ndarray:
     return out
 
 
-def debug_levels(csr, outputs=("diag",), q=None):
-    """Host-only v3 level schedule (no GPU): (lev[n], info dict). For CPU tests."""
+def debug_levels(csr, outputs=("diag",), q=None, slot_R: int = 0, slot_L: int = 0):
+    """Host-only v3 level schedule (no GPU): (lev[n], info dict); with slot_R > 0
+    also info["slots"], the v4 slot schedule (row per slot, -1 = padding)."""
     cplx = np.iscomplexobj(csr.val)
     rp = np.ascontiguousarray(csr.row_ptr, np.int64)
     col = np.ascontiguousarray(csr.col, np.int32)
@@ -151,10 +153,16 @@ def debug_levels(csr, outputs=("diag",), q=None):
     for o in outputs:
         bits |= OUTPUTS[o]
     lev = np.zeros(csr.n, np.int32)
-    info = np.zeros(6, np.int64)
-    _check(load().mcinv_debug_levels(*args, bits, lev.ctypes.data, info.ctypes.data))
-    names = ["levels", "max_items", "fused_pairs", "deferred_pairs", "trace_items", "entries"]
-    return lev, dict(zip(names, (int(x) for x in info)))
+    info = np.zeros(7, np.int64)
+    cap = max(slot_R, 1) * csr.n + 64  # one row per group at worst
+    slots = np.zeros(cap, np.int32) if slot_R > 0 else None
+    _check(load().mcinv_debug_levels(*args, bits, lev.ctypes.data, info.ctypes.data, slot_R, slot_L,
+                                     None if slots is None else slots.ctypes.data, cap))
+    names = ["levels", "max_items", "fused_pairs", "deferred_pairs", "trace_items", "entries", "nslots"]
+    d = dict(zip(names, (int(x) for x in info)))
+    if slots is not None:
+        d["slots"] = slots[:d["nslots"]].copy()
+    return lev, d
 
 
 class Inverter:

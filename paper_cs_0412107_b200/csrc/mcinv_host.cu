@@ -613,11 +613,15 @@ LevelDev::Slots *get_slots(mcinv_ctx *ctx, LevelDev *lv, int R, int W) {
     } else if (const char *e = std::getenv("MCINV_SLACK")) {
         order = mcinv::schedule_slots(ctx->n, lv->h_rec, lv->h_ent_col, R, std::atoi(e));
     } else {
-        // the largest slack (W, W/2, W/4 groups) whose schedule pads at most 3% of the
-        // slots: wide DAGs (config 2) take the full slack, narrow ones (lattices) less
-        for (int L = W;; L /= 2) {
+        // the largest slack (W, W/2, ..., 1 groups) whose schedule pads at most 3% of the
+        // slots: wide DAGs (config 2) take the full slack, narrow ones (lattices) less;
+        // if none does (a DAG narrower than a warp group), the least padded one
+        std::vector<int> best;
+        for (int L = W; L >= 1; L /= 2) {
             order = mcinv::schedule_slots(ctx->n, lv->h_rec, lv->h_ent_col, R, L);
-            if (L <= std::max(1, W / 4) || (int64_t)order.size() <= ctx->n + ctx->n * 3 / 100) break;
+            if ((int64_t)order.size() <= ctx->n + ctx->n * 3 / 100) break;
+            if (best.empty() || order.size() < best.size()) best = order;
+            if (L == 1) order = best;
         }
     }
     for (int o : order) {
@@ -1175,7 +1179,8 @@ mcinv_status mcinv_run_until(mcinv_ctx *ctx, const mcinv_run_args *args, unsigne
 
 mcinv_status mcinv_debug_levels(mcinv_dtype dtype, int64_t n, const int64_t *row_ptr, const int32_t *col_idx,
                                 const void *values, const int64_t *q_row_ptr, const int32_t *q_col_idx,
-                                const void *q_values, unsigned outputs, int32_t *level, int64_t *info) {
+                                const void *q_values, unsigned outputs, int32_t *level, int64_t *info,
+                                int slot_R, int slot_L, int32_t *info_slots, int64_t slots_capacity) {
     if (!info) return MCINV_E_INVALID;
     mcinv_ctx c;
     mcinv_ctx *ctx = &c;
@@ -1196,6 +1201,20 @@ mcinv_status mcinv_debug_levels(mcinv_dtype dtype, int64_t n, const int64_t *row
     LevelDev *lv = dtype == MCINV_C128 ? get_levels<cd>(ctx, outputs) : get_levels<double>(ctx, outputs);
     if (!lv->error.empty()) return fail(ctx, MCINV_E_INVALID, lv->error);
     const mcinv::LevelPlan &P = lv->host;
+    if (info_slots) {
+        // v4 slot schedule of this plan for R rows per warp group and slack L (levels.h)
+        std::vector<int4> rec(n);
+        for (int64_t o = 0; o < n; ++o) {
+            const int i = P.ord_row[o], beg = P.ord_eptr[o], cnt = P.ord_eptr[o + 1] - beg;
+            int nlow = 0;
+            while (nlow < cnt && P.ent_col[beg + nlow] < i) ++nlow;
+            rec[o] = make_int4(i, beg, cnt | nlow << 16, -1);
+        }
+        const std::vector<int> order = mcinv::schedule_slots(n, rec, P.ent_col, slot_R, slot_L);
+        if ((int64_t)order.size() > slots_capacity) return fail(ctx, MCINV_E_BUFFER, "slots", (int64_t)order.size());
+        for (size_t t = 0; t < order.size(); ++t) info_slots[t] = order[t] < 0 ? -1 : P.ord_row[order[t]];
+        info[6] = (int64_t)order.size();
+    }
     info[0] = P.D;
     info[1] = P.max_rows;
     info[2] = P.fused_pairs;

@@ -108,3 +108,35 @@ def test_trace_items(mc):
     _, info = mc.debug_levels(c, outputs=("trace",), q=q)
     assert info["trace_items"] == int(np.sum(np.diff(q.row_ptr) > 0))
     assert info["levels"] == 2 * 3 + 1
+
+
+@pytest.mark.parametrize("make,R,L", [
+    (lambda: W.pedigree(600, seed=13), 4, 32),
+    (lambda: W.pedigree(600, seed=13), 1, 8),
+    (lambda: W.lattice(8, 2, 0.2, seed=14), 2, 16),
+    (lambda: W.lattice(4, 3, 0.2, seed=15), 8, 4),
+    (lambda: W.dense_config1(20, seed=16), 32, 1),
+])
+def test_v4_slot_schedule(mc, make, R, L):
+    """The v4 slot schedule (levels.cu schedule_slots) is what the dataflow
+    kernel's correctness and deadlock-freedom rest on: every row
+    appears exactly once, the slots come in whole warp groups of R, every
+    lower neighbour of a row sits in an EARLIER group (never the same one:
+    rows of a group run concurrently), and rows are placed at least L groups
+    after their lower neighbours whenever the schedule does not pad."""
+    c = make()
+    _, info = mc.debug_levels(c, slot_R=R, slot_L=L)
+    slots = info["slots"]
+    assert slots.size % R == 0
+    rows = slots[slots >= 0]
+    assert np.array_equal(np.sort(rows), np.arange(c.n))
+    group = np.empty(c.n, np.int64)
+    group[slots[slots >= 0]] = np.nonzero(slots >= 0)[0] // R
+    nb = neighbours(c)
+    for i in range(c.n):
+        for j in nb[i]:
+            if j < i:
+                assert group[j] < group[i]
+    # every group holds at least one row (padding only completes groups)
+    assert slots.size <= R * c.n
+    assert np.all((slots.reshape(-1, R) >= 0).any(axis=1))

@@ -19,7 +19,7 @@ def main():
     ap.add_argument("--chains", type=int, default=0)
     ap.add_argument("--repeat", type=int, default=1)
     ap.add_argument("--outputs", default="")
-    ap.add_argument("--noise", default="gauss", choices=["gauss", "z2"])
+    ap.add_argument("--noise", default="gauss", choices=["gauss", "z2", "zero"])
     ap.add_argument("--dirac", type=int, default=0, help="free Wilson-Dirac N^4 lattice (trace, Q = I) instead")
     a = ap.parse_args()
     import torch
