@@ -27,12 +27,18 @@ using mcinv::ZW;
 
 namespace {
 
+// Device buffers come from the stream-ordered allocator (cudaMallocAsync on the
+// legacy stream, default pool with an unlimited release threshold): creating and
+// destroying contexts does not synchronize the device (cudaFree would), which
+// matters for the end-to-end path (a context per matrix).
+inline cudaError_t dev_alloc(void **p, size_t bytes) { return cudaMallocAsync(p, bytes, 0); }
+
 struct DevBuf {
     void *p = nullptr;
     size_t bytes = 0;
     ~DevBuf() { release(); }
     void release() {
-        if (p) cudaFree(p);
+        if (p) cudaFreeAsync(p, 0);
         p = nullptr;
         bytes = 0;
     }
@@ -161,13 +167,15 @@ mcinv_status upload(mcinv_ctx *ctx, DevBuf &b, const std::vector<T> &h) {
     b.release();
     if (ctx->host_only) return MCINV_OK;
     const size_t bytes = std::max<size_t>(sizeof(T), h.size() * sizeof(T));
-    if (cudaMalloc(&b.p, bytes) != cudaSuccess) {
+    if (dev_alloc(&b.p, bytes) != cudaSuccess) {
         cudaGetLastError();
         b.p = nullptr;
-        return fail(ctx, MCINV_E_NOMEM, "cudaMalloc failed");
+        return fail(ctx, MCINV_E_NOMEM, "device allocation failed");
     }
     b.bytes = bytes;
-    if (!h.empty()) CK(cudaMemcpy(b.p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice));
+    // on the legacy stream, in order with the allocation; callers synchronize that
+    // stream before the data is used on another stream (uploads_done)
+    if (!h.empty()) CK(cudaMemcpyAsync(b.p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, 0));
     return MCINV_OK;
 }
 
@@ -709,9 +717,11 @@ mcinv_status run_typed(mcinv_ctx *ctx, const mcinv_run_args *a, const Layout &L,
         threads3 = (int)((want + 31) / 32 * 32);
     }
     LevelDev::Slots *sl = v4 ? get_slots<S>(ctx, lv, 32 >> (L.lgC - lgK), threads3 / 32) : nullptr;
+    if (!ctx->host_only) CK(cudaStreamSynchronize(0));  // plan uploads (legacy stream) complete
     if (v4 && !sl) return fail(ctx, MCINV_E_NOMEM, "v4 slot arrays");
     if (v4 && !ctx->err_flag.p) {
-        if (cudaMalloc(&ctx->err_flag.p, 16) != cudaSuccess) return fail(ctx, MCINV_E_NOMEM, "v4 flag");
+        if (dev_alloc(&ctx->err_flag.p, 16) != cudaSuccess) return fail(ctx, MCINV_E_NOMEM, "v4 flag");
+        CK(cudaStreamSynchronize(0));
         ctx->err_flag.bytes = 16;
     }
     if (v4) CK(cudaMemsetAsync(ctx->err_flag.p, 0, 16, st));
@@ -865,10 +875,18 @@ mcinv_status mcinv_create(mcinv_ctx **out, int device, mcinv_dtype dtype, int64_
     if (n < 1 || n >= (int64_t(1) << 31)) return fail(ctx, MCINV_E_INVALID, "n out of range");
     CK(cudaSetDevice(device));
     CK(cudaDeviceGetAttribute(&ctx->nsm, cudaDevAttrMultiProcessorCount, device));
+    {
+        cudaMemPool_t pool;
+        uint64_t keep = UINT64_MAX;  // freed blocks stay in the pool: no release to the OS
+        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess)
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        cudaGetLastError();
+    }
     std::vector<std::vector<Entry>> rows;
     TRY(read_csr(ctx, n, row_ptr, col_idx, (const double *)values, dtype == MCINV_C128, rows));
     TRY(dtype == MCINV_C128 ? build_matrix<cd>(ctx, rows) : build_matrix<double>(ctx, rows));
     TRY(default_pattern(ctx));
+    CK(cudaStreamSynchronize(0));  // uploads complete before any stream uses them
     ctx->valid = true;
     ctx->err.clear();
     return MCINV_OK;
@@ -879,7 +897,9 @@ mcinv_status mcinv_set_trace_q(mcinv_ctx *ctx, const int64_t *row_ptr, const int
     CK(cudaSetDevice(ctx->device));
     std::vector<std::vector<Entry>> rows;
     TRY(read_csr(ctx, ctx->n, row_ptr, col_idx, (const double *)values, ctx->dtype == MCINV_C128, rows));
-    return ctx->dtype == MCINV_C128 ? build_q<cd>(ctx, rows) : build_q<double>(ctx, rows);
+    TRY(ctx->dtype == MCINV_C128 ? build_q<cd>(ctx, rows) : build_q<double>(ctx, rows));
+    CK(cudaStreamSynchronize(0));
+    return MCINV_OK;
 }
 
 mcinv_status mcinv_set_pattern(mcinv_ctx *ctx, int64_t count, const int32_t *rows, const int32_t *cols) {
@@ -888,7 +908,9 @@ mcinv_status mcinv_set_pattern(mcinv_ctx *ctx, int64_t count, const int32_t *row
         return fail(ctx, MCINV_E_INVALID, "pattern");
     CK(cudaSetDevice(ctx->device));
     ctx->pattern_custom = true;
-    return build_pattern(ctx, count, rows, cols);
+    TRY(build_pattern(ctx, count, rows, cols));
+    CK(cudaStreamSynchronize(0));
+    return MCINV_OK;
 }
 
 mcinv_status mcinv_pattern_size(const mcinv_ctx *ctx, int64_t *count) {
@@ -922,7 +944,7 @@ mcinv_status mcinv_run(mcinv_ctx *ctx, const mcinv_run_args *args) {
     } else {
         if (ctx->own_ws.bytes < L.total) {
             ctx->own_ws.release();
-            if (cudaMalloc(&ctx->own_ws.p, L.total) != cudaSuccess) {
+            if (dev_alloc(&ctx->own_ws.p, L.total) != cudaSuccess || cudaStreamSynchronize(0) != cudaSuccess) {
                 cudaGetLastError();
                 ctx->own_ws.p = nullptr;
                 return fail(ctx, MCINV_E_NOMEM, "workspace allocation", (int64_t)L.total);
@@ -985,7 +1007,7 @@ mcinv_status mcinv_result(mcinv_ctx *ctx, unsigned output, int64_t total_chains,
         const size_t need = 2 * comps * sizeof(double);
         if (ctx->tmp.bytes < need) {
             ctx->tmp.release();
-            if (cudaMalloc(&ctx->tmp.p, need) != cudaSuccess) {
+            if (dev_alloc(&ctx->tmp.p, need) != cudaSuccess || cudaStreamSynchronize(0) != cudaSuccess) {
                 cudaGetLastError();
                 ctx->tmp.p = nullptr;
                 return fail(ctx, MCINV_E_NOMEM, "result staging");
@@ -1014,7 +1036,19 @@ mcinv_status mcinv_result(mcinv_ctx *ctx, unsigned output, int64_t total_chains,
 
 void mcinv_destroy(mcinv_ctx *ctx) {
     if (!ctx) return;
-    if (ctx->valid || ctx->own_ws.p) cudaSetDevice(ctx->device);
+    if (ctx->valid || ctx->own_ws.p) {
+        cudaSetDevice(ctx->device);
+        // the buffers are freed stream-ordered on the legacy stream: first let it wait for
+        // the last run's stream (a non-blocking caller stream is not ordered with it)
+        if (ctx->have_run && ctx->stream) {
+            cudaEvent_t ev;
+            if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) == cudaSuccess) {
+                cudaEventRecord(ev, ctx->stream);
+                cudaStreamWaitEvent(0, ev, 0);
+                cudaEventDestroy(ev);
+            }
+        }
+    }
     delete ctx;
 }
 
