@@ -494,3 +494,43 @@ def test_config3_full_size_dense_lu(mc, orc):
         zg, wg = inv.get_state(ch, 1)
         states_match(zg, wg, r["z"], r["w"])
     inv.close()
+
+
+@pytest.mark.parametrize("kernel", ["v1", "v3", "v4"])
+def test_irregular_structure(mc, orc, kernel, monkeypatch):
+    """An unsorted CSR with duplicate entries (summed), explicit zeros (kept),
+    rows with no off-diagonal entry and a few dense rows (long entry lists:
+    several gather chunks), a non-symmetric pattern, and a shard that starts
+    at chain 64: every kernel vs the oracle."""
+    monkeypatch.setenv("MCINV_KERNEL", kernel)
+    rng = np.random.default_rng(77)
+    n = 150
+    rows, cols, vals = [], [], []
+    for i in range(n):
+        rows.append(i), cols.append(i), vals.append(0.0)  # diagonal fixed below
+        if i % 7 == 3:
+            continue  # diagonal only
+        k = 40 if i % 25 == 0 else rng.integers(1, 6)
+        for j in rng.choice(n, size=k, replace=False):
+            if j != i:
+                rows.append(i), cols.append(int(j)), vals.append(float(rng.uniform(-1, 1)))
+        if i % 5 == 0:  # a duplicate and an explicit zero
+            rows.append(i), cols.append(cols[-1]), vals.append(0.25)
+            rows.append(i), cols.append((i + 1) % n), vals.append(0.0)
+    rows, cols, vals = np.array(rows), np.array(cols), np.array(vals)
+    perm = rng.permutation(rows.size)  # unsorted within rows
+    rows, cols, vals = rows[perm], cols[perm], vals[perm]
+    order = np.argsort(rows, kind="stable")
+    rows, cols, vals = rows[order], cols[order], vals[order]
+    offsum = np.zeros(n)
+    np.add.at(offsum, rows[rows != cols], np.abs(vals[rows != cols]))
+    vals[rows == cols] = 1.2 * offsum[rows[rows == cols]] + 1.0
+    rp = np.zeros(n + 1, np.int64)
+    np.add.at(rp, rows + 1, 1)
+    c = W.CSR(n, np.cumsum(rp), cols.astype(np.int32), vals)
+    # the default pattern is the canonical (duplicate-summed) structure of C, explicit zeros included
+    canon = c.to_scipy().tocoo()
+    key = np.unique(canon.row.astype(np.int64) * n + canon.col)
+    pat = ((key // n).astype(np.int32), (key % n).astype(np.int32))
+    compare_run(mc, orc, c, pattern=pat, seed=19, chains=96, burn_in=3, cycles=4, outputs=("diag", "pattern"),
+                group_size=16, chain_begin=64)
