@@ -26,6 +26,8 @@
 // products over P lanes in V-1 shuffles, then log2(P/V) butterflies), after
 // which each lane posts ONE fire-and-forget reduction (red.global.add) into
 // the group's slot; the slots of all groups (41 MB for config 2) stay in L2.
+#include <cstdlib>
+
 #include "mcinv_internal.cuh"
 #include "noise.cuh"
 #include "scalar.cuh"
@@ -549,18 +551,26 @@ cudaError_t launch4k(const Sweep3Params<S> &p, int threads, cudaStream_t st) {
     const int C = 1 << p.lgC;
     const int blocks = (p.chains + C - 1) / C;
     const size_t smem = ((size_t)p.n + 15) / 16 * 16;
+    // shared memory only holds the counters: give the rest of the unified L1 to the cache
+    // (plan data and the partner re-reads of the accumulation hit there)
+    int carve = (int)((smem + 8192) * 100 / (228 * 1024)) + 1;
+    if (const char *ev = std::getenv("MCINV_CARVE")) carve = std::atoi(ev);
+    if (carve > 100) carve = 100;
     cudaError_t e;
     if (threads <= 512) {
         auto k = sweep4_kernel<S, 2 * KS, 512, LGP, K>;
         e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
         if (e == cudaSuccess) k<<<blocks, threads, smem, st>>>(p);
     } else if (threads <= 768) {
         auto k = sweep4_kernel<S, KS, 768, LGP, K>;
         e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
         if (e == cudaSuccess) k<<<blocks, threads, smem, st>>>(p);
     } else {
         auto k = sweep4_kernel<S, KS, 1024, LGP, K>;
         e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
         if (e == cudaSuccess) k<<<blocks, threads, smem, st>>>(p);
     }
     if (e != cudaSuccess) return e;
