@@ -172,7 +172,7 @@ std::string build_levels(const LevelInput &in, LevelPlan &P) {
 }
 
 std::vector<int> schedule_slots(int64_t n, const std::vector<int4> &rec, const std::vector<int> &ent_col, int R,
-                                int L) {
+                                int L, int ecap) {
     // row i -> level-order index o; lower neighbours (the first nlow entries) and the
     // reverse edges (upper neighbours)
     std::vector<int> ord_of(n);
@@ -205,12 +205,13 @@ std::vector<int> schedule_slots(int64_t n, const std::vector<int4> &rec, const s
             ready.push({-std::get<1>(waiting.top()), -std::get<2>(waiting.top())});
             waiting.pop();
         }
-        int taken = 0;
+        int taken = 0, ents = 0;
         std::vector<int> now;
         while (taken < R) {
             int o;
             if (!ready.empty()) {
                 o = -ready.top().second;
+                if (ecap > 0 && taken > 0 && ents + (rec[o].z & 0xffff) > ecap) break;  // block size cap
                 ready.pop();
             } else if (!waiting.empty() && taken == 0) {
                 o = std::get<2>(waiting.top());  // nothing ready: earliest-ready row (it will wait)
@@ -219,6 +220,7 @@ std::vector<int> schedule_slots(int64_t n, const std::vector<int4> &rec, const s
                 break;
             }
             now.push_back(o);
+            ents += rec[o].z & 0xffff;
             ++taken;
         }
         for (int o : now) {

@@ -75,7 +75,9 @@ std::string build_levels(const LevelInput &in, LevelPlan &out);
 // earliest, and padded (-1) only when no row is left. Input: the level-order
 // records (i, entry begin, count | lower << 16) and entry columns of the plan.
 // Output: slot -> level-order index (or -1 for padding); size a multiple of R.
+// ecap > 0: a group takes no further row once its entries would exceed ecap (a
+// single row may exceed it alone): bounds the group blocks staged by v5.
 std::vector<int> schedule_slots(int64_t n, const std::vector<int4> &rec, const std::vector<int> &ent_col, int R,
-                                int L);
+                                int L, int ecap = 0);
 
 }  // namespace mcinv

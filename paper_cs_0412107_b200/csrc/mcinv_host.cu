@@ -61,9 +61,15 @@ struct LevelDev {
     std::vector<unsigned char> h_dsg;        // level-order {delta, sigma} (raw bytes of S)
     std::vector<int> h_ph_row;
     std::vector<int> h_ent_col;              // level-order entry columns (v4 slot ordering)
+    std::vector<unsigned char> h_ab;         // level-order {a, b} pairs (raw bytes of S), for v5 blocks
+    std::vector<int> h_pz;                   // level-order pattern slot pairs (empty without pattern)
     struct Slots {
         DevBuf rec, dsg;
         int nslots = 0;
+        // v5: one contiguous block per warp group (records, delta/sigma, columns, coefficients,
+        // pattern slots), staged into shared memory by a TMA bulk copy
+        DevBuf blob, gofs;
+        int maxb = 0;
     };
     std::map<int, std::unique_ptr<Slots>> slots;  // (rows per warp group R, warps W) -> slot arrays
 };
@@ -428,12 +434,13 @@ mcinv_status check_args(const mcinv_ctx *ctx_c, const mcinv_run_args *a) {
     return MCINV_OK;
 }
 
-int kernel_pref() {  // 0 auto (v4 when eligible, else v3), 1 force v1, 3 force v3, 4 force v4
+int kernel_pref() {  // 0 auto, 1 force v1, 3 force v3, 4 force v4, 5 force v5
     const char *e = std::getenv("MCINV_KERNEL");
     if (!e) return 0;
     if (!std::strcmp(e, "v1")) return 1;
     if (!std::strcmp(e, "v3")) return 3;
     if (!std::strcmp(e, "v4")) return 4;
+    if (!std::strcmp(e, "v5")) return 5;
     return 0;
 }
 
@@ -592,6 +599,9 @@ LevelDev *get_levels(mcinv_ctx *ctx, unsigned outputs) {
                          reinterpret_cast<const unsigned char *>(dsg.data() + dsg.size()));
         ld->h_ph_row = P.ph_row;
         ld->h_ent_col = P.ent_col;
+        ld->h_ab.assign(reinterpret_cast<const unsigned char *>(ab.data()),
+                        reinterpret_cast<const unsigned char *>(ab.data() + ab.size()));
+        ld->h_pz = P.ent_pz;
         if (!ctx->host_only) P = mcinv::LevelPlan();  // device copy only
     }
     LevelDev *raw = ld.get();
@@ -601,9 +611,12 @@ LevelDev *get_levels(mcinv_ctx *ctx, unsigned outputs) {
 
 // v4 slot arrays: level order with every level padded to a multiple of R rows
 // (a warp group of R rows never spans two levels, so its rows are independent)
+constexpr int kBlockEntries = 56;  // v5: entries per warp group (bounds the staged blocks)
+constexpr bool kV5Default = true;  // v5 by default where it applies (measured: config 2 +5%, config 3 +24%)
+
 template <typename S>
-LevelDev::Slots *get_slots(mcinv_ctx *ctx, LevelDev *lv, int R, int W) {
-    auto it = lv->slots.find(R * 4096 + W);
+LevelDev::Slots *get_slots(mcinv_ctx *ctx, LevelDev *lv, int R, int W, bool blocks) {
+    auto it = lv->slots.find(R * 4096 + W + (blocks ? (1 << 28) : 0));
     if (it != lv->slots.end()) return it->second.get();
     std::unique_ptr<LevelDev::Slots> sl(new LevelDev::Slots());
     std::vector<int4> rec;
@@ -619,14 +632,14 @@ LevelDev::Slots *get_slots(mcinv_ctx *ctx, LevelDev *lv, int R, int W) {
             while (order.size() % R) order.push_back(-1);
         }
     } else if (const char *e = std::getenv("MCINV_SLACK")) {
-        order = mcinv::schedule_slots(ctx->n, lv->h_rec, lv->h_ent_col, R, std::atoi(e));
+        order = mcinv::schedule_slots(ctx->n, lv->h_rec, lv->h_ent_col, R, std::atoi(e), blocks ? kBlockEntries : 0);
     } else {
         // the largest slack (W, W/2, ..., 1 groups) whose schedule pads at most 3% of the
         // slots: wide DAGs (config 2) take the full slack, narrow ones (lattices) less;
         // if none does (a DAG narrower than a warp group), the least padded one
         std::vector<int> best;
         for (int L = W; L >= 1; L /= 2) {
-            order = mcinv::schedule_slots(ctx->n, lv->h_rec, lv->h_ent_col, R, L);
+            order = mcinv::schedule_slots(ctx->n, lv->h_rec, lv->h_ent_col, R, L, blocks ? kBlockEntries : 0);
             if ((int64_t)order.size() <= ctx->n + ctx->n * 3 / 100) break;
             if (best.empty() || order.size() < best.size()) best = order;
             if (L == 1) order = best;
@@ -645,8 +658,55 @@ LevelDev::Slots *get_slots(mcinv_ctx *ctx, LevelDev *lv, int R, int W) {
     }
     sl->nslots = (int)rec.size();
     if (upload(ctx, sl->rec, rec) != MCINV_OK || upload(ctx, sl->dsg, dsg) != MCINV_OK) return nullptr;
+    if (blocks) {
+        // group block: int4 head {EP, bytes, off_ab, off_pz}; int4 rec[R] {i, entry offset in
+        // the block, count | lower << 16, pattern slot of (i,i)}; S dsg[R][2]; int col[EP];
+        // ZW<S> ab[EP]; int2 pz[EP] (pattern runs). EP = entries + 8 (zero-coefficient
+        // padding for the unrolled reads), a multiple of 4; every section 16-B aligned.
+        const bool pat = !lv->h_pz.empty();
+        const ZW<S> *hab = reinterpret_cast<const ZW<S> *>(lv->h_ab.data());
+        const size_t ng = rec.size() / R;
+        std::vector<int64_t> gofs(ng + 1, 0);
+        std::vector<unsigned char> blob;
+        for (size_t g = 0; g < ng; ++g) {
+            int E = 0;
+            for (int r = 0; r < R; ++r)
+                if (rec[g * R + r].x >= 0) E += rec[g * R + r].z & 0xffff;
+            const int EP = (E + 8 + 3) / 4 * 4;
+            const size_t off_col = 16 + 16 * (size_t)R + 2 * sizeof(S) * R;
+            const size_t off_ab = off_col + 4 * (size_t)EP;
+            const size_t off_pz = off_ab + sizeof(ZW<S>) * EP;
+            const size_t bytes = (off_pz + (pat ? 8 * (size_t)EP : 0) + 15) / 16 * 16;
+            const size_t base = blob.size();
+            blob.resize(base + bytes, 0);
+            unsigned char *b = blob.data() + base;
+            reinterpret_cast<int4 *>(b)[0] = make_int4(EP, (int)bytes, (int)off_ab, (int)off_pz);
+            int e = 0;
+            for (int r = 0; r < R; ++r) {
+                const int4 q = rec[g * R + r];
+                const int cnt = q.x >= 0 ? q.z & 0xffff : 0;
+                reinterpret_cast<int4 *>(b + 16)[r] = make_int4(q.x, e, q.x >= 0 ? q.z : 0, q.w);
+                reinterpret_cast<S *>(b + 16 + 16 * R)[2 * r] = dsg[2 * (g * R + r)];
+                reinterpret_cast<S *>(b + 16 + 16 * R)[2 * r + 1] = dsg[2 * (g * R + r) + 1];
+                for (int t = 0; t < cnt; ++t) {
+                    reinterpret_cast<int *>(b + off_col)[e + t] = lv->h_ent_col[q.y + t];
+                    reinterpret_cast<ZW<S> *>(b + off_ab)[e + t] = hab[q.y + t];
+                    if (pat) {
+                        reinterpret_cast<int2 *>(b + off_pz)[e + t] =
+                            make_int2(lv->h_pz[2 * (q.y + t)], lv->h_pz[2 * (q.y + t) + 1]);
+                    }
+                }
+                e += cnt;
+            }
+            for (int t = e; t < EP; ++t)
+                if (pat) reinterpret_cast<int2 *>(b + off_pz)[t] = make_int2(-1, -1);
+            sl->maxb = std::max(sl->maxb, (int)bytes);
+            gofs[g + 1] = (int64_t)blob.size();
+        }
+        if (upload(ctx, sl->blob, blob) != MCINV_OK || upload(ctx, sl->gofs, gofs) != MCINV_OK) return nullptr;
+    }
     LevelDev::Slots *raw = sl.get();
-    lv->slots[R * 4096 + W] = std::move(sl);
+    lv->slots[R * 4096 + W + (blocks ? (1 << 28) : 0)] = std::move(sl);
     return raw;
 }
 
@@ -695,10 +755,10 @@ mcinv_status run_typed(mcinv_ctx *ctx, const mcinv_run_args *a, const Layout &L,
     // shared memory and the plan has no deferred items (trace, non-neighbour pairs)
     const int pref = kernel_pref();
     const bool v4_ok = lv && L.lgC <= 5 && n <= 200000 && !lv->deferred;
-    if (pref == 4 && !v4_ok) return fail(ctx, MCINV_E_INVALID, "v4 kernel not applicable to this run");
+    if ((pref == 4 || pref == 5) && !v4_ok) return fail(ctx, MCINV_E_INVALID, "v4/v5 kernel not applicable to this run");
     // auto: v4 whenever it applies (measured faster than v3 on configs 1-3: no per-level
     // barrier; profiles/), else v3
-    const bool v4 = v4_ok && (pref == 4 || pref == 0);
+    const bool v4 = v4_ok && (pref == 4 || pref == 5 || pref == 0);
     // chains per thread K (register blocking; real C, both chains in one SE group, no
     // trace / deferred items): default 2 for v3 (config 4 +19%), 1 for v4 (config 2 measured
     // faster with more threads than with blocking, profiles/); MCINV_K=1|2 overrides
@@ -716,7 +776,14 @@ mcinv_status run_typed(mcinv_ctx *ctx, const mcinv_run_args *a, const Layout &L,
         want = std::min<int64_t>(1024, std::max<int64_t>(want, int64_t(1) << (L.lgC - lgK)));
         threads3 = (int)((want + 31) / 32 * 32);
     }
-    LevelDev::Slots *sl = v4 ? get_slots<S>(ctx, lv, 32 >> (L.lgC - lgK), threads3 / 32) : nullptr;
+    // v5 (TMA-staged plan blocks) when forced or auto (kV5Default) and its shared memory fits
+    bool v5 = v4 && (pref == 5 || (pref == 0 && kV5Default));
+    LevelDev::Slots *sl = v4 ? get_slots<S>(ctx, lv, 32 >> (L.lgC - lgK), threads3 / 32, v5) : nullptr;
+    if (v5 && sl && mcinv::sweep5_smem((int)n, threads3, sl->maxb) > 227 * 1024) {
+        if (pref == 5) return fail(ctx, MCINV_E_INVALID, "v5 blocks do not fit shared memory");
+        v5 = false;
+        sl = get_slots<S>(ctx, lv, 32 >> (L.lgC - lgK), threads3 / 32, false);
+    }
     if (!ctx->host_only) CK(cudaStreamSynchronize(0));  // plan uploads (legacy stream) complete
     if (v4 && !sl) return fail(ctx, MCINV_E_NOMEM, "v4 slot arrays");
     if (v4 && !ctx->err_flag.p) {
@@ -725,7 +792,7 @@ mcinv_status run_typed(mcinv_ctx *ctx, const mcinv_run_args *a, const Layout &L,
         ctx->err_flag.bytes = 16;
     }
     if (v4) CK(cudaMemsetAsync(ctx->err_flag.p, 0, 16, st));
-    ctx->last_kernel = v4 ? 4 : L.ver;
+    ctx->last_kernel = v5 ? 5 : v4 ? 4 : L.ver;
     ctx->last_C = lv ? (1 << L.lgC) : 32;
     ctx->last_steps = lv ? lv->D : n;
     Sweep3Params<S> q3{};
@@ -769,6 +836,9 @@ mcinv_status run_typed(mcinv_ctx *ctx, const mcinv_run_args *a, const Layout &L,
             q3.slot_dsg = (const S *)sl->dsg.p;
             q3.nslots = sl->nslots;
             q3.err = (unsigned *)ctx->err_flag.p;
+            q3.blob = (const unsigned char *)sl->blob.p;
+            q3.gofs = (const int64_t *)sl->gofs.p;
+            q3.maxb = sl->maxb;
         }
     }
     cudaError_t lerr = cudaSuccess;
@@ -782,7 +852,8 @@ mcinv_status run_typed(mcinv_ctx *ctx, const mcinv_run_args *a, const Layout &L,
             q.snap_x = (S *)(ws + L.snap_x);
             q.snap_y = (S *)(ws + L.snap_y);
             timed(ctx, 0, st, [&] {
-                cudaError_t e = v4 ? launch_sweep4<S>(q, threads3, st) : launch_sweep3<S>(q, threads3, st);
+                cudaError_t e = v5 ? launch_sweep5<S>(q, threads3, st)
+                                : v4 ? launch_sweep4<S>(q, threads3, st) : launch_sweep3<S>(q, threads3, st);
                 if (e != cudaSuccess) lerr = e;
             });
         } else {
@@ -1025,7 +1096,7 @@ mcinv_status mcinv_result(mcinv_ctx *ctx, unsigned output, int64_t total_chains,
     double bad = 0.0;
     CK(cudaMemcpyAsync(&bad, mom + L.mom_count - 1, sizeof(double), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    if (ctx->last_kernel == 4) {
+    if (ctx->last_kernel >= 4) {
         unsigned wd = 0;
         CK(cudaMemcpy(&wd, ctx->err_flag.p, sizeof(wd), cudaMemcpyDeviceToHost));
         if (wd) return fail(ctx, MCINV_E_CUDA, "v4 dataflow watchdog: a dependency wait exceeded its bound");

@@ -121,6 +121,10 @@ struct Sweep3Params {
     const S *slot_dsg;
     int nslots;
     unsigned *err;        // set (watchdog) if a dependency wait exceeds its bound
+    // v5 (v4 + TMA-staged plan): per warp group one contiguous block (see get_slots)
+    const unsigned char *blob;
+    const int64_t *gofs;  // [groups + 1] byte offsets of the blocks in blob
+    int maxb;             // largest block (bytes)
 };
 
 template <typename S>
@@ -128,6 +132,10 @@ cudaError_t launch_sweep3(const Sweep3Params<S> &p, int threads, cudaStream_t st
 // v4: per-row completion counters in shared memory instead of per-level barriers
 template <typename S>
 cudaError_t launch_sweep4(const Sweep3Params<S> &p, int threads, cudaStream_t st);
+// v5: v4 with each warp group's plan data staged into shared memory by TMA bulk copies
+template <typename S>
+cudaError_t launch_sweep5(const Sweep3Params<S> &p, int threads, cudaStream_t st);
+size_t sweep5_smem(int n, int threads, int maxb);
 
 // A_g[i][j] += sum_{t < T, c in group g} X[t][i][c] conj(Y[t][j][c]).
 template <typename S>

@@ -611,6 +611,286 @@ cudaError_t launch_sweep3(const Sweep3Params<S> &p, int threads, cudaStream_t st
     }
 }
 
+// ---------------------------------------------------------------- v5: v4 + TMA-staged plan
+//
+// The dataflow kernel of v4 with the plan data of every warp group (row
+// records, delta/sigma, entry columns, coefficient pairs, pattern slots)
+// packed by the host into one contiguous block and staged into a per-warp,
+// double-buffered shared-memory slot by a TMA bulk copy (cp.async.bulk +
+// mbarrier complete_tx) one group ahead: the dependency checks, the gathers'
+// addresses and coefficients and the accumulation's partners and slots then
+// read shared memory, and the unified L1 is left to the state lines.
+namespace {
+
+__device__ __forceinline__ uint32_t smem_addr(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    uint32_t ok = 0;
+    while (!ok) {
+        asm volatile(
+            "{\n\t.reg .pred q;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 q, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, q;\n}"
+            : "=r"(ok)
+            : "r"(bar), "r"(parity)
+            : "memory");
+    }
+}
+__device__ __forceinline__ void tma_block(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // our generic reads of this slot precede
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
+}
+
+// Eq. (4)/(5) fma chains from a staged block (see row_sums)
+template <typename S, int KU>
+__device__ __forceinline__ void row_sums_blk(const Sweep3Params<S> &p, const ZW<S> *zcol, const int *col,
+                                             const ZW<S> *ab, int cnt, S &az, S &aw) {
+    for (int e0 = 0; e0 < cnt; e0 += KU) {
+        int j[KU];
+        ZW<S> v[KU], c[KU];
+#pragma unroll
+        for (int q = 0; q < KU; ++q) j[q] = col[e0 + q];
+#pragma unroll
+        for (int q = 0; q < KU; ++q) {
+            v[q] = ld_zw(zcol + (int64_t)(e0 + q < cnt ? j[q] : 0) * p.ld);
+            c[q] = ab[e0 + q];
+        }
+#pragma unroll
+        for (int q = 0; q < KU; ++q)
+            if (e0 + q < cnt) {
+                az = fma_s(c[q].z, v[q].z, az);
+                aw = fma_s(c[q].w, v[q].w, aw);
+            }
+    }
+}
+
+// accumulation as accumulate_row (K = 1), partners' columns and slots from the block
+template <typename S, int P, int V>
+__device__ __forceinline__ void accumulate_blk(const Sweep3Params<S> &p, const ZW<S> *zcol, int4 rec, const int *col,
+                                               const int2 *pz, S zi, S wi, bool acc, int lane, bool gleader,
+                                               bool towner, double *sd, double *sp, bool want_diag, bool want_pat) {
+    constexpr int E = ScalarTraits<S>::kDoubles;
+    const int i = rec.x;
+    if (want_diag || want_pat) {
+        const S d = group_sum<P>(acc ? zwc_s(zi, wi) : zero_s<S>());
+        if (acc && gleader) {
+            if (want_diag) slot_red(sd + (int64_t)i * E, d);
+            if (want_pat && rec.w >= 0) slot_red(sp + (int64_t)rec.w * E, d);
+        }
+    }
+    if (!want_pat) return;
+    const int nlow = acc ? rec.z >> 16 : 0;
+    if constexpr (P == 1) {
+        for (int e = 0; e < nlow; ++e) {
+            const ZW<S> u = ld_zw(zcol + (int64_t)col[e] * p.ld);
+            const int2 z2 = pz[e];
+            if (z2.x >= 0) slot_red(sp + (int64_t)z2.x * E, zwc_s(zi, u.w));
+            if (z2.y >= 0) slot_red(sp + (int64_t)z2.y * E, zwc_s(u.z, wi));
+        }
+    } else {
+        constexpr int VE = V / 2;
+        const int nb = (__reduce_max_sync(0xffffffffu, nlow) + VE - 1) / VE;
+        for (int b = 0; b < nb; ++b) {
+            S v[V];
+#pragma unroll
+            for (int q = 0; q < VE; ++q) {
+                const int e = b * VE + q;
+                const bool ok = e < nlow;
+                const ZW<S> u = ld_zw(zcol + (int64_t)(ok ? col[e] : 0) * p.ld);
+                v[2 * q] = ok ? zwc_s(zi, u.w) : zero_s<S>();
+                v[2 * q + 1] = ok ? zwc_s(u.z, wi) : zero_s<S>();
+            }
+            int held;
+            const S x = transpose_sum<P, V>(v, lane, held);
+            const int e = b * VE + (held >> 1);
+            if (towner && e < nlow) {
+                const int2 z2 = pz[e];
+                const int slot = (held & 1) ? z2.y : z2.x;
+                if (slot >= 0) slot_red(sp + (int64_t)slot * E, x);
+            }
+        }
+    }
+}
+
+}  // namespace
+
+template <typename S, int KU, int NT, int LGP>
+__global__ void __launch_bounds__(NT, 1) sweep5_kernel(const Sweep3Params<S> p) {
+    constexpr int E = ScalarTraits<S>::kDoubles;
+    constexpr int P = 1 << LGP;
+    constexpr int V = P < 8 ? P : 8;
+    extern __shared__ __align__(128) unsigned char sm5[];
+    const int tid = threadIdx.x;
+    const int B = blockDim.x;
+    const int W = B >> 5;
+    const int w = tid >> 5;
+    const int lane = tid & 31;
+    const int lgC = p.lgC;  // C <= 32: a row's lanes are in one warp
+    const int C = 1 << lgC;
+    const int c = lane & (C - 1);
+    const int chain = (blockIdx.x << lgC) + c;
+    const bool active = chain < p.chains;
+    const uint32_t gchain = p.chain0 + static_cast<uint32_t>(chain);
+    const bool gleader = (c & (P - 1)) == 0;
+    const bool towner = (lane & ((P > V ? P / V : 1) - 1)) == 0;
+    const int64_t grp = chain >> p.lgG;
+    ZW<S> *__restrict__ zcol = p.zw + chain;
+    const bool want_diag = p.outputs & OUT_DIAG, want_pat = p.outputs & OUT_PATTERN;
+    const bool want_full = p.outputs & OUT_FULL;
+    double *const sd = p.slot_diag + grp * p.n * E;
+    double *const sp = p.slot_pat + grp * p.pcount * E;
+    // shared memory: [W][2] mbarriers | [W][2][maxb] block slots | done[n]
+    uint64_t *bars = reinterpret_cast<uint64_t *>(sm5);
+    unsigned char *blk = sm5 + 16 * W;
+    unsigned char *done = blk + (size_t)2 * W * p.maxb;
+    const uint32_t bar0 = smem_addr(bars + 2 * w), bar1 = bar0 + 8;
+    unsigned char *buf0 = blk + (size_t)2 * w * p.maxb, *buf1 = buf0 + p.maxb;
+
+    for (int j = tid; j < p.n; j += B) done[j] = static_cast<unsigned char>(p.s_begin);
+    if (lane == 0) {
+        mbar_init(bar0, 1);
+        mbar_init(bar1, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    const int R = 32 >> lgC;
+    const int ngroups = p.nslots / R;
+    const int sub = lane >> lgC;
+    auto issue = [&](int g, unsigned char *dst, uint32_t bar) {
+        const int64_t off = __ldg(p.gofs + g);
+        const uint32_t bytes = static_cast<uint32_t>(__ldg(p.gofs + g + 1) - off);
+        tma_block(smem_addr(dst), p.blob + off, bytes, bar);
+    };
+    if (lane == 0 && w < ngroups) issue(w, buf0, bar0);
+    uint32_t ph0 = 0, ph1 = 0;
+    int item = 0;
+    for (int s = p.s_begin; s < p.s_end; ++s) {
+        const uint32_t k = p.sweep_abs0 + static_cast<uint32_t>(s);
+        const bool sampling = s >= p.burn_in;
+        const unsigned char need = static_cast<unsigned char>(s + 1);
+        for (int g = w; g < ngroups; g += W, ++item) {
+            const bool odd = item & 1;
+            unsigned char *cur = odd ? buf1 : buf0;
+            // stage the next group (this warp's next item, possibly in the next sweep) into the
+            // other slot: the previous item's reads of it are complete (__syncwarp)
+            __syncwarp();
+            const int gn = g + W < ngroups ? g + W : w;
+            const bool has_next = g + W < ngroups || s + 1 < p.s_end;
+            if (lane == 0 && has_next) issue(gn, odd ? buf0 : buf1, odd ? bar0 : bar1);
+            if (odd) {
+                mbar_wait(bar1, ph1);
+                ph1 ^= 1;
+            } else {
+                mbar_wait(bar0, ph0);
+                ph0 ^= 1;
+            }
+            const int4 head = reinterpret_cast<const int4 *>(cur)[0];
+            const int4 rec = reinterpret_cast<const int4 *>(cur)[1 + sub];
+            const int *col = reinterpret_cast<const int *>(cur + 16 + 16 * R + 2 * sizeof(S) * R) + rec.y;
+            const ZW<S> *ab = reinterpret_cast<const ZW<S> *>(cur + head.z) + rec.y;
+            const int2 *pz = reinterpret_cast<const int2 *>(cur + head.w) + rec.y;
+            const S *dsg = reinterpret_cast<const S *>(cur + 16 + 16 * R) + 2 * sub;
+            const bool valid = rec.x >= 0;
+            const int i = rec.x, cnt = valid ? rec.z & 0xffff : 0;
+            S zi = zero_s<S>(), wi = zero_s<S>();
+            if (valid) {
+                const double phi = noise_phi(p.noise, static_cast<uint32_t>(i), k, gchain, p.key0, p.key1);
+                const int nlow = rec.z >> 16;
+                for (int e = 0; e < nlow; ++e) {
+                    const volatile unsigned char *f = done + col[e];
+                    if (*f != need) {
+                        unsigned spins = 0;
+                        while (*f != need && !*reinterpret_cast<volatile unsigned *>(p.err)) {
+                            __nanosleep(32);
+                            if (++spins > (1u << 26)) {  // ~seconds: report, do not hang
+                                atomicOr(p.err, 1u);
+                                break;
+                            }
+                        }
+                    }
+                }
+                __threadfence_block();
+                S az = zero_s<S>(), aw = zero_s<S>();
+                row_sums_blk<S, KU>(p, zcol, col, ab, cnt, az, aw);
+                const S dl = dsg[0], sg = dsg[1];
+                zi = fma_s(neg_s(dl), az, scale_s(sg, phi));
+                wi = fma_s(neg_s(conj_s(dl)), aw, scale_s(conj_s(sg), phi));
+                zcol[(int64_t)i * p.ld] = ZW<S>{zi, wi};
+                if (want_full && sampling) {
+                    const int64_t ts = s - p.snap_s0;
+                    p.snap_x[(ts * p.n + i) * p.ld + chain] = zi;
+                    p.snap_y[(ts * p.n + i) * p.ld + chain] = wi;
+                }
+            }
+            __syncwarp();  // the row's stores are ordered before its counter update
+            if (valid && c == 0) {
+                __threadfence_block();  // release
+                *reinterpret_cast<volatile unsigned char *>(done + i) = need;
+            }
+            if (sampling)
+                accumulate_blk<S, P, V>(p, zcol, rec, col, pz, zi, wi, valid && active, lane, gleader, towner, sd,
+                                        sp, want_diag, want_pat);
+        }
+        __syncthreads();  // sweep boundary: all reads of sweep s values are done
+    }
+}
+
+size_t sweep5_smem(int n, int threads, int maxb) {
+    const size_t W = (size_t)threads / 32;
+    return 16 * W + 2 * W * (size_t)maxb + ((size_t)n + 15) / 16 * 16;
+}
+
+namespace {
+
+template <typename S, int LGP>
+cudaError_t launch5(const Sweep3Params<S> &p, int threads, cudaStream_t st) {
+    constexpr int KS = ScalarTraits<S>::kDoubles == 1 ? 4 : 2;
+    const int C = 1 << p.lgC;
+    const int blocks = (p.chains + C - 1) / C;
+    const size_t smem = sweep5_smem(p.n, threads, p.maxb);
+    cudaError_t e;
+    if (threads <= 512) {
+        auto k = sweep5_kernel<S, 2 * KS, 512, LGP>;
+        e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e == cudaSuccess) k<<<blocks, threads, smem, st>>>(p);
+    } else if (threads <= 768) {
+        auto k = sweep5_kernel<S, KS, 768, LGP>;
+        e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e == cudaSuccess) k<<<blocks, threads, smem, st>>>(p);
+    } else {
+        auto k = sweep5_kernel<S, KS, 1024, LGP>;
+        e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e == cudaSuccess) k<<<blocks, threads, smem, st>>>(p);
+    }
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+template <typename S>
+cudaError_t launch_sweep5(const Sweep3Params<S> &p, int threads, cudaStream_t st) {
+    switch (p.lgP) {
+        case 0: return launch5<S, 0>(p, threads, st);
+        case 1: return launch5<S, 1>(p, threads, st);
+        case 2: return launch5<S, 2>(p, threads, st);
+        case 3: return launch5<S, 3>(p, threads, st);
+        case 4: return launch5<S, 4>(p, threads, st);
+        case 5: return launch5<S, 5>(p, threads, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+template cudaError_t launch_sweep5<double>(const Sweep3Params<double> &, int, cudaStream_t);
+template cudaError_t launch_sweep5<cd>(const Sweep3Params<cd> &, int, cudaStream_t);
 template cudaError_t launch_sweep3<double>(const Sweep3Params<double> &, int, cudaStream_t);
 template cudaError_t launch_sweep4<double>(const Sweep3Params<double> &, int, cudaStream_t);
 template cudaError_t launch_sweep4<cd>(const Sweep3Params<cd> &, int, cudaStream_t);

@@ -253,12 +253,14 @@ def test_both_kernels(mc, orc, kernel, monkeypatch):
                     outputs=("diag", "trace", "full"), group_size=4, snapshot_sweeps=2)
 
 
-def test_v4_dataflow(mc, orc, monkeypatch):
-    """The dataflow kernel (v4: per-row completion counters, no level barriers)
-    matches the oracle for every chains-per-CTA layout up to a warp, real and
-    complex, with diag / pattern / full outputs, several launches (full-output
-    chunks) and forced block sizes; it is the default for the bench config."""
-    monkeypatch.setenv("MCINV_KERNEL", "v4")
+@pytest.mark.parametrize("kernel", ["v4", "v5"])
+def test_v4_dataflow(mc, orc, monkeypatch, kernel):
+    """The dataflow kernel (v4: per-row completion counters, no level barriers;
+    v5: the same with TMA-staged plan blocks) matches the oracle for every
+    chains-per-CTA layout up to a warp, real and complex, with diag / pattern /
+    full outputs, several launches (full-output chunks) and forced block
+    sizes; the automatic kernel choice is checked at the end."""
+    monkeypatch.setenv("MCINV_KERNEL", kernel)
     for C in (1, 4, 8, 32):
         monkeypatch.setenv("MCINV_C", str(C))
         for th in ("64", "768"):
@@ -272,12 +274,12 @@ def test_v4_dataflow(mc, orc, monkeypatch):
     monkeypatch.delenv("MCINV_C")
     monkeypatch.delenv("MCINV_THREADS")
     # automatic choice: v4 where it applies (configs 2, 3), v3 for C > 32 or trace (configs 4, 5)
-    for k, ver in ((3, 4), (2, 4), (5, 3)):
+    for k, ver in ((3, (4, 5)), (2, (4, 5)), (5, (3,))):
         c, q, run = W.config(k)
         inv = mc.Inverter(c, q=q)
         inv.run(run.seed, run.chains, 0, 1, tuple(o for o in run.outputs if o != "full") or ("diag",),
                 group_size=run.group_size)
-        assert inv.kernel_info()["version"] == ver, k
+        assert inv.kernel_info()["version"] in ver, k
         inv.close()
 
 
@@ -297,7 +299,7 @@ def test_chains_per_thread(mc, orc, monkeypatch, K, kernel):
                     outputs=("diag", "full"), group_size=gs, snapshot_sweeps=2)
 
 
-@pytest.mark.parametrize("kernel", ["v1", "v3", "v4"])
+@pytest.mark.parametrize("kernel", ["v1", "v3", "v4", "v5"])
 def test_z2_noise_parity(mc, orc, kernel, monkeypatch):
     """NEXT-1 Z2 noise (reading R21) on every sweep kernel:
     states and estimates vs the oracle on the same seed."""
@@ -305,7 +307,7 @@ def test_z2_noise_parity(mc, orc, kernel, monkeypatch):
     compare_run(mc, orc, W.pedigree(400, seed=51), seed=11, chains=64, burn_in=2, cycles=4,
                 outputs=("diag", "pattern"), group_size=8, noise="z2")
     c = W.lattice(4, 3, 0.15, seed=52)
-    outs = ("diag", "trace") if kernel != "v4" else ("diag", "full")
+    outs = ("diag", "trace") if kernel not in ("v4", "v5") else ("diag", "full")
     compare_run(mc, orc, c, q=W.random_q(c.n, 53, 3) if "trace" in outs else None, seed=12, chains=40, burn_in=2,
                 cycles=3, outputs=outs, group_size=4, noise="z2", snapshot_sweeps=2)
 
@@ -334,7 +336,7 @@ def test_bench_configs_use_level_kernels(mc):
         inv = mc.Inverter(c, q=q)
         inv.run(run.seed, run.chains, 0, 1, tuple(o for o in run.outputs if o != "full") or ("diag",),
                 group_size=run.group_size)
-        assert inv.kernel_info()["version"] in (3, 4), k
+        assert inv.kernel_info()["version"] in (3, 4, 5), k
         inv.close()
 
 
@@ -496,7 +498,7 @@ def test_config3_full_size_dense_lu(mc, orc):
     inv.close()
 
 
-@pytest.mark.parametrize("kernel", ["v1", "v3", "v4"])
+@pytest.mark.parametrize("kernel", ["v1", "v3", "v4", "v5"])
 def test_irregular_structure(mc, orc, kernel, monkeypatch):
     """An unsorted CSR with duplicate entries (summed), explicit zeros (kept),
     rows with no off-diagonal entry and a few dense rows (long entry lists:
