@@ -288,6 +288,7 @@ def ours_arm(args):
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": tr, "traffic_bytes_per_site": tps,
                 "kernel": {3: "sweep3_kernel (v3, level barriers)", 4: "sweep4_kernel (v4, dataflow)",
+                           5: "sweep5_kernel (v5, dataflow + TMA-staged plan blocks)",
                            1: "sweep_kernel (v1)"}.get(kinfo["version"], str(kinfo)),
                 "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": bytes_launch,

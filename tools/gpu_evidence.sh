@@ -17,6 +17,6 @@ if [ -z "$NO_NCU" ]; then
   echo "launches rc=$?" >> gpurun_out/ncu_launches.log
   RCMD="python tools/run_one.py --config ${NCFG:-2} --sweeps 12 --burn 2"
   timeout 300 $RCMD > gpurun_out/run_plain.log 2>&1 &&
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"sweep[34]" -c 1 -o gpurun_out/prof_sweep3 -f $RCMD > gpurun_out/ncu_full.log 2>&1
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"sweep[345]" -c 1 -o gpurun_out/prof_sweep3 -f $RCMD > gpurun_out/ncu_full.log 2>&1
   echo "full rc=$?" >> gpurun_out/ncu_full.log
 fi
