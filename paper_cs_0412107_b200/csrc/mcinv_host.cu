@@ -437,10 +437,11 @@ mcinv_status check_args(const mcinv_ctx *ctx_c, const mcinv_run_args *a) {
 int kernel_pref() {  // 0 auto, 1 force v1, 3 force v3, 4 force v4, 5 force v5
     const char *e = std::getenv("MCINV_KERNEL");
     if (!e) return 0;
-    if (!std::strcmp(e, "v1")) return 1;
-    if (!std::strcmp(e, "v3")) return 3;
-    if (!std::strcmp(e, "v4")) return 4;
-    if (!std::strcmp(e, "v5")) return 5;
+    const char *d = e[0] == 'v' ? e + 1 : e;  // "v3" or "3"
+    if (!std::strcmp(d, "1")) return 1;
+    if (!std::strcmp(d, "3")) return 3;
+    if (!std::strcmp(d, "4")) return 4;
+    if (!std::strcmp(d, "5")) return 5;
     return 0;
 }
 
@@ -473,6 +474,8 @@ Layout make_layout(const mcinv_ctx *ctx, const mcinv_run_args *a) {
     L.ksub = 1;
     if (L.ver == 3) {
         L.lgC = choose_lgC(ctx, a->chains);
+        // (not capped at 32 for the dataflow kernels: config 4 measured 2.98e10 with v5 at
+        // C = 32 vs 3.7e10 with v3 at C = 64 -- HBM-bound, the matrix row is read once per C)
         const int64_t q = std::max<int64_t>(32, int64_t(1) << L.lgC);  // padded chains stay in bounds
         L.ld = (int)((a->chains + q - 1) / q * q);
         // accumulator slots are the SE groups (the kernel sums the chains of a
@@ -751,38 +754,50 @@ mcinv_status run_typed(mcinv_ctx *ctx, const mcinv_run_args *a, const Layout &L,
     LevelDev *lv = L.ver == 3 ? get_levels<S>(ctx, a->outputs) : nullptr;
     if (lv && !lv->error.empty()) return fail(ctx, MCINV_E_INVALID, "level schedule: " + lv->error);
     if (lv && L.lgP > L.lgC) return fail(ctx, MCINV_E_INVALID, "layout: group lanes exceed chains per CTA");
-    // v4 (dataflow) when the chains of a row fit one warp, the per-row counters fit
-    // shared memory and the plan has no deferred items (trace, non-neighbour pairs)
+    // dataflow kernels (v5 TMA-staged plan blocks, v4 plan through L1) when the chains of a
+    // row fit one warp and the plan has no deferred items (trace, non-neighbour pairs); v5
+    // when its shared memory (counters: a byte per row, a bit beyond 160k rows; two block
+    // slots per warp) fits, else v4 when its byte counters fit (n <= 200k), else v3.
+    // MCINV_KERNEL=v3|v4|v5 forces one (error if it does not apply).
     const int pref = kernel_pref();
-    const bool v4_ok = lv && L.lgC <= 5 && n <= 200000 && !lv->deferred;
-    if ((pref == 4 || pref == 5) && !v4_ok) return fail(ctx, MCINV_E_INVALID, "v4/v5 kernel not applicable to this run");
-    // auto: v4 whenever it applies (measured faster than v3 on configs 1-3: no per-level
-    // barrier; profiles/), else v3
-    const bool v4 = v4_ok && (pref == 4 || pref == 5 || pref == 0);
+    const bool flow_ok = lv && L.lgC <= 5 && !lv->deferred;
+    if ((pref == 4 || pref == 5) && !flow_ok) return fail(ctx, MCINV_E_INVALID, "v4/v5 kernel not applicable to this run");
+    // auto: dataflow only up to 200k rows -- beyond, v3 (level barriers, K = 2 chains per
+    // thread) measured 15-20% faster than v5 with bit counters at n = 1e6 (C = 8/16/32:
+    // 3.04/3.45/3.69e10 vs 2.64/2.57/3.00e10 site-updates/s; profiles/r01_bigsmall.log)
+    bool v4 = flow_ok && (pref == 4 || pref == 5 || (pref == 0 && n <= 200000));  // v4 or v5
     // chains per thread K (register blocking; real C, both chains in one SE group, no
-    // trace / deferred items): default 2 for v3 (config 4 +19%), 1 for v4 (config 2 measured
-    // faster with more threads than with blocking, profiles/); MCINV_K=1|2 overrides
+    // trace / deferred items): default 2 for v3 (config 4 +19%), 1 for the dataflow kernels
+    // (config 2 measured faster with more threads than with blocking, profiles/); MCINV_K
     int lgK = (lv && ctx->dtype == MCINV_F64 && L.lgC >= 1 && a->group_size >= 2 && !lv->deferred) ? 1 : 0;
     if (const char *e = std::getenv("MCINV_K")) lgK = std::atoi(e) >= 2 ? lgK : 0;
-    else if (v4) lgK = 0;
+    if (v4) lgK = 0;
     // threads: v3 enough for the widest phase x C/K (<= 768: 85 registers, measured best
-    // for configs 2-5); v4 1024 real / 768 complex (more warps keep more rows in flight;
-    // measured best for configs 2 / 3), fewer for tiny n; a multiple of 32 and of C/K
-    int threads3 = 0;
-    if (lv) {
-        int64_t want = v4 ? std::min<int64_t>(ctx->dtype == MCINV_C128 ? 768 : 1024, (int64_t)n << (L.lgC - lgK))
-                          : std::min<int64_t>(768, (int64_t)std::max(lv->max_rows, 1) << (L.lgC - lgK));
+    // for configs 2-5); dataflow 1024 real / 768 complex (more warps keep more rows in
+    // flight; measured best for configs 2 / 3), fewer for tiny n; a multiple of 32 and of C/K
+    auto threads_for = [&](bool flow) {
+        int64_t want = flow ? std::min<int64_t>(ctx->dtype == MCINV_C128 ? 768 : 1024, (int64_t)n << (L.lgC - lgK))
+                            : std::min<int64_t>(768, (int64_t)std::max(lv->max_rows, 1) << (L.lgC - lgK));
         if (const char *e = std::getenv("MCINV_THREADS")) want = std::atoi(e);
         want = std::min<int64_t>(1024, std::max<int64_t>(want, int64_t(1) << (L.lgC - lgK)));
-        threads3 = (int)((want + 31) / 32 * 32);
-    }
-    // v5 (TMA-staged plan blocks) when forced or auto (kV5Default) and its shared memory fits
+        return (int)((want + 31) / 32 * 32);
+    };
+    int threads3 = lv ? threads_for(v4) : 0;
     bool v5 = v4 && (pref == 5 || (pref == 0 && kV5Default));
-    LevelDev::Slots *sl = v4 ? get_slots<S>(ctx, lv, 32 >> (L.lgC - lgK), threads3 / 32, v5) : nullptr;
+    LevelDev::Slots *sl = v5 ? get_slots<S>(ctx, lv, 32 >> L.lgC, threads3 / 32, true) : nullptr;
     if (v5 && sl && mcinv::sweep5_smem((int)n, threads3, sl->maxb) > 227 * 1024) {
         if (pref == 5) return fail(ctx, MCINV_E_INVALID, "v5 blocks do not fit shared memory");
         v5 = false;
-        sl = get_slots<S>(ctx, lv, 32 >> (L.lgC - lgK), threads3 / 32, false);
+    }
+    if (v4 && !v5) {
+        if (n > 200000) {  // v4's byte counters do not fit: level kernel (its layout is the same)
+            if (pref == 4) return fail(ctx, MCINV_E_INVALID, "v4 counters do not fit shared memory");
+            v4 = false;
+            if (ctx->dtype == MCINV_F64 && L.lgC >= 1 && a->group_size >= 2 && !std::getenv("MCINV_K")) lgK = 1;
+            threads3 = threads_for(false);
+        } else {
+            sl = get_slots<S>(ctx, lv, 32 >> L.lgC, threads3 / 32, false);
+        }
     }
     if (!ctx->host_only) CK(cudaStreamSynchronize(0));  // plan uploads (legacy stream) complete
     if (v4 && !sl) return fail(ctx, MCINV_E_NOMEM, "v4 slot arrays");

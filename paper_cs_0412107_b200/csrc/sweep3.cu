@@ -612,6 +612,7 @@ cudaError_t launch_sweep3(const Sweep3Params<S> &p, int threads, cudaStream_t st
 }
 
 // ---------------------------------------------------------------- v5: v4 + TMA-staged plan
+constexpr int kByteCounters = 160000;  // larger n: one completion bit per row
 //
 // The dataflow kernel of v4 with the plan data of every warp group (row
 // records, delta/sigma, entry columns, coefficient pairs, pattern slots)
@@ -721,7 +722,10 @@ __device__ __forceinline__ void accumulate_blk(const Sweep3Params<S> &p, const Z
 
 }  // namespace
 
-template <typename S, int KU, int NT, int LGP>
+// BITS: one completion bit per row instead of a byte (n up to ~1.8M rows in shared memory):
+// with the sweep barrier a row's counter only has to tell "updated in this sweep" from
+// "in the previous one", i.e. its parity; publishing toggles the bit (atomicXor).
+template <typename S, int KU, int NT, int LGP, bool BITS>
 __global__ void __launch_bounds__(NT, 1) sweep5_kernel(const Sweep3Params<S> p) {
     constexpr int E = ScalarTraits<S>::kDoubles;
     constexpr int P = 1 << LGP;
@@ -750,10 +754,16 @@ __global__ void __launch_bounds__(NT, 1) sweep5_kernel(const Sweep3Params<S> p) 
     uint64_t *bars = reinterpret_cast<uint64_t *>(sm5);
     unsigned char *blk = sm5 + 16 * W;
     unsigned char *done = blk + (size_t)2 * W * p.maxb;
+    unsigned *dbits = reinterpret_cast<unsigned *>(done);
     const uint32_t bar0 = smem_addr(bars + 2 * w), bar1 = bar0 + 8;
     unsigned char *buf0 = blk + (size_t)2 * w * p.maxb, *buf1 = buf0 + p.maxb;
 
-    for (int j = tid; j < p.n; j += B) done[j] = static_cast<unsigned char>(p.s_begin);
+    if constexpr (BITS) {
+        const unsigned fill = (p.s_begin & 1) ? 0xffffffffu : 0u;
+        for (int j = tid; j < (p.n + 31) / 32; j += B) dbits[j] = fill;
+    } else {
+        for (int j = tid; j < p.n; j += B) done[j] = static_cast<unsigned char>(p.s_begin);
+    }
     if (lane == 0) {
         mbar_init(bar0, 1);
         mbar_init(bar1, 1);
@@ -805,10 +815,17 @@ __global__ void __launch_bounds__(NT, 1) sweep5_kernel(const Sweep3Params<S> p) 
                 const double phi = noise_phi(p.noise, static_cast<uint32_t>(i), k, gchain, p.key0, p.key1);
                 const int nlow = rec.z >> 16;
                 for (int e = 0; e < nlow; ++e) {
-                    const volatile unsigned char *f = done + col[e];
-                    if (*f != need) {
+                    const int j = col[e];
+                    auto ready = [&]() -> bool {
+                        if constexpr (BITS)
+                            return ((reinterpret_cast<volatile unsigned *>(dbits)[j >> 5] >> (j & 31)) & 1u) ==
+                                   (need & 1u);
+                        else
+                            return reinterpret_cast<volatile unsigned char *>(done)[j] == need;
+                    };
+                    if (!ready()) {
                         unsigned spins = 0;
-                        while (*f != need && !*reinterpret_cast<volatile unsigned *>(p.err)) {
+                        while (!ready() && !*reinterpret_cast<volatile unsigned *>(p.err)) {
                             __nanosleep(32);
                             if (++spins > (1u << 26)) {  // ~seconds: report, do not hang
                                 atomicOr(p.err, 1u);
@@ -833,7 +850,8 @@ __global__ void __launch_bounds__(NT, 1) sweep5_kernel(const Sweep3Params<S> p) 
             __syncwarp();  // the row's stores are ordered before its counter update
             if (valid && c == 0) {
                 __threadfence_block();  // release
-                *reinterpret_cast<volatile unsigned char *>(done + i) = need;
+                if constexpr (BITS) atomicXor(dbits + (i >> 5), 1u << (i & 31));
+                else *reinterpret_cast<volatile unsigned char *>(done + i) = need;
             }
             if (sampling)
                 accumulate_blk<S, P, V>(p, zcol, rec, col, pz, zi, wi, valid && active, lane, gleader, towner, sd,
@@ -845,33 +863,39 @@ __global__ void __launch_bounds__(NT, 1) sweep5_kernel(const Sweep3Params<S> p) 
 
 size_t sweep5_smem(int n, int threads, int maxb) {
     const size_t W = (size_t)threads / 32;
-    return 16 * W + 2 * W * (size_t)maxb + ((size_t)n + 15) / 16 * 16;
+    const size_t counters = n > kByteCounters ? ((size_t)n + 127) / 128 * 16 : ((size_t)n + 15) / 16 * 16;
+    return 16 * W + 2 * W * (size_t)maxb + counters;
 }
 
 namespace {
 
-template <typename S, int LGP>
-cudaError_t launch5(const Sweep3Params<S> &p, int threads, cudaStream_t st) {
+template <typename S, int LGP, bool BITS>
+cudaError_t launch5b(const Sweep3Params<S> &p, int threads, cudaStream_t st) {
     constexpr int KS = ScalarTraits<S>::kDoubles == 1 ? 4 : 2;
     const int C = 1 << p.lgC;
     const int blocks = (p.chains + C - 1) / C;
     const size_t smem = sweep5_smem(p.n, threads, p.maxb);
     cudaError_t e;
     if (threads <= 512) {
-        auto k = sweep5_kernel<S, 2 * KS, 512, LGP>;
+        auto k = sweep5_kernel<S, 2 * KS, 512, LGP, BITS>;
         e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e == cudaSuccess) k<<<blocks, threads, smem, st>>>(p);
     } else if (threads <= 768) {
-        auto k = sweep5_kernel<S, KS, 768, LGP>;
+        auto k = sweep5_kernel<S, KS, 768, LGP, BITS>;
         e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e == cudaSuccess) k<<<blocks, threads, smem, st>>>(p);
     } else {
-        auto k = sweep5_kernel<S, KS, 1024, LGP>;
+        auto k = sweep5_kernel<S, KS, 1024, LGP, BITS>;
         e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e == cudaSuccess) k<<<blocks, threads, smem, st>>>(p);
     }
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
+}
+
+template <typename S, int LGP>
+cudaError_t launch5(const Sweep3Params<S> &p, int threads, cudaStream_t st) {
+    return p.n > kByteCounters ? launch5b<S, LGP, true>(p, threads, st) : launch5b<S, LGP, false>(p, threads, st);
 }
 
 }  // namespace

@@ -536,3 +536,17 @@ def test_irregular_structure(mc, orc, kernel, monkeypatch):
     pat = ((key // n).astype(np.int32), (key % n).astype(np.int32))
     compare_run(mc, orc, c, pattern=pat, seed=19, chains=96, burn_in=3, cycles=4, outputs=("diag", "pattern"),
                 group_size=16, chain_begin=64)
+
+
+def test_v5_bit_counters_large_n(mc, orc):
+    """n above the byte-counter limit (160k rows): v5 keeps one completion bit
+    per row (parity with the sweep barrier); states of sampled chains and the
+    diag estimate vs the oracle."""
+    c = W.pedigree(170000, seed=91)
+    inv = mc.Inverter(c)
+    inv.run(23, 64, 1, 2, ("diag",), group_size=32)
+    assert inv.kernel_info()["version"] == 5
+    r = orc.Matrix(c).run(23, 2, 1, 2, ("diag",), chain_begin=62)
+    zg, wg = inv.get_state(62, 2)
+    states_match(zg, wg, r["z"], r["w"])
+    inv.close()
