@@ -125,6 +125,7 @@ struct Sweep3Params {
     const unsigned char *blob;
     const int64_t *gofs;  // [groups + 1] byte offsets of the blocks in blob
     int maxb;             // largest block (bytes)
+    int spin_ns;          // dataflow waits: __nanosleep between counter polls (0: none)
 };
 
 template <typename S>

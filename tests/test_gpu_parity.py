@@ -550,3 +550,29 @@ def test_v5_bit_counters_large_n(mc, orc):
     zg, wg = inv.get_state(62, 2)
     states_match(zg, wg, r["z"], r["w"])
     inv.close()
+
+
+@pytest.mark.parametrize("kernel", ["v4", "v5"])
+def test_dataflow_long_dependency_chain(mc, orc, monkeypatch, kernel):
+    """Worst case for the dataflow kernels: a non-symmetric tridiagonal C
+    (every row depends on the previous one, a dependency chain of depth n in
+    each sweep) plus a few long-range couplings, with many warps and many
+    sweeps in one launch; states and diag / pattern estimates vs the oracle."""
+    monkeypatch.setenv("MCINV_KERNEL", kernel)
+    n = 300
+    a = np.zeros((n, n))
+    for i in range(n):
+        a[i, i] = 3.0
+        if i > 0:
+            a[i, i - 1] = -0.9
+        if i + 1 < n:
+            a[i, i + 1] = -0.7
+        if i % 37 == 5 and i + 150 < n:
+            a[i, i + 150] = 0.4
+            a[i + 150, i] = -0.3
+    c = W.CSR.from_dense(a)
+    for C, th in ((8, "1024"), (32, "1024"), (1, "256")):
+        monkeypatch.setenv("MCINV_C", str(C))
+        monkeypatch.setenv("MCINV_THREADS", th)
+        compare_run(mc, orc, c, seed=12, chains=64, burn_in=7, cycles=13, outputs=("diag", "pattern"),
+                    group_size=8)
