@@ -27,6 +27,7 @@
 // which each lane posts ONE fire-and-forget reduction (red.global.add) into
 // the group's slot; the slots of all groups (41 MB for config 2) stay in L2.
 #include <cstdlib>
+#include <type_traits>
 
 #include "mcinv_internal.cuh"
 #include "noise.cuh"
@@ -76,6 +77,14 @@ __device__ __forceinline__ S transpose_sum(S (&v)[V], int lane, int &held) {
         }
     }
     return v[0];
+}
+
+// &zcol[j * ld] as one IMAD.WIDE.U32 (32 x 32 -> 64-bit product plus the base) instead of
+// a 64-bit multiply and shift: j < 2^31 and the row stride in bytes (ld * sizeof) < 2^32
+template <typename T>
+__device__ __forceinline__ T *zrow(T *zcol, int j, uint32_t stride) {
+    using C = typename std::conditional<std::is_const<T>::value, const char, char>::type;
+    return reinterpret_cast<T *>(reinterpret_cast<C *>(zcol) + static_cast<uint64_t>(static_cast<uint32_t>(j)) * stride);
 }
 
 // the (a, b) coefficient pair of an entry in one (real) or two (complex) 16-B loads
@@ -141,6 +150,7 @@ __device__ __forceinline__ void st_zwk(ZW<S> *p, const ZWK<S, K> &r) {
 template <typename S, int KU, int K>
 __device__ __forceinline__ void row_sums(const Sweep3Params<S> &p, const ZW<S> *zcol, int beg, int cnt,
                                          S (&az)[K], S (&aw)[K]) {
+    const uint32_t zst = static_cast<uint32_t>(p.ld) * static_cast<uint32_t>(sizeof(ZW<S>));
     for (int e0 = 0; e0 < cnt; e0 += KU) {
         int j[KU];
         ZWK<S, K> v[KU];
@@ -149,7 +159,7 @@ __device__ __forceinline__ void row_sums(const Sweep3Params<S> &p, const ZW<S> *
         for (int q = 0; q < KU; ++q) j[q] = __ldg(p.ent_col + beg + e0 + q);
 #pragma unroll
         for (int q = 0; q < KU; ++q) {
-            v[q] = ld_zwk<S, K>(zcol + (int64_t)(e0 + q < cnt ? j[q] : 0) * p.ld);
+            v[q] = ld_zwk<S, K>(zrow(zcol, (e0 + q < cnt ? j[q] : 0), zst));
             ab[q] = ldg_ab(reinterpret_cast<const ZW<S> *>(p.ent_ab) + beg + e0 + q);
         }
 #pragma unroll
@@ -184,6 +194,7 @@ template <typename S, int P, int V, int K>
 __device__ __forceinline__ void accumulate_row(const Sweep3Params<S> &p, const ZW<S> *zcol, int4 rec, const S (&zi)[K],
                                                const S (&wi)[K], const bool (&acc)[K], int lane, bool gleader,
                                                bool towner, double *sd, double *sp, bool want_diag, bool want_pat) {
+    const uint32_t zst = static_cast<uint32_t>(p.ld) * static_cast<uint32_t>(sizeof(ZW<S>));
     constexpr int E = ScalarTraits<S>::kDoubles;
     const int i = rec.x, beg = rec.y;
     bool any = false;
@@ -206,7 +217,7 @@ __device__ __forceinline__ void accumulate_row(const Sweep3Params<S> &p, const Z
     const int nlow = any ? rec.z >> 16 : 0;
     if constexpr (P == 1) {
         for (int e = 0; e < nlow; ++e) {
-            const ZWK<S, K> u = ld_zwk<S, K>(zcol + (int64_t)__ldg(p.ent_col + beg + e) * p.ld);
+            const ZWK<S, K> u = ld_zwk<S, K>(zrow(zcol, __ldg(p.ent_col + beg + e), zst));
             S x = zero_s<S>(), y = zero_s<S>();
 #pragma unroll
             for (int h = 0; h < K; ++h)
@@ -228,7 +239,7 @@ __device__ __forceinline__ void accumulate_row(const Sweep3Params<S> &p, const Z
                 const int e = b * VE + q;
                 const int jc = __ldg(p.ent_col + beg + e);  // padded: always in bounds
                 const bool ok = e < nlow;
-                const ZWK<S, K> u = ld_zwk<S, K>(zcol + (int64_t)(ok ? jc : 0) * p.ld);
+                const ZWK<S, K> u = ld_zwk<S, K>(zrow(zcol, (ok ? jc : 0), zst));
                 S x = zero_s<S>(), y = zero_s<S>();
 #pragma unroll
                 for (int h = 0; h < K; ++h)
@@ -255,6 +266,7 @@ __device__ __forceinline__ void accumulate_row(const Sweep3Params<S> &p, const Z
 
 template <typename S, int KU, int NT, int LGP, int K>
 __global__ void __launch_bounds__(NT, 1) sweep3_kernel(const Sweep3Params<S> p) {
+    const uint32_t zst = static_cast<uint32_t>(p.ld) * static_cast<uint32_t>(sizeof(ZW<S>));
     constexpr int E = ScalarTraits<S>::kDoubles;
     constexpr int P = 1 << LGP;        // lanes of one SE group inside this CTA (K chains per lane)
     constexpr int V = P < 8 ? P : 8;   // products per transpose-reduction (pairs of one entry)
@@ -316,7 +328,7 @@ __global__ void __launch_bounds__(NT, 1) sweep3_kernel(const Sweep3Params<S> p) 
                         wi[h] = fma_s(neg_s(conj_s(dl)), aw[h], scale_s(conj_s(sg), phi[h]));
                         out.v[h] = ZW<S>{zi[h], wi[h]};
                     }
-                    st_zwk<S, K>(zcol + (int64_t)i * p.ld, out);
+                    st_zwk<S, K>(zrow(zcol, i, zst), out);
                     if (want_full && sampling) {
                         const int64_t ts = s - p.snap_s0;
 #pragma unroll
@@ -346,8 +358,8 @@ __global__ void __launch_bounds__(NT, 1) sweep3_kernel(const Sweep3Params<S> p) 
                             S qz = zero_s<S>();
                             for (int e = __ldg(p.tq_eptr + o); e < __ldg(p.tq_eptr + o + 1); ++e)
                                 qz = add_s(qz, mul_s(ldg_s(p.tq_val + e),
-                                                     ld_zw(zcol + (int64_t)__ldg(p.tq_col + e) * p.ld).z));
-                            tr = add_s(tr, zwc_s(qz, ld_zw(zcol + (int64_t)i * p.ld).w));
+                                                     ld_zw(zrow(zcol, __ldg(p.tq_col + e), zst)).z));
+                            tr = add_s(tr, zwc_s(qz, ld_zw(zrow(zcol, i, zst)).w));
                         }
                     }
                     // ---- deferred pattern pairs z_i w_j^*
@@ -360,8 +372,8 @@ __global__ void __launch_bounds__(NT, 1) sweep3_kernel(const Sweep3Params<S> p) 
                             const int o = q0 + (t >> lgL);
                             S x = zero_s<S>();
                             if (valid && active[0])
-                                x = zwc_s(ld_zw(zcol + (int64_t)__ldg(p.pp_i + o) * p.ld).z,
-                                          ld_zw(zcol + (int64_t)__ldg(p.pp_j + o) * p.ld).w);
+                                x = zwc_s(ld_zw(zrow(zcol, __ldg(p.pp_i + o), zst)).z,
+                                          ld_zw(zrow(zcol, __ldg(p.pp_j + o), zst)).w);
                             x = group_sum<P>(x);
                             if (valid && active[0] && gleader)
                                 slot_red(sp + (int64_t)__ldg(p.pp_slot + o) * E, x);
@@ -431,6 +443,7 @@ __device__ __forceinline__ void wait_ready(F ready, unsigned *err, int spin_ns) 
 
 template <typename S, int KU, int NT, int LGP, int K>
 __global__ void __launch_bounds__(NT, 1) sweep4_kernel(const Sweep3Params<S> p) {
+    const uint32_t zst = static_cast<uint32_t>(p.ld) * static_cast<uint32_t>(sizeof(ZW<S>));
     constexpr int E = ScalarTraits<S>::kDoubles;
     constexpr int P = 1 << LGP;        // lanes of one SE group (K chains per lane)
     constexpr int V = P < 8 ? P : 8;
@@ -503,7 +516,7 @@ __global__ void __launch_bounds__(NT, 1) sweep4_kernel(const Sweep3Params<S> p) 
                     wi[h] = fma_s(neg_s(conj_s(dl)), aw[h], scale_s(conj_s(sg), phi[h]));
                     out.v[h] = ZW<S>{zi[h], wi[h]};
                 }
-                st_zwk<S, K>(zcol + (int64_t)i * p.ld, out);
+                st_zwk<S, K>(zrow(zcol, i, zst), out);
                 if (want_full && sampling) {
                     const int64_t ts = s - p.snap_s0;
 #pragma unroll
@@ -671,6 +684,7 @@ __device__ __forceinline__ void prefetch_l2(const void *p) {
 template <typename S, int KU>
 __device__ __forceinline__ void row_sums_blk(const Sweep3Params<S> &p, const ZW<S> *zcol, const int *col,
                                              const ZW<S> *ab, int cnt, S &az, S &aw) {
+    const uint32_t zst = static_cast<uint32_t>(p.ld) * static_cast<uint32_t>(sizeof(ZW<S>));
     for (int e0 = 0; e0 < cnt; e0 += KU) {
         int j[KU];
         ZW<S> v[KU], c[KU];
@@ -678,7 +692,7 @@ __device__ __forceinline__ void row_sums_blk(const Sweep3Params<S> &p, const ZW<
         for (int q = 0; q < KU; ++q) j[q] = col[e0 + q];
 #pragma unroll
         for (int q = 0; q < KU; ++q) {
-            v[q] = ld_zw(zcol + (int64_t)(e0 + q < cnt ? j[q] : 0) * p.ld);
+            v[q] = ld_zw(zrow(zcol, (e0 + q < cnt ? j[q] : 0), zst));
             c[q] = ab[e0 + q];
         }
 #pragma unroll
@@ -695,6 +709,7 @@ template <typename S, int P, int V>
 __device__ __forceinline__ void accumulate_blk(const Sweep3Params<S> &p, const ZW<S> *zcol, int4 rec, const int *col,
                                                const int2 *pz, S zi, S wi, bool acc, int lane, bool gleader,
                                                bool towner, double *sd, double *sp, bool want_diag, bool want_pat) {
+    const uint32_t zst = static_cast<uint32_t>(p.ld) * static_cast<uint32_t>(sizeof(ZW<S>));
     constexpr int E = ScalarTraits<S>::kDoubles;
     const int i = rec.x;
     if (want_diag || want_pat) {
@@ -708,7 +723,7 @@ __device__ __forceinline__ void accumulate_blk(const Sweep3Params<S> &p, const Z
     const int nlow = acc ? rec.z >> 16 : 0;
     if constexpr (P == 1) {
         for (int e = 0; e < nlow; ++e) {
-            const ZW<S> u = ld_zw(zcol + (int64_t)col[e] * p.ld);
+            const ZW<S> u = ld_zw(zrow(zcol, col[e], zst));
             const int2 z2 = pz[e];
             if (z2.x >= 0) slot_red(sp + (int64_t)z2.x * E, zwc_s(zi, u.w));
             if (z2.y >= 0) slot_red(sp + (int64_t)z2.y * E, zwc_s(u.z, wi));
@@ -722,7 +737,7 @@ __device__ __forceinline__ void accumulate_blk(const Sweep3Params<S> &p, const Z
             for (int q = 0; q < VE; ++q) {
                 const int e = b * VE + q;
                 const bool ok = e < nlow;
-                const ZW<S> u = ld_zw(zcol + (int64_t)(ok ? col[e] : 0) * p.ld);
+                const ZW<S> u = ld_zw(zrow(zcol, (ok ? col[e] : 0), zst));
                 v[2 * q] = ok ? zwc_s(zi, u.w) : zero_s<S>();
                 v[2 * q + 1] = ok ? zwc_s(u.z, wi) : zero_s<S>();
             }
@@ -745,6 +760,7 @@ __device__ __forceinline__ void accumulate_blk(const Sweep3Params<S> &p, const Z
 // "in the previous one", i.e. its parity; publishing toggles the bit (atomicXor).
 template <typename S, int KU, int NT, int LGP, bool BITS>
 __global__ void __launch_bounds__(NT, 1) sweep5_kernel(const Sweep3Params<S> p) {
+    const uint32_t zst = static_cast<uint32_t>(p.ld) * static_cast<uint32_t>(sizeof(ZW<S>));
     constexpr int E = ScalarTraits<S>::kDoubles;
     constexpr int P = 1 << LGP;
     constexpr int V = P < 8 ? P : 8;
@@ -834,9 +850,9 @@ __global__ void __launch_bounds__(NT, 1) sweep5_kernel(const Sweep3Params<S> p) 
                 // upper neighbours hold their sweep s-1 values until this row publishes: start
                 // their lines on the way before the noise (its ALU time covers the latency)
                 if (p.prefetch == 1)
-                    for (int e = nlow; e < cnt; ++e) prefetch_l1(zcol + (int64_t)col[e] * p.ld);
+                    for (int e = nlow; e < cnt; ++e) prefetch_l1(zrow(zcol, col[e], zst));
                 else if (p.prefetch >= 2)  // 3: lower ones too (L2 is the coherence point: safe)
-                    for (int e = p.prefetch == 3 ? 0 : nlow; e < cnt; ++e) prefetch_l2(zcol + (int64_t)col[e] * p.ld);
+                    for (int e = p.prefetch == 3 ? 0 : nlow; e < cnt; ++e) prefetch_l2(zrow(zcol, col[e], zst));
                 const double phi = noise_phi(p.noise, static_cast<uint32_t>(i), k, gchain, p.key0, p.key1);
                 for (int e = 0; e < nlow; ++e) {
                     const int j = col[e];
@@ -855,7 +871,7 @@ __global__ void __launch_bounds__(NT, 1) sweep5_kernel(const Sweep3Params<S> p) 
                 const S dl = dsg[0], sg = dsg[1];
                 zi = fma_s(neg_s(dl), az, scale_s(sg, phi));
                 wi = fma_s(neg_s(conj_s(dl)), aw, scale_s(conj_s(sg), phi));
-                zcol[(int64_t)i * p.ld] = ZW<S>{zi, wi};
+                *zrow(zcol, i, zst) = ZW<S>{zi, wi};
                 if (want_full && sampling) {
                     const int64_t ts = s - p.snap_s0;
                     p.snap_x[(ts * p.n + i) * p.ld + chain] = zi;
