@@ -758,7 +758,7 @@ __device__ __forceinline__ void accumulate_blk(const Sweep3Params<S> &p, const Z
 // BITS: one completion bit per row instead of a byte (n up to ~1.8M rows in shared memory):
 // with the sweep barrier a row's counter only has to tell "updated in this sweep" from
 // "in the previous one", i.e. its parity; publishing toggles the bit (atomicXor).
-template <typename S, int KU, int NT, int LGP, bool BITS>
+template <typename S, int KU, int NT, int LGC, int LGP, bool BITS>
 __global__ void __launch_bounds__(NT, 1) sweep5_kernel(const Sweep3Params<S> p) {
     const uint32_t zst = static_cast<uint32_t>(p.ld) * static_cast<uint32_t>(sizeof(ZW<S>));
     constexpr int E = ScalarTraits<S>::kDoubles;
@@ -770,8 +770,8 @@ __global__ void __launch_bounds__(NT, 1) sweep5_kernel(const Sweep3Params<S> p) 
     const int W = B >> 5;
     const int w = tid >> 5;
     const int lane = tid & 31;
-    const int lgC = p.lgC;  // C <= 32: a row's lanes are in one warp
-    const int C = 1 << lgC;
+    constexpr int lgC = LGC;  // C <= 32: a row's lanes are in one warp (compile-time: R, sub, c)
+    constexpr int C = 1 << lgC;
     const int c = lane & (C - 1);
     const int chain = (blockIdx.x << lgC) + c;
     const bool active = chain < p.chains;
@@ -805,7 +805,7 @@ __global__ void __launch_bounds__(NT, 1) sweep5_kernel(const Sweep3Params<S> p) 
     }
     __syncthreads();
 
-    const int R = 32 >> lgC;
+    constexpr int R = 32 >> lgC;
     const int ngroups = p.nslots / R;
     const int sub = lane >> lgC;
     auto issue = [&](int g, unsigned char *dst, uint32_t bar) {
@@ -900,46 +900,56 @@ size_t sweep5_smem(int n, int threads, int maxb) {
 
 namespace {
 
-template <typename S, int LGP, bool BITS>
+// one thread count per scalar type (1024 real, 768 complex: the register budget of one
+// CTA per SM); C and the group lanes P are template parameters (compile-time R, lane maps)
+template <typename S, int LGC, int LGP, bool BITS>
 cudaError_t launch5b(const Sweep3Params<S> &p, int threads, cudaStream_t st) {
-    constexpr int KS = ScalarTraits<S>::kDoubles == 1 ? 4 : 2;
-    const int C = 1 << p.lgC;
-    const int blocks = (p.chains + C - 1) / C;
+    constexpr bool kReal = ScalarTraits<S>::kDoubles == 1;
+    constexpr int NT = kReal ? 1024 : 768, KU = kReal ? 4 : 2;
+    if (threads > NT) return cudaErrorInvalidConfiguration;
+    const int blocks = (p.chains + (1 << LGC) - 1) >> LGC;
     const size_t smem = sweep5_smem(p.n, threads, p.maxb);
-    cudaError_t e;
-    if (threads <= 512) {
-        auto k = sweep5_kernel<S, 2 * KS, 512, LGP, BITS>;
-        e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e == cudaSuccess) k<<<blocks, threads, smem, st>>>(p);
-    } else if (threads <= 768) {
-        auto k = sweep5_kernel<S, KS, 768, LGP, BITS>;
-        e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e == cudaSuccess) k<<<blocks, threads, smem, st>>>(p);
-    } else {
-        auto k = sweep5_kernel<S, KS, 1024, LGP, BITS>;
-        e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e == cudaSuccess) k<<<blocks, threads, smem, st>>>(p);
-    }
+    auto k = sweep5_kernel<S, KU, NT, LGC, LGP, BITS>;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
+    k<<<blocks, threads, smem, st>>>(p);
     return cudaGetLastError();
 }
 
-template <typename S, int LGP>
+template <typename S, int LGC, int LGP>
 cudaError_t launch5(const Sweep3Params<S> &p, int threads, cudaStream_t st) {
-    return p.n > kByteCounters ? launch5b<S, LGP, true>(p, threads, st) : launch5b<S, LGP, false>(p, threads, st);
+    if constexpr (LGP > LGC) {
+        return cudaErrorInvalidValue;
+    } else {
+        return p.n > kByteCounters ? launch5b<S, LGC, LGP, true>(p, threads, st)
+                                   : launch5b<S, LGC, LGP, false>(p, threads, st);
+    }
+}
+
+template <typename S, int LGC>
+cudaError_t launch5c(const Sweep3Params<S> &p, int threads, cudaStream_t st) {
+    switch (p.lgP) {
+        case 0: return launch5<S, LGC, 0>(p, threads, st);
+        case 1: return launch5<S, LGC, 1>(p, threads, st);
+        case 2: return launch5<S, LGC, 2>(p, threads, st);
+        case 3: return launch5<S, LGC, 3>(p, threads, st);
+        case 4: return launch5<S, LGC, 4>(p, threads, st);
+        case 5: return launch5<S, LGC, 5>(p, threads, st);
+        default: return cudaErrorInvalidValue;
+    }
 }
 
 }  // namespace
 
 template <typename S>
 cudaError_t launch_sweep5(const Sweep3Params<S> &p, int threads, cudaStream_t st) {
-    switch (p.lgP) {
-        case 0: return launch5<S, 0>(p, threads, st);
-        case 1: return launch5<S, 1>(p, threads, st);
-        case 2: return launch5<S, 2>(p, threads, st);
-        case 3: return launch5<S, 3>(p, threads, st);
-        case 4: return launch5<S, 4>(p, threads, st);
-        case 5: return launch5<S, 5>(p, threads, st);
+    switch (p.lgC) {
+        case 0: return launch5c<S, 0>(p, threads, st);
+        case 1: return launch5c<S, 1>(p, threads, st);
+        case 2: return launch5c<S, 2>(p, threads, st);
+        case 3: return launch5c<S, 3>(p, threads, st);
+        case 4: return launch5c<S, 4>(p, threads, st);
+        case 5: return launch5c<S, 5>(p, threads, st);
         default: return cudaErrorInvalidValue;
     }
 }
