@@ -664,9 +664,14 @@ LevelDev::Slots *get_slots(mcinv_ctx *ctx, LevelDev *lv, int R, int W, bool bloc
     if (blocks) {
         // group block: int4 head {EP, bytes, off_ab, off_pz}; int4 rec[R] {i, entry offset in
         // the block, count | lower << 16, pattern slot of (i,i)}; S dsg[R][2]; int col[EP];
-        // ZW<S> ab[EP]; int2 pz[EP] (pattern runs). EP = entries + 8 (zero-coefficient
-        // padding for the unrolled reads), a multiple of 4; every section 16-B aligned.
+        // ZW<S> ab[EP]; int2 pz[EP] (pattern runs). Each row's entries are padded to a multiple
+        // of the kernel's gather unroll KU (4 real, 2 complex) with zero coefficients on the
+        // row's last column (its own row if it has none): the unrolled fma chain then needs no
+        // predicate, and fma(0, v, a) == a for the finite states of a converging run (only the
+        // sign of an exact zero sum can differ). EP a multiple of 4; sections 16-B aligned.
         const bool pat = !lv->h_pz.empty();
+        const int KU = sizeof(S) == sizeof(double) ? 4 : 2;
+        auto padded = [KU](int c) { return (c + KU - 1) / KU * KU; };
         const ZW<S> *hab = reinterpret_cast<const ZW<S> *>(lv->h_ab.data());
         const size_t ng = rec.size() / R;
         std::vector<int64_t> gofs(ng + 1, 0);
@@ -674,8 +679,8 @@ LevelDev::Slots *get_slots(mcinv_ctx *ctx, LevelDev *lv, int R, int W, bool bloc
         for (size_t g = 0; g < ng; ++g) {
             int E = 0;
             for (int r = 0; r < R; ++r)
-                if (rec[g * R + r].x >= 0) E += rec[g * R + r].z & 0xffff;
-            const int EP = (E + 8 + 3) / 4 * 4;
+                if (rec[g * R + r].x >= 0) E += padded(rec[g * R + r].z & 0xffff);
+            const int EP = (E + 3) / 4 * 4;
             const size_t off_col = 16 + 16 * (size_t)R + 2 * sizeof(S) * R;
             const size_t off_ab = off_col + 4 * (size_t)EP;
             const size_t off_pz = off_ab + sizeof(ZW<S>) * EP;
@@ -699,7 +704,12 @@ LevelDev::Slots *get_slots(mcinv_ctx *ctx, LevelDev *lv, int R, int W, bool bloc
                             make_int2(lv->h_pz[2 * (q.y + t)], lv->h_pz[2 * (q.y + t) + 1]);
                     }
                 }
-                e += cnt;
+                const int last = cnt > 0 ? lv->h_ent_col[q.y + cnt - 1] : q.x;
+                for (int t = cnt; t < padded(cnt); ++t) {
+                    reinterpret_cast<int *>(b + off_col)[e + t] = last;  // ab[e + t] stays zero
+                    if (pat) reinterpret_cast<int2 *>(b + off_pz)[e + t] = make_int2(-1, -1);
+                }
+                e += padded(cnt);
             }
             for (int t = e; t < EP; ++t)
                 if (pat) reinterpret_cast<int2 *>(b + off_pz)[t] = make_int2(-1, -1);

@@ -680,7 +680,9 @@ __device__ __forceinline__ void prefetch_l2(const void *p) {
     asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
 
-// Eq. (4)/(5) fma chains from a staged block (see row_sums)
+// Eq. (4)/(5) fma chains from a staged block (see row_sums): the host padded the row's
+// entries to a multiple of KU with zero coefficients on a valid column, so the unrolled
+// chain runs unpredicated
 template <typename S, int KU>
 __device__ __forceinline__ void row_sums_blk(const Sweep3Params<S> &p, const ZW<S> *zcol, const int *col,
                                              const ZW<S> *ab, int cnt, S &az, S &aw) {
@@ -692,15 +694,14 @@ __device__ __forceinline__ void row_sums_blk(const Sweep3Params<S> &p, const ZW<
         for (int q = 0; q < KU; ++q) j[q] = col[e0 + q];
 #pragma unroll
         for (int q = 0; q < KU; ++q) {
-            v[q] = ld_zw(zrow(zcol, (e0 + q < cnt ? j[q] : 0), zst));
+            v[q] = ld_zw(zrow(zcol, j[q], zst));
             c[q] = ab[e0 + q];
         }
 #pragma unroll
-        for (int q = 0; q < KU; ++q)
-            if (e0 + q < cnt) {
-                az = fma_s(c[q].z, v[q].z, az);
-                aw = fma_s(c[q].w, v[q].w, aw);
-            }
+        for (int q = 0; q < KU; ++q) {
+            az = fma_s(c[q].z, v[q].z, az);
+            aw = fma_s(c[q].w, v[q].w, aw);
+        }
     }
 }
 
@@ -849,10 +850,15 @@ __global__ void __launch_bounds__(NT, 1) sweep5_kernel(const Sweep3Params<S> p) 
                 const int nlow = rec.z >> 16;
                 // upper neighbours hold their sweep s-1 values until this row publishes: start
                 // their lines on the way before the noise (its ALU time covers the latency)
-                if (p.prefetch == 1)
+                if (p.prefetch == 3) {  // all neighbours into L2 (the coherence point: safe for lower ones)
+                    for (int e0 = 0; e0 < cnt; e0 += KU)  // KU-padded entry lists: no predicate
+#pragma unroll
+                        for (int q = 0; q < KU; ++q) prefetch_l2(zrow(zcol, col[e0 + q], zst));
+                } else if (p.prefetch == 1) {
                     for (int e = nlow; e < cnt; ++e) prefetch_l1(zrow(zcol, col[e], zst));
-                else if (p.prefetch >= 2)  // 3: lower ones too (L2 is the coherence point: safe)
-                    for (int e = p.prefetch == 3 ? 0 : nlow; e < cnt; ++e) prefetch_l2(zrow(zcol, col[e], zst));
+                } else if (p.prefetch == 2) {
+                    for (int e = nlow; e < cnt; ++e) prefetch_l2(zrow(zcol, col[e], zst));
+                }
                 const double phi = noise_phi(p.noise, static_cast<uint32_t>(i), k, gchain, p.key0, p.key1);
                 for (int e = 0; e < nlow; ++e) {
                     const int j = col[e];
