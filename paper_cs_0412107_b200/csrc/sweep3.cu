@@ -429,9 +429,15 @@ template <typename F>
 __device__ __forceinline__ void wait_ready(F ready, unsigned *err, int spin_ns) {
     if (ready()) return;
     for (unsigned spins = 1;; ++spins) {
-        if (spin_ns > 0) __nanosleep(spin_ns);
-        if (ready()) return;
-        if ((spins & 255u) == 0) {
+        if (spin_ns > 0) {
+            __nanosleep(spin_ns);
+            if (ready()) return;
+        } else {  // busy poll: 8 polls per round (a load, a compare and a branch each)
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (ready()) return;
+        }
+        if ((spins & 63u) == 0) {
             if (*reinterpret_cast<volatile unsigned *>(err)) return;
             if (spins > (1u << 26)) {
                 atomicOr(err, 1u);
