@@ -126,6 +126,7 @@ struct Sweep3Params {
     const int64_t *gofs;  // [groups + 1] byte offsets of the blocks in blob
     int maxb;             // largest block (bytes)
     int spin_ns;          // dataflow waits: __nanosleep between counter polls (0: none)
+    int reconv;           // v5: __syncwarp at the item end (bit 0) / after the dependency waits (bit 1)
     int prefetch;         // v5: prefetch upper neighbours' lines before the noise (0 off, 1 L1, 2 L2)
 };
 

@@ -852,6 +852,7 @@ __global__ void __launch_bounds__(NT, 1) sweep5_kernel(const Sweep3Params<S> p) 
             const bool valid = rec.x >= 0;
             const int i = rec.x, cnt = valid ? rec.z & 0xffff : 0;
             S zi = zero_s<S>(), wi = zero_s<S>();
+            double phi = 0.0;
             if (valid) {
                 const int nlow = rec.z >> 16;
                 // upper neighbours hold their sweep s-1 values until this row publishes: start
@@ -865,7 +866,7 @@ __global__ void __launch_bounds__(NT, 1) sweep5_kernel(const Sweep3Params<S> p) 
                 } else if (p.prefetch == 2) {
                     for (int e = nlow; e < cnt; ++e) prefetch_l2(zrow(zcol, col[e], zst));
                 }
-                const double phi = noise_phi(p.noise, static_cast<uint32_t>(i), k, gchain, p.key0, p.key1);
+                phi = noise_phi(p.noise, static_cast<uint32_t>(i), k, gchain, p.key0, p.key1);
                 for (int e = 0; e < nlow; ++e) {
                     const int j = col[e];
                     auto ready = [&]() -> bool {
@@ -877,6 +878,11 @@ __global__ void __launch_bounds__(NT, 1) sweep5_kernel(const Sweep3Params<S> p) 
                     };
                     wait_ready(ready, p.err, p.spin_ns);
                 }
+            }
+            // rows whose dependencies were ready left the wait early; reconverge so that the
+            // gathers and the fma chains of the warp's R rows issue as one instruction stream
+            if (p.reconv & 2) __syncwarp();
+            if (valid) {
                 __threadfence_block();
                 S az = zero_s<S>(), aw = zero_s<S>();
                 row_sums_blk<S, KU>(p, zcol, col, ab, cnt, az, aw);
@@ -899,6 +905,10 @@ __global__ void __launch_bounds__(NT, 1) sweep5_kernel(const Sweep3Params<S> p) 
             if (sampling)
                 accumulate_blk<S, P, V>(p, zcol, rec, col, pz, zi, wi, valid && active, lane, gleader, towner, sd,
                                         sp, want_diag, want_pat);
+            // reconverge before the next item: lanes that skipped a divergent step of the
+            // accumulation (leaders' reductions) otherwise start it as a separate sub-warp and
+            // the split persists (diag-only config 2: 1.57e10 without, 2.79e10 with)
+            if (p.reconv & 1) __syncwarp();
         }
         __syncthreads();  // sweep boundary: all reads of sweep s values are done
     }
@@ -924,6 +934,15 @@ cudaError_t launch5b(const Sweep3Params<S> &p, int threads, cudaStream_t st) {
     auto k = sweep5_kernel<S, KU, NT, LGC, LGP, BITS>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
+    // the smallest shared-memory carveout that holds the CTA: the rest of the unified L1
+    // caches state lines (left to the driver, the carveout varied with the block size:
+    // diag-only config 2 ran 1.6e10 against 2.3e10 with pattern blocks)
+    int carve = (int)((smem + 8192) * 100 / (228 * 1024)) + 1;
+    if (const char *ev = std::getenv("MCINV_CARVE")) carve = std::atoi(ev);
+    if (carve >= 0) {
+        e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, carve > 100 ? 100 : carve);
+        if (e != cudaSuccess) return e;
+    }
     k<<<blocks, threads, smem, st>>>(p);
     return cudaGetLastError();
 }

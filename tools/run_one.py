@@ -19,6 +19,7 @@ def main():
     ap.add_argument("--chains", type=int, default=0)
     ap.add_argument("--repeat", type=int, default=1)
     ap.add_argument("--outputs", default="")
+    ap.add_argument("--group-size", type=int, default=0, help="SE group size (default: the config's)")
     ap.add_argument("--noise", default="gauss", choices=["gauss", "z2", "zero"])
     ap.add_argument("--dirac", type=int, default=0, help="free Wilson-Dirac N^4 lattice (trace, Q = I) instead")
     a = ap.parse_args()
@@ -36,7 +37,7 @@ def main():
     inv.set_timing(True)
     for _ in range(a.repeat):
         t = time.perf_counter()
-        inv.run(run.seed, chains, a.burn, a.sweeps - a.burn, outs, group_size=run.group_size, noise=a.noise)
+        inv.run(run.seed, chains, a.burn, a.sweeps - a.burn, outs, group_size=a.group_size or run.group_size, noise=a.noise)
         torch.cuda.synchronize()
         dt = time.perf_counter() - t
         st = inv.stats()
