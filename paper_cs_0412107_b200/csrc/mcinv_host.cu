@@ -856,6 +856,10 @@ mcinv_status run_typed(mcinv_ctx *ctx, const mcinv_run_args *a, const Layout &L,
         q3.slot_diag = p.slot_diag;
         q3.slot_pat = p.slot_pat;
         q3.slot_trace = p.slot_trace;
+        // MCINV_RECONV bits: 1 reconverge the warp at the end of each item (default: diag-only
+        // config 2 1.57 -> 2.79e10), 2 also after the dependency waits (measured -6%)
+        q3.reconv = 1;
+        if (const char *e = std::getenv("MCINV_RECONV")) q3.reconv = std::atoi(e);
         if (sl) {
             q3.slot_rec = (const int4 *)sl->rec.p;
             q3.slot_dsg = (const S *)sl->dsg.p;
@@ -871,10 +875,6 @@ mcinv_status run_typed(mcinv_ctx *ctx, const mcinv_run_args *a, const Layout &L,
             // MCINV_PREFETCH: L2 prefetch of every neighbour's line before the noise (3, default;
             // 220-sweep runs: config 2 2.02 -> 2.06e10, config 3 3.00 -> 3.26e10), upper
             // neighbours only into L2 (2) or L1 (1), none (0) -- profiles/r01_prefetch.log
-            // MCINV_RECONV bits: 1 reconverge the warp at the end of each item (default: diag-only
-            // config 2 1.57 -> 2.79e10), 2 also after the dependency waits (measured -6%)
-            q3.reconv = 1;
-            if (const char *e = std::getenv("MCINV_RECONV")) q3.reconv = std::atoi(e);
             q3.prefetch = 3;
             if (const char *e = std::getenv("MCINV_PREFETCH")) q3.prefetch = std::atoi(e);
         }
