@@ -876,8 +876,11 @@ mcinv_status run_typed(mcinv_ctx *ctx, const mcinv_run_args *a, const Layout &L,
             // 220-sweep runs: config 2 2.02 -> 2.06e10, config 3 3.00 -> 3.26e10), upper
             // neighbours only into L2 (2) or L1 (1), none (0) -- profiles/r01_prefetch.log
             q3.prefetch = 3;
-            if (const char *e = std::getenv("MCINV_PREFETCH")) q3.prefetch = std::atoi(e);
         }
+        // v3 (level kernel): the same prefetch for real C (config 4: 3.82 -> 4.02e10), not for
+        // complex (config 5: 1.36 -> 1.34e10)
+        if (!sl && ctx->dtype == MCINV_F64) q3.prefetch = 3;
+        if (const char *e = std::getenv("MCINV_PREFETCH")) q3.prefetch = std::atoi(e);
     }
     cudaError_t lerr = cudaSuccess;
     auto sweep = [&](int s0, int s1, int snap_s0, unsigned outs) {

@@ -87,6 +87,13 @@ __device__ __forceinline__ T *zrow(T *zcol, int j, uint32_t stride) {
     return reinterpret_cast<T *>(reinterpret_cast<C *>(zcol) + static_cast<uint64_t>(static_cast<uint32_t>(j)) * stride);
 }
 
+__device__ __forceinline__ void prefetch_l1(const void *p) {
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+__device__ __forceinline__ void prefetch_l2(const void *p) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
 // the (a, b) coefficient pair of an entry in one (real) or two (complex) 16-B loads
 __device__ __forceinline__ ZW<double> ldg_ab(const ZW<double> *p) {
     const double2 v = __ldg(reinterpret_cast<const double2 *>(p));
@@ -309,6 +316,8 @@ __global__ void __launch_bounds__(NT, 1) sweep3_kernel(const Sweep3Params<S> p) 
 #pragma unroll
                 for (int h = 0; h < K; ++h) zi[h] = wi[h] = zero_s<S>();
                 if (valid) {
+                    if (p.prefetch == 3)  // the neighbours' state lines into L2 while the noise runs
+                        for (int e = 0; e < cnt; ++e) prefetch_l2(zrow(zcol, __ldg(p.ent_col + beg + e), zst));
                     // noise first: its temporaries are dead before the gathers are in flight
                     double phi[K];
 #pragma unroll
@@ -677,13 +686,6 @@ __device__ __forceinline__ void tma_block(uint32_t dst, const void *src, uint32_
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
                  "l"(src), "r"(bytes), "r"(bar)
                  : "memory");
-}
-
-__device__ __forceinline__ void prefetch_l1(const void *p) {
-    asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
-}
-__device__ __forceinline__ void prefetch_l2(const void *p) {
-    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
 
 // Eq. (4)/(5) fma chains from a staged block (see row_sums): the host padded the row's
