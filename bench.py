@@ -173,17 +173,21 @@ def algorithmic_bytes_per_chain_sweep(c) -> int:
     return e * (2 * off + 2 * c.n)
 
 
-def committed_traffic(workload: str):
-    """DRAM bytes (read + write) per site-update of the sweep kernel, from the
-    committed `ncu --set full` summary (profiles/ncu_summary.json; captured on a
-    shorter launch of the same shape, so it is stored per site-update)."""
+def committed_summary(workload: str) -> dict:
+    """The committed `ncu --set full` summary of the sweep kernel on this workload
+    (profiles/ncu_summary.json; captured on a shorter launch of the same shape, so
+    it is stored per site-update): DRAM bytes and warp instructions per site."""
     path = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(path) as f:
-            d = json.load(f)
-        return d.get(workload, {}).get("dram_bytes_per_site")
+            return json.load(f).get(workload, {})
     except (OSError, ValueError):
-        return None
+        return {}
+
+
+def committed_traffic(workload: str):
+    """DRAM bytes (read + write) per site-update of the sweep kernel (ncu)."""
+    return committed_summary(workload).get("dram_bytes_per_site")
 
 
 # ----------------------------------------------------------------- arms
@@ -295,6 +299,17 @@ def ours_arm(args):
                 "algorithmic_bytes_per_site": b_chain_sweep / c.n,
                 "sweep_ms_per_launch": sweep_launch_ms,
                 "sweep_share_of_step": st["sweep_ms"] / (ms * args.steps)}
+        # second ceiling: instruction issue. ncu's warp instructions per
+        # site-update on this workload x the SMs holding a CTA x 4 issue slots per clock at the
+        # clock measured during the timed region
+        ipc = committed_summary(name).get("warp_inst_per_site")
+        if ipc and clk.get("sm_mhz"):
+            props = torch.cuda.get_device_properties(local)
+            sms = min(props.multi_processor_count, -(-chains // max(1, kinfo["chains_per_warp"])))
+            ceiling = sms * 4 * clk["sm_mhz"] * 1e6 / ipc
+            rate = chains * c.n * sweeps_per_launch / (sweep_launch_ms / 1e3)
+            roof["issue"] = {"warp_inst_per_site": ipc, "sms_used": sms, "ceiling": ceiling, "unit": UNIT,
+                             "frac": rate / ceiling}
 
     if "full" in outputs and st["contract_launches"]:
         # the full-inverse contraction dominates (config 3): FP64 tensor-core (DMMA) bound;

@@ -180,11 +180,14 @@ mcinv_status mcinv_set_timing(mcinv_ctx *ctx, int enable);
 mcinv_status mcinv_stats(mcinv_ctx *ctx, int64_t *launches, double *sweep_ms, int64_t *sweep_launches,
                          double *contract_ms, int64_t *contract_launches);
 
-/* Which sweep kernel the last mcinv_run used: version 3 = level-scheduled
- * kernel (sweep3.cu, the default) with chains_per_warp = chains per CTA and
- * steps_per_sweep = levels D; version 1 = row-by-row kernel (sweep.cu, one
- * thread per chain; the simple reference kernel). MCINV_KERNEL=v1|v3 in the
- * environment forces one. */
+/* Which sweep kernel the last mcinv_run used: 5 = dataflow kernel with
+ * TMA-staged plan blocks (sweep3.cu, the default where it applies), 4 = the
+ * same reading its plan through L1, 3 = level-scheduled kernel (C > 32 chains
+ * per CTA, trace, more than 200k rows), 1 = row-by-row kernel (sweep.cu, one
+ * thread per chain; the simple reference kernel). chains_per_warp = C, the
+ * chains of one CTA (for 4/5 also the lanes of one row within a warp);
+ * steps_per_sweep = levels D of the row DAG. MCINV_KERNEL=v1|v3|v4|v5 in the
+ * environment forces one (MCINV_E_INVALID if it does not apply). */
 mcinv_status mcinv_kernel_info(const mcinv_ctx *ctx, int *version, int *chains_per_warp, int64_t *steps_per_sweep);
 
 /* ------------------------------------------------------------ test-only */

@@ -74,7 +74,9 @@ def main():
                 js = {}
             js[a.workload] = {"dram_bytes_per_site": dram / a.sites, "capture": os.path.basename(a.full),
                               "tag": a.tag, "sites": a.sites,
-                              "duration_ns": num(d.get("gpu__time_duration.sum"))}
+                              "warp_inst_per_site": (inst / a.sites) if inst else None,
+                              "issue_active_pct": num(d.get("smsp__issue_active.avg.pct_of_peak_sustained_active")),
+                              "duration_ms": num(d.get("gpu__time_duration.sum"))}
             json.dump(js, open(path, "w"), indent=1)
         open(os.path.join(prof, f"{a.tag}_ncu_full.txt"), "w").write("\n".join(lines) + "\n")
         print("\n".join(lines))
