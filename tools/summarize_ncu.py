@@ -57,9 +57,9 @@ def main():
         lines.append("warp stall reasons (share of samples):")
         for k, v in sorted(st.items(), key=lambda t: -(t[1] or 0))[:10]:
             lines.append(f"  {100 * (v or 0) / tot:5.1f}%  {k.replace('smsp__pcsamp_warps_issue_stalled_', '')}")
-        dram = (num(d.get("dram__bytes_read.sum")) or 0) + (num(d.get("dram__bytes_write.sum")) or 0)
-        scale = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0}.get(units.get("dram__bytes_read.sum"), 1.0)
-        dram *= scale
+        scale = {"Tbyte": 1e12, "Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0}
+        dram = sum((num(d.get(k)) or 0) * scale.get(units.get(k), 1.0)
+                   for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
         if a.sites:
             lines.append(f"sites (chains x rows x sweeps) in the capture: {a.sites:.6g}")
             lines.append(f"DRAM bytes per site-update: {dram / a.sites:.2f}")
