@@ -782,12 +782,13 @@ mcinv_status run_typed(mcinv_ctx *ctx, const mcinv_run_args *a, const Layout &L,
     int lgK = (lv && ctx->dtype == MCINV_F64 && L.lgC >= 1 && a->group_size >= 2 && !lv->deferred) ? 1 : 0;
     if (const char *e = std::getenv("MCINV_K")) lgK = std::atoi(e) >= 2 ? lgK : 0;
     if (v4) lgK = 0;
-    // threads: v3 enough for the widest phase x C/K (<= 768: 85 registers, measured best
-    // for configs 2-5); dataflow 1024 real / 768 complex (more warps keep more rows in
+    // threads: v3 enough for the widest phase x C/K, at most 1024 (64 registers; measured
+    // over 768 / 85 registers after the round's tuning: config 4 3.97 -> 4.15e10, config 5
+    // 1.38 -> 1.43e10); dataflow 1024 real / 768 complex (more warps keep more rows in
     // flight; measured best for configs 2 / 3), fewer for tiny n; a multiple of 32 and of C/K
     auto threads_for = [&](bool flow) {
         int64_t want = flow ? std::min<int64_t>(ctx->dtype == MCINV_C128 ? 768 : 1024, (int64_t)n << (L.lgC - lgK))
-                            : std::min<int64_t>(768, (int64_t)std::max(lv->max_rows, 1) << (L.lgC - lgK));
+                            : std::min<int64_t>(1024, (int64_t)std::max(lv->max_rows, 1) << (L.lgC - lgK));
         if (const char *e = std::getenv("MCINV_THREADS")) want = std::atoi(e);
         want = std::min<int64_t>(1024, std::max<int64_t>(want, int64_t(1) << (L.lgC - lgK)));
         return (int)((want + 31) / 32 * 32);
