@@ -637,16 +637,28 @@ LevelDev::Slots *get_slots(mcinv_ctx *ctx, LevelDev *lv, int R, int W, bool bloc
     } else if (const char *e = std::getenv("MCINV_SLACK")) {
         order = mcinv::schedule_slots(ctx->n, lv->h_rec, lv->h_ent_col, R, std::atoi(e), blocks ? kBlockEntries : 0);
     } else {
-        // the largest slack (W, W/2, ..., 1 groups) whose schedule pads at most 3% of the
-        // slots: wide DAGs (config 2) take the full slack, narrow ones (lattices) less;
-        // if none does (a DAG narrower than a warp group), the least padded one
-        std::vector<int> best;
+        // the largest slack (W, 3W/4, W/2, 3W/8, ..., 1 groups) whose schedule pads at most
+        // 5% of the slots (MCINV_SLACK_PAD, percent): wide DAGs (config 2: L = 24 of 32,
+        // measured 2.26 -> 2.37e10 over the former 3% rule) take most of the slack, narrow
+        // ones (lattices) less; if none does, the least padded one
+        double pad = 5.0;
+        if (const char *e = std::getenv("MCINV_SLACK_PAD")) pad = std::atof(e);
+        std::vector<int> cand;
         for (int L = W; L >= 1; L /= 2) {
-            order = mcinv::schedule_slots(ctx->n, lv->h_rec, lv->h_ent_col, R, L, blocks ? kBlockEntries : 0);
-            if ((int64_t)order.size() <= ctx->n + ctx->n * 3 / 100) break;
-            if (best.empty() || order.size() < best.size()) best = order;
-            if (L == 1) order = best;
+            cand.push_back(L);
+            if (L >= 4 && (3 * L / 4) < L) cand.push_back(3 * L / 4);
         }
+        std::vector<int> best;
+        bool found = false;
+        for (int L : cand) {
+            order = mcinv::schedule_slots(ctx->n, lv->h_rec, lv->h_ent_col, R, L, blocks ? kBlockEntries : 0);
+            if ((double)order.size() <= (double)ctx->n * (1.0 + pad / 100.0)) {
+                found = true;
+                break;
+            }
+            if (best.empty() || order.size() < best.size()) best = order;
+        }
+        if (!found) order = best;
     }
     for (int o : order) {
         if (o < 0) {
