@@ -615,6 +615,10 @@ LevelDev *get_levels(mcinv_ctx *ctx, unsigned outputs) {
 // v4 slot arrays: level order with every level padded to a multiple of R rows
 // (a warp group of R rows never spans two levels, so its rows are independent)
 constexpr int kBlockEntries = 56;  // v5: entries per warp group (bounds the staged blocks)
+int block_entries() {  // MCINV_BLOCK_ENTRIES overrides (experiments)
+    const char *e = std::getenv("MCINV_BLOCK_ENTRIES");
+    return e ? std::atoi(e) : kBlockEntries;
+}
 constexpr bool kV5Default = true;  // v5 by default where it applies (measured: config 2 +5%, config 3 +24%)
 
 template <typename S>
@@ -635,7 +639,7 @@ LevelDev::Slots *get_slots(mcinv_ctx *ctx, LevelDev *lv, int R, int W, bool bloc
             while (order.size() % R) order.push_back(-1);
         }
     } else if (const char *e = std::getenv("MCINV_SLACK")) {
-        order = mcinv::schedule_slots(ctx->n, lv->h_rec, lv->h_ent_col, R, std::atoi(e), blocks ? kBlockEntries : 0);
+        order = mcinv::schedule_slots(ctx->n, lv->h_rec, lv->h_ent_col, R, std::atoi(e), blocks ? block_entries() : 0);
     } else {
         // the largest slack (W, 3W/4, W/2, 3W/8, ..., 1 groups) whose schedule pads at most
         // 5% of the slots (MCINV_SLACK_PAD, percent): wide DAGs (config 2: L = 24 of 32,
@@ -651,7 +655,7 @@ LevelDev::Slots *get_slots(mcinv_ctx *ctx, LevelDev *lv, int R, int W, bool bloc
         std::vector<int> best;
         bool found = false;
         for (int L : cand) {
-            order = mcinv::schedule_slots(ctx->n, lv->h_rec, lv->h_ent_col, R, L, blocks ? kBlockEntries : 0);
+            order = mcinv::schedule_slots(ctx->n, lv->h_rec, lv->h_ent_col, R, L, blocks ? block_entries() : 0);
             if ((double)order.size() <= (double)ctx->n * (1.0 + pad / 100.0)) {
                 found = true;
                 break;
