@@ -14,6 +14,8 @@
 // with a padded row stride so the m8n8k4 fragment loads (lane -> row = lane/4,
 // k = lane%4) are bank-conflict free; complex values stay interleaved (one
 // 16-B shared load gives both parts of a fragment element).
+#include <cstdlib>
+
 #include "mcinv_internal.cuh"
 #include "scalar.cuh"
 
@@ -48,49 +50,72 @@ template <typename S> struct Tile;
 template <> struct Tile<double> { static constexpr int LD = BM + 4; };  // 8-B elements
 template <> struct Tile<cd> { static constexpr int LD = BM + 2; };      // 16-B elements
 
-template <typename S>
+template <typename S, int NTH>
 __device__ __forceinline__ void stage(S *sm, const S *g, int t0k, int i0, int n, int ld, int gs, int c0, int K,
                                      int tid) {
     // element (k, r) of the chunk = g[((t) * n + i0 + r) * ld + c0 + c], k = t0k + kk, t = k / gs, c = k % gs
     constexpr int LDS = Tile<S>::LD;
-    for (int e = tid; e < KC * BM; e += 128) {
-        const int r = e / KC, kk = e % KC;  // consecutive threads: consecutive chains (contiguous in gmem)
-        const int k = t0k + kk;
-        const bool ok = k < K && i0 + r < n;
-        const int t = ok ? k / gs : 0, c = ok ? k % gs : 0;
+    static_assert(NTH % KC == 0, "a thread keeps its k column");
+    const int kk = tid % KC, r0 = tid / KC;
+    constexpr int RSTEP = NTH / KC;
+    const int k = t0k + kk;
+    if (gs % KC == 0) {
+        // the chunk lies in one snapshot sweep t (KC divides gs): one division per chunk,
+        // then a row stride per element (the staging was integer-bound with a division each)
+        const int t = t0k / gs, c = t0k - t * gs + kk;
+        const S *src = g + ((int64_t)t * n + i0 + r0) * ld + c0 + c;
+        const int64_t step = (int64_t)RSTEP * ld;
+#pragma unroll 4
+        for (int r = r0; r < BM; r += RSTEP, src += step) {
+            const bool ok = i0 + r < n;
+            const S *q = ok ? src : g;
+            if constexpr (ScalarTraits<S>::kDoubles == 2) cp_async(sm + kk * LDS + r, q, ok);
+            else cp_async8(sm + kk * LDS + r, q, ok);
+        }
+        return;
+    }
+    const bool okk = k < K;
+    const int t = okk ? k / gs : 0, c = okk ? k % gs : 0;
+    for (int r = r0; r < BM; r += RSTEP) {
+        const bool ok = okk && i0 + r < n;
         const S *src = g + ((int64_t)t * n + (ok ? i0 + r : 0)) * ld + c0 + c;
         if constexpr (ScalarTraits<S>::kDoubles == 2) cp_async(sm + kk * LDS + r, src, ok);
         else cp_async8(sm + kk * LDS + r, src, ok);
     }
 }
 
-template <typename S, bool CPLX>
-__global__ void __launch_bounds__(128) contract_kernel(const S *__restrict__ x, const S *__restrict__ y,
-                                                      double *__restrict__ acc, int n, int ld, int gs, int T) {
+// WN: output columns per warp (32: 4 warps of 32 x 32; 16: 8 warps of 32 x 16, half the
+// accumulator registers per thread and twice the warps per SM)
+template <typename S, bool CPLX, int WN>
+__global__ void __launch_bounds__(32 * 2 * (BN / WN)) contract_kernel(const S *__restrict__ x, const S *__restrict__ y,
+                                                                    double *__restrict__ acc, int n, int ld, int gs,
+                                                                    int T) {
     constexpr int LDS = Tile<S>::LD;
+    constexpr int NTH = 32 * 2 * (BN / WN);
+    constexpr int NB = WN / 8;  // 8-column tiles per warp
     extern __shared__ __align__(16) unsigned char smem_raw[];
     S *xs = reinterpret_cast<S *>(smem_raw);  // [2][KC][LDS]
     S *ys = xs + 2 * KC * LDS;                // [2][KC][LDS]
     const int g = blockIdx.z;
     const int i0 = blockIdx.y * BM, j0 = blockIdx.x * BN;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+    const int wm = (warp & 1) * 32, wn = (warp >> 1) * WN;
     const int K = T * gs, c0 = g * gs;
-    double cr[4][4][2], ci[4][4][2];
+    double cr[4][NB][2], ci[4][NB][2];
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
-        for (int b = 0; b < 4; ++b) cr[a][b][0] = cr[a][b][1] = ci[a][b][0] = ci[a][b][1] = 0.0;
+        for (int b = 0; b < NB; ++b) cr[a][b][0] = cr[a][b][1] = ci[a][b][0] = ci[a][b][1] = 0.0;
 
     const int nk = (K + KC - 1) / KC;
-    stage<S>(xs, x, 0, i0, n, ld, gs, c0, K, tid);
-    stage<S>(ys, y, 0, j0, n, ld, gs, c0, K, tid);
+    stage<S, NTH>(xs, x, 0, i0, n, ld, gs, c0, K, tid);
+    stage<S, NTH>(ys, y, 0, j0, n, ld, gs, c0, K, tid);
     cp_commit();
     for (int kc = 0; kc < nk; ++kc) {
         const int buf = kc & 1;
         if (kc + 1 < nk) {
-            stage<S>(xs + (buf ^ 1) * KC * LDS, x, (kc + 1) * KC, i0, n, ld, gs, c0, K, tid);
-            stage<S>(ys + (buf ^ 1) * KC * LDS, y, (kc + 1) * KC, j0, n, ld, gs, c0, K, tid);
+            stage<S, NTH>(xs + (buf ^ 1) * KC * LDS, x, (kc + 1) * KC, i0, n, ld, gs, c0, K, tid);
+            stage<S, NTH>(ys + (buf ^ 1) * KC * LDS, y, (kc + 1) * KC, j0, n, ld, gs, c0, K, tid);
         }
         cp_commit();
         cp_wait<1>();
@@ -99,14 +124,12 @@ __global__ void __launch_bounds__(128) contract_kernel(const S *__restrict__ x, 
 #pragma unroll
         for (int ks = 0; ks < KC; ks += 4) {
             const int kk = ks + (lane & 3);
-            S av[4], bv[4];
+            S av[4], bv[NB];
 #pragma unroll
-            for (int a = 0; a < 4; ++a) {
-                av[a] = xb[kk * LDS + wm + a * 8 + (lane >> 2)];
-                bv[a] = yb[kk * LDS + wn + a * 8 + (lane >> 2)];
-            }
-            // four passes over the 16 tiles: consecutive DMMAs never share an accumulator
-            // (15 independent DMMAs between two updates of the same tile)
+            for (int a = 0; a < 4; ++a) av[a] = xb[kk * LDS + wm + a * 8 + (lane >> 2)];
+#pragma unroll
+            for (int b = 0; b < NB; ++b) bv[b] = yb[kk * LDS + wn + b * 8 + (lane >> 2)];
+            // four passes over the 4 x NB tiles: consecutive DMMAs never share an accumulator
             if constexpr (CPLX) {
                 double na[4];
 #pragma unroll
@@ -114,24 +137,24 @@ __global__ void __launch_bounds__(128) contract_kernel(const S *__restrict__ x, 
 #pragma unroll
                 for (int a = 0; a < 4; ++a)
 #pragma unroll
-                    for (int b = 0; b < 4; ++b) dmma(cr[a][b][0], cr[a][b][1], av[a].re, bv[b].re);
+                    for (int b = 0; b < NB; ++b) dmma(cr[a][b][0], cr[a][b][1], av[a].re, bv[b].re);
 #pragma unroll
                 for (int a = 0; a < 4; ++a)
 #pragma unroll
-                    for (int b = 0; b < 4; ++b) dmma(ci[a][b][0], ci[a][b][1], av[a].im, bv[b].re);
+                    for (int b = 0; b < NB; ++b) dmma(ci[a][b][0], ci[a][b][1], av[a].im, bv[b].re);
 #pragma unroll
                 for (int a = 0; a < 4; ++a)
 #pragma unroll
-                    for (int b = 0; b < 4; ++b) dmma(cr[a][b][0], cr[a][b][1], av[a].im, bv[b].im);
+                    for (int b = 0; b < NB; ++b) dmma(cr[a][b][0], cr[a][b][1], av[a].im, bv[b].im);
 #pragma unroll
                 for (int a = 0; a < 4; ++a)
 #pragma unroll
-                    for (int b = 0; b < 4; ++b) dmma(ci[a][b][0], ci[a][b][1], na[a], bv[b].im);
+                    for (int b = 0; b < NB; ++b) dmma(ci[a][b][0], ci[a][b][1], na[a], bv[b].im);
             } else {
 #pragma unroll
                 for (int a = 0; a < 4; ++a)
 #pragma unroll
-                    for (int b = 0; b < 4; ++b) dmma(cr[a][b][0], cr[a][b][1], av[a], bv[b]);
+                    for (int b = 0; b < NB; ++b) dmma(cr[a][b][0], cr[a][b][1], av[a], bv[b]);
             }
         }
         __syncthreads();
@@ -142,7 +165,7 @@ __global__ void __launch_bounds__(128) contract_kernel(const S *__restrict__ x, 
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
-        for (int b = 0; b < 4; ++b) {
+        for (int b = 0; b < NB; ++b) {
             const int i = i0 + wm + a * 8 + (lane >> 2);
             const int j = j0 + wn + b * 8 + (lane & 3) * 2;
             if (i >= n) continue;
@@ -181,9 +204,18 @@ void launch_contract(const S *x, const S *y, double *acc, int n, int ld, int cha
     const int G = chains / gs;
     dim3 grid((n + BN - 1) / BN, (n + BM - 1) / BM, G);
     const size_t smem = 2 * 2 * KC * Tile<S>::LD * sizeof(S);
-    auto k = contract_kernel<S, ScalarTraits<S>::kDoubles == 2>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k<<<grid, 128, smem, st>>>(x, y, acc, n, ld, gs, T);
+    constexpr bool kC = ScalarTraits<S>::kDoubles == 2;
+    // MCINV_CONTRACT_WN: output columns per warp (32: 4 warps per CTA, 16: 8 warps)
+    const char *e = std::getenv("MCINV_CONTRACT_WN");
+    if (e && std::atoi(e) == 16) {
+        auto k = contract_kernel<S, kC, 16>;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k<<<grid, 256, smem, st>>>(x, y, acc, n, ld, gs, T);
+    } else {
+        auto k = contract_kernel<S, kC, 32>;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k<<<grid, 128, smem, st>>>(x, y, acc, n, ld, gs, T);
+    }
 }
 
 template void launch_contract<double>(const double *, const double *, double *, int, int, int, int, int,
