@@ -181,7 +181,7 @@ mcinv_status mcinv_stats(mcinv_ctx *ctx, int64_t *launches, double *sweep_ms, in
                          double *contract_ms, int64_t *contract_launches);
 
 /* Which sweep kernel the last mcinv_run used: 5 = dataflow kernel with
- * TMA-staged plan blocks (sweep3.cu, the default where it applies), 4 = the
+ * TMA-staged plan blocks (sweep5.cu, the default where it applies), 4 = the
  * same reading its plan through L1, 3 = level-scheduled kernel (C > 32 chains
  * per CTA, trace, more than 200k rows), 1 = row-by-row kernel (sweep.cu, one
  * thread per chain; the simple reference kernel). chains_per_warp = C, the

@@ -1,6 +1,6 @@
 """Build libmcinv.so (the C-ABI library) in-tree with nvcc for sm_100a.
 
-The library is the product: kernels (sweep3.cu, sweep.cu, contract.cu, reduce.cu) and
+The library is the product: kernels (sweep3.cu, sweep5.cu, sweep.cu, contract.cu, reduce.cu) and
 the C ABI / host preprocessing (mcinv_host.cu). ``--fmad=false`` so that
 only explicit fma() calls fuse (reading R10); cudart is linked
 statically so the library does not depend on the CUDA runtime torch ships.
@@ -15,8 +15,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libmcinv.so")
-SOURCES = ["mcinv_host.cu", "levels.cu", "sweep.cu", "sweep3.cu", "contract.cu", "reduce.cu"]
-HEADERS = ["mcinv_internal.cuh", "noise.cuh", "scalar.cuh", "levels.h"]
+SOURCES = ["mcinv_host.cu", "levels.cu", "sweep.cu", "sweep3.cu", "sweep5.cu", "contract.cu", "reduce.cu"]
+HEADERS = ["mcinv_internal.cuh", "noise.cuh", "scalar.cuh", "levels.h", "sweep_common.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "--fmad=false", "-Xcompiler", "-fPIC,-O2",
