@@ -576,3 +576,18 @@ def test_dataflow_long_dependency_chain(mc, orc, monkeypatch, kernel):
         monkeypatch.setenv("MCINV_THREADS", th)
         compare_run(mc, orc, c, seed=12, chains=64, burn_in=7, cycles=13, outputs=("diag", "pattern"),
                     group_size=8)
+
+
+@pytest.mark.parametrize("wn", ["32", "16"])
+def test_contraction_tiles_and_staging(mc, orc, monkeypatch, wn):
+    """K3 with both warp tilings (MCINV_CONTRACT_WN) and both staging paths: a
+    group size that 16 divides (one snapshot sweep per k-chunk) and one that it
+    does not (per-element k / gs), complex and real, ragged n (not a multiple
+    of the 64-wide CTA tile)."""
+    monkeypatch.setenv("MCINV_CONTRACT_WN", wn)
+    c = W.lattice(5, 3, 0.15, seed=31)  # n = 125: two ragged tiles per dimension
+    for gs in (16, 8):
+        compare_run(mc, orc, c, seed=9, chains=64, burn_in=2, cycles=5, outputs=("full",), group_size=gs,
+                    snapshot_sweeps=3)
+    compare_run(mc, orc, W.pedigree(90, seed=32), seed=10, chains=48, burn_in=1, cycles=4, outputs=("full",),
+                group_size=48 // 3, snapshot_sweeps=2)
