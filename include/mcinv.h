@@ -160,7 +160,9 @@ mcinv_status mcinv_accumulators(mcinv_ctx *ctx, double **dev_ptr, size_t *count)
  * capacity is in doubles. on_device != 0: both are device pointers, written
  * asynchronously on the run's stream; otherwise host pointers and the call
  * synchronizes. Returns E_DIVERGED if any chain diverged, E_BUFFER (required
- * capacity via mcinv_error_detail's index) if capacity is too small. */
+ * capacity via mcinv_error_detail's index) if capacity is too small, E_STATE
+ * if no sampling sweep has run since the last fresh run (cycles = 0: a
+ * burn-in-only run, to be continued with resume = 1). */
 mcinv_status mcinv_result(mcinv_ctx *ctx, unsigned output, int64_t total_chains,
                           double *estimate, double *std_error, size_t capacity, int on_device);
 

@@ -1110,6 +1110,8 @@ mcinv_status mcinv_result(mcinv_ctx *ctx, unsigned output, int64_t total_chains,
         return fail(ctx, MCINV_E_INVALID, "output not computed by the last run");
     if (total_chains < a.chains || total_chains % a.group_size)
         return fail(ctx, MCINV_E_INVALID, "total_chains");
+    if (ctx->acc_cycles < 1)  // burn-in only so far: Eq. (1/C) has no samples to average
+        return fail(ctx, MCINV_E_STATE, "no sampling sweeps since the last fresh run (cycles = 0)");
     CK(cudaSetDevice(ctx->device));
     const int64_t n = ctx->n;
     int64_t count = 0;

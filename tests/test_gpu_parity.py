@@ -182,6 +182,22 @@ def test_edge_cases(mc, orc):
     # diagonal complex with the branch cut
     compare_run(mc, orc, W.diagonal(np.array([-2.0 + 0j, 1j, 3.0, -1 - 1e-3j])), seed=2, chains=33 * 1,
                 burn_in=0, cycles=4, outputs=("diag",), group_size=1)
+    # burn-in only (cycles = 0): no estimate yet (E_STATE); resuming with cycles gives the
+    # same result as one run with the burn-in and the cycles (exact resume)
+    c2 = W.pedigree(200, seed=4)
+    inv = mc.Inverter(c2)
+    inv.run(5, 64, 3, 0, ("diag",), group_size=8)
+    with pytest.raises(mc.MCInvError) as e:
+        inv.result("diag")
+    assert e.value.code == 8
+    inv.run(5, 64, 0, 4, ("diag",), group_size=8, sweep_begin=3, resume=True)
+    e1, _ = inv.result("diag")
+    inv.close()
+    one = mc.Inverter(c2)
+    one.run(5, 64, 3, 4, ("diag",), group_size=8)
+    e2, _ = one.result("diag")
+    one.close()
+    np.testing.assert_allclose(e1, e2, rtol=1e-12, atol=0)  # atomics: summation order may differ
     # empty pattern list
     c = W.random_dense(8, seed=3)
     inv = mc.Inverter(c, pattern=(np.zeros(0, np.int32), np.zeros(0, np.int32)))
