@@ -109,6 +109,8 @@ struct mcinv_ctx {
     std::vector<std::complex<double>> h_q_val;
     std::map<unsigned, std::unique_ptr<LevelDev>> levels;                 // outputs -> level schedule
     int nsm = 148;
+    int64_t l2_bytes = 126 << 20;  // device L2 (queried at create)
+    mutable int depth = -1;        // levels D of the row DAG (cached by level_depth)
     int last_kernel = 0;  // 1 = v1 (row by row), 3 = v3 (level schedule), 4 = v4 (dataflow)
     DevBuf err_flag;      // v4 watchdog flag (device unsigned)
     int last_C = 0;
@@ -453,10 +455,40 @@ int ilog2(int64_t x) {
 
 // v3: C = chains per CTA, the smallest power of two that fits the chains in
 // one wave of CTAs (one per SM), at most 1024 (MCINV_C overrides)
+// levels D of the lower-neighbour DAG (lev(i) = 1 + max lev of the lower neighbours), from the
+// union adjacency; structure only, cached
+int level_depth(const mcinv_ctx *ctx) {
+    if (ctx->depth >= 0) return ctx->depth;
+    std::vector<int> lev(ctx->n, 0);
+    int D = 0;
+    for (int64_t i = 0; i < ctx->n; ++i) {
+        int l = 0;
+        for (int q = ctx->h_u_ptr[i]; q < ctx->h_u_ptr[i + 1]; ++q)
+            if (ctx->h_u_col[q] < i) l = std::max(l, lev[ctx->h_u_col[q]] + 1);
+        lev[i] = l;
+        D = std::max(D, l + 1);
+    }
+    ctx->depth = D;
+    return D;
+}
+
+// chains per CTA: the smallest power of two that fits every chain in one wave of CTAs; for
+// the level kernel (C > 32) rather the largest C from there down to 16 whose wave of CTAs
+// keeps one level's state (rows per level x chains of the wave x sizeof(ZW)) in 3/4 of L2:
+// the CTAs then run in several waves (each all sweeps of its chains) and the neighbours'
+// lines of the previous levels hit L2 (config 5: C = 128 -> 16, 1.43 -> 1.62e10
+// site-updates/s; config 4's levels are too wide for any C and keep C = 64)
 int choose_lgC(const mcinv_ctx *ctx, int64_t chains) {
     if (const char *e = std::getenv("MCINV_C")) return ilog2(std::max(1, std::atoi(e)));
     int lg = 0;
     while (lg < 10 && ((chains + (int64_t(1) << lg) - 1) >> lg) > ctx->nsm) ++lg;
+    if (lg <= 5 || std::getenv("MCINV_NO_L2_BLOCKING")) return lg;
+    const double rows = (double)ctx->n / std::max(1, level_depth(ctx));
+    const double zw = ctx->dtype == MCINV_C128 ? 32.0 : 16.0;
+    for (int c = lg; c >= 4; --c) {
+        const double wave_chains = std::min<double>((double)chains, (double)ctx->nsm * (double)(int64_t(1) << c));
+        if (rows * wave_chains * zw <= 0.75 * (double)ctx->l2_bytes) return c;
+    }
     return lg;
 }
 
@@ -1004,6 +1036,10 @@ mcinv_status mcinv_create(mcinv_ctx **out, int device, mcinv_dtype dtype, int64_
     if (n < 1 || n >= (int64_t(1) << 31)) return fail(ctx, MCINV_E_INVALID, "n out of range");
     CK(cudaSetDevice(device));
     CK(cudaDeviceGetAttribute(&ctx->nsm, cudaDevAttrMultiProcessorCount, device));
+    {
+        int l2 = 0;
+        if (cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, device) == cudaSuccess && l2 > 0) ctx->l2_bytes = l2;
+    }
     {
         cudaMemPool_t pool;
         uint64_t keep = UINT64_MAX;  // freed blocks stay in the pool: no release to the OS
