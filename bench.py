@@ -136,8 +136,15 @@ def oracle_sample(cfgk: int, target_s: float):
         res = pool.map(_oracle_worker, jobs)
     sites = sum(r[0] for r in res)
     wall = max(r[1] for r in res)
+    model = "?"
+    try:
+        with open("/proc/cpuinfo") as f:
+            model = next(l.split(":", 1)[1].strip() for l in f if l.startswith("model name"))
+    except (OSError, StopIteration):
+        pass
     desc = (f"{W.CONFIGS[cfgk]['name']}: {cores} processes x 1 chain x {burn}+{cyc} sweeps at full n={c.n} "
-            f"({sites:.3g} site-updates, outputs {','.join(run.outputs)} minus full when n>256)")
+            f"({sites:.3g} site-updates, outputs {','.join(run.outputs)} minus full when n>256) on {model}; "
+            f"single process {pilot_s / pilot_t:.3g} site-updates/s")
     return sites / wall, cores, desc
 
 
