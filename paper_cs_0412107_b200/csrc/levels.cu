@@ -6,6 +6,8 @@
 
 #include "levels.h"
 
+#include <cstdlib>
+
 namespace mcinv {
 
 namespace {
@@ -199,6 +201,8 @@ std::vector<int> schedule_slots(int64_t n, const std::vector<int4> &rec, const s
         if (pending[o] == 0) waiting.push(Key(0, -height[o], (int)o));
     std::vector<int> slots;
     slots.reserve(n + n / 4);
+    const char *se = std::getenv("MCINV_SIMILAR");  // window (0: plain height order)
+    const int similar = se ? std::atoi(se) : 32;
     int64_t placed = 0;
     for (int G = 0; placed < n; ++G) {
         while (!waiting.empty() && std::get<0>(waiting.top()) <= G) {
@@ -209,7 +213,32 @@ std::vector<int> schedule_slots(int64_t n, const std::vector<int4> &rec, const s
         std::vector<int> now;
         while (taken < R) {
             int o;
-            if (!ready.empty()) {
+            if (!ready.empty() && similar > 0 && taken > 0) {
+                // among the next `similar` ready rows (by height) take the one whose entry and
+                // lower-neighbour counts are closest to the group's first row: the R rows of a
+                // warp item then run their waits and gather loops with less divergence
+                // (config 2 2.36 -> 2.43e10 with a window of 32; config 3 unchanged)
+                std::vector<std::pair<int, int>> cand;
+                while (!ready.empty() && (int)cand.size() < similar) {
+                    cand.push_back(ready.top());
+                    ready.pop();
+                }
+                const int o0 = now[0];
+                int best = 0;
+                auto dist = [&](int x) {
+                    return std::abs((rec[x].z & 0xffff) - (rec[o0].z & 0xffff)) +
+                           std::abs((rec[x].z >> 16) - (rec[o0].z >> 16));
+                };
+                for (int q = 1; q < (int)cand.size(); ++q)
+                    if (dist(-cand[q].second) < dist(-cand[best].second)) best = q;
+                o = -cand[best].second;
+                for (int q = 0; q < (int)cand.size(); ++q)
+                    if (q != best) ready.push(cand[q]);
+                if (ecap > 0 && ents + (rec[o].z & 0xffff) > ecap) {
+                    ready.push(cand[best]);
+                    break;
+                }
+            } else if (!ready.empty()) {
                 o = -ready.top().second;
                 if (ecap > 0 && taken > 0 && ents + (rec[o].z & 0xffff) > ecap) break;  // block size cap
                 ready.pop();
