@@ -289,6 +289,7 @@ __global__ void __launch_bounds__(NT, 1) sweep4_kernel(const Sweep3Params<S> p) 
                 accumulate_row<S, P, V, K>(p, zcol, rec, zi, wi, acc, lane, gleader, towner, sd, sp, want_diag,
                                            want_pat);
             }
+            if (p.reconv & 1) __syncwarp();  // reconverge before the next item (see v5)
         }
         __syncthreads();  // sweep boundary: all reads of sweep s values are done
     }
