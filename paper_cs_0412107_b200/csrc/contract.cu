@@ -86,7 +86,10 @@ __device__ __forceinline__ void stage(S *sm, const S *g, int t0k, int i0, int n,
 
 // WN: output columns per warp (32: 4 warps of 32 x 32; 16: 8 warps of 32 x 16, half the
 // accumulator registers per thread and twice the warps per SM)
-template <typename S, bool CPLX, int WN>
+// M3 (complex only): the 3-multiplication form of x conj(y) -- P1 = xr yr, P2 = xi yi,
+// P3 = (xr + xi)(yr - yi); Re = P1 + P2, Im = P3 - P1 + P2 -- three real DMMA products per
+// complex one instead of four (the DMMA pipe is the bound)
+template <typename S, bool CPLX, int WN, bool M3>
 __global__ void __launch_bounds__(32 * 2 * (BN / WN)) contract_kernel(const S *__restrict__ x, const S *__restrict__ y,
                                                                     double *__restrict__ acc, int n, int ld, int gs,
                                                                     int T) {
@@ -102,10 +105,16 @@ __global__ void __launch_bounds__(32 * 2 * (BN / WN)) contract_kernel(const S *_
     const int wm = (warp & 1) * 32, wn = (warp >> 1) * WN;
     const int K = T * gs, c0 = g * gs;
     double cr[4][NB][2], ci[4][NB][2];
+    constexpr int A3 = M3 ? 4 : 1, B3 = M3 ? NB : 1;
+    double c3[A3][B3][2];
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
         for (int b = 0; b < NB; ++b) cr[a][b][0] = cr[a][b][1] = ci[a][b][0] = ci[a][b][1] = 0.0;
+#pragma unroll
+    for (int a = 0; a < A3; ++a)
+#pragma unroll
+        for (int b = 0; b < B3; ++b) c3[a][b][0] = c3[a][b][1] = 0.0;
 
     const int nk = (K + KC - 1) / KC;
     stage<S, NTH>(xs, x, 0, i0, n, ld, gs, c0, K, tid);
@@ -130,7 +139,25 @@ __global__ void __launch_bounds__(32 * 2 * (BN / WN)) contract_kernel(const S *_
 #pragma unroll
             for (int b = 0; b < NB; ++b) bv[b] = yb[kk * LDS + wn + b * 8 + (lane >> 2)];
             // four passes over the 4 x NB tiles: consecutive DMMAs never share an accumulator
-            if constexpr (CPLX) {
+            if constexpr (CPLX && M3) {
+                double sa[4], db[NB];
+#pragma unroll
+                for (int a = 0; a < 4; ++a) sa[a] = av[a].re + av[a].im;
+#pragma unroll
+                for (int b = 0; b < NB; ++b) db[b] = bv[b].re - bv[b].im;
+#pragma unroll
+                for (int a = 0; a < 4; ++a)
+#pragma unroll
+                    for (int b = 0; b < NB; ++b) dmma(cr[a][b][0], cr[a][b][1], av[a].re, bv[b].re);
+#pragma unroll
+                for (int a = 0; a < 4; ++a)
+#pragma unroll
+                    for (int b = 0; b < NB; ++b) dmma(ci[a][b][0], ci[a][b][1], av[a].im, bv[b].im);
+#pragma unroll
+                for (int a = 0; a < A3; ++a)
+#pragma unroll
+                    for (int b = 0; b < B3; ++b) dmma(c3[a][b][0], c3[a][b][1], sa[a], db[b]);
+            } else if constexpr (CPLX) {
                 double na[4];
 #pragma unroll
                 for (int a = 0; a < 4; ++a) na[a] = -av[a].re;
@@ -158,6 +185,18 @@ __global__ void __launch_bounds__(32 * 2 * (BN / WN)) contract_kernel(const S *_
             }
         }
         __syncthreads();
+    }
+    if constexpr (M3) {  // Re = P1 + P2, Im = P3 - P1 + P2
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < NB; ++b)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const double p1 = cr[a][b][h], p2 = ci[a][b][h];
+                    cr[a][b][h] = p1 + p2;
+                    ci[a][b][h] = c3[a < A3 ? a : 0][b < B3 ? b : 0][h] - p1 + p2;
+                }
     }
     // accumulate into A_g (layout [G][n][n] x e doubles): each lane owns 2 adjacent columns
     const int e = CPLX ? 2 : 1;
@@ -207,12 +246,19 @@ void launch_contract(const S *x, const S *y, double *acc, int n, int ld, int cha
     constexpr bool kC = ScalarTraits<S>::kDoubles == 2;
     // MCINV_CONTRACT_WN: output columns per warp (32: 4 warps per CTA, 16: 8 warps)
     const char *e = std::getenv("MCINV_CONTRACT_WN");
-    if (e && std::atoi(e) == 16) {
-        auto k = contract_kernel<S, kC, 16>;
+    const char *m3 = std::getenv("MCINV_CONTRACT_3M");
+    // complex: the 3-multiplication form by default (config 3: 34.2 -> 39.5 algorithmic FP64
+    // TFLOP/s, i.e. 8 n^2 flops per chain-sweep counted; MCINV_CONTRACT_3M=0 for 4 products)
+    if (kC && !(m3 && std::atoi(m3) == 0)) {  // 3 products per complex MAC, 8 warps of 32 x 16
+        auto k = contract_kernel<S, kC, 16, kC>;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k<<<grid, 256, smem, st>>>(x, y, acc, n, ld, gs, T);
+    } else if (e && std::atoi(e) == 16) {
+        auto k = contract_kernel<S, kC, 16, false>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         k<<<grid, 256, smem, st>>>(x, y, acc, n, ld, gs, T);
     } else {
-        auto k = contract_kernel<S, kC, 32>;
+        auto k = contract_kernel<S, kC, 32, false>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         k<<<grid, 128, smem, st>>>(x, y, acc, n, ld, gs, T);
     }

@@ -594,13 +594,15 @@ def test_dataflow_long_dependency_chain(mc, orc, monkeypatch, kernel):
                     group_size=8)
 
 
-@pytest.mark.parametrize("wn", ["32", "16"])
-def test_contraction_tiles_and_staging(mc, orc, monkeypatch, wn):
-    """K3 with both warp tilings (MCINV_CONTRACT_WN) and both staging paths: a
-    group size that 16 divides (one snapshot sweep per k-chunk) and one that it
-    does not (per-element k / gs), complex and real, ragged n (not a multiple
-    of the 64-wide CTA tile)."""
+@pytest.mark.parametrize("wn,m3", [("32", "0"), ("16", "0"), ("32", "1")])
+def test_contraction_tiles_and_staging(mc, orc, monkeypatch, wn, m3):
+    """K3 with both warp tilings (MCINV_CONTRACT_WN), the complex product with
+    four real products or in the 3-multiplication form (MCINV_CONTRACT_3M, the
+    default), and both staging paths: a group size that 16 divides (one
+    snapshot sweep per k-chunk) and one that it does not (per-element k / gs),
+    complex and real, ragged n (not a multiple of the 64-wide CTA tile)."""
     monkeypatch.setenv("MCINV_CONTRACT_WN", wn)
+    monkeypatch.setenv("MCINV_CONTRACT_3M", m3)
     c = W.lattice(5, 3, 0.15, seed=31)  # n = 125: two ragged tiles per dimension
     for gs in (16, 8):
         compare_run(mc, orc, c, seed=9, chains=64, burn_in=2, cycles=5, outputs=("full",), group_size=gs,
