@@ -174,7 +174,7 @@ std::string build_levels(const LevelInput &in, LevelPlan &P) {
 }
 
 std::vector<int> schedule_slots(int64_t n, const std::vector<int4> &rec, const std::vector<int> &ent_col, int R,
-                                int L, int ecap) {
+                                int L, int ecap, int similar) {
     // row i -> level-order index o; lower neighbours (the first nlow entries) and the
     // reverse edges (upper neighbours)
     std::vector<int> ord_of(n);
@@ -201,8 +201,6 @@ std::vector<int> schedule_slots(int64_t n, const std::vector<int4> &rec, const s
         if (pending[o] == 0) waiting.push(Key(0, -height[o], (int)o));
     std::vector<int> slots;
     slots.reserve(n + n / 4);
-    const char *se = std::getenv("MCINV_SIMILAR");  // window (0: plain height order)
-    const int similar = se ? std::atoi(se) : 32;
     int64_t placed = 0;
     for (int G = 0; placed < n; ++G) {
         while (!waiting.empty() && std::get<0>(waiting.top()) <= G) {
@@ -218,19 +216,25 @@ std::vector<int> schedule_slots(int64_t n, const std::vector<int4> &rec, const s
                 // lower-neighbour counts are closest to the group's first row: the R rows of a
                 // warp item then run their waits and gather loops with less divergence
                 // (config 2 2.36 -> 2.43e10 with a window of 32; config 3 unchanged)
-                std::vector<std::pair<int, int>> cand;
-                while (!ready.empty() && (int)cand.size() < similar) {
-                    cand.push_back(ready.top());
-                    ready.pop();
-                }
                 const int o0 = now[0];
-                int best = 0;
                 auto dist = [&](int x) {
                     return std::abs((rec[x].z & 0xffff) - (rec[o0].z & 0xffff)) +
                            std::abs((rec[x].z >> 16) - (rec[o0].z >> 16));
                 };
-                for (int q = 1; q < (int)cand.size(); ++q)
-                    if (dist(-cand[q].second) < dist(-cand[best].second)) best = q;
+                // candidates in height order; stop at the first exact match (the same choice as
+                // scanning the whole window: the first of the minimal distance)
+                std::vector<std::pair<int, int>> cand;
+                int best = 0, bestd = 1 << 30;
+                while (!ready.empty() && (int)cand.size() < similar) {
+                    cand.push_back(ready.top());
+                    ready.pop();
+                    const int d = dist(-cand.back().second);
+                    if (d < bestd) {
+                        bestd = d;
+                        best = (int)cand.size() - 1;
+                        if (d == 0) break;
+                    }
+                }
                 o = -cand[best].second;
                 for (int q = 0; q < (int)cand.size(); ++q)
                     if (q != best) ready.push(cand[q]);

@@ -77,7 +77,10 @@ std::string build_levels(const LevelInput &in, LevelPlan &out);
 // Output: slot -> level-order index (or -1 for padding); size a multiple of R.
 // ecap > 0: a group takes no further row once its entries would exceed ecap (a
 // single row may exceed it alone): bounds the group blocks staged by v5.
+// similar > 0: a group's rows after the first are chosen among the next `similar`
+// ready rows (by height) as the first whose entry and lower-neighbour counts are
+// closest to the first row's (less divergence among a warp's rows).
 std::vector<int> schedule_slots(int64_t n, const std::vector<int4> &rec, const std::vector<int> &ent_col, int R,
-                                int L, int ecap = 0);
+                                int L, int ecap = 0, int similar = 0);
 
 }  // namespace mcinv

@@ -664,6 +664,9 @@ LevelDev::Slots *get_slots(mcinv_ctx *ctx, LevelDev *lv, int R, int W, bool bloc
     // slot order: the list schedule (levels.h schedule_slots) with a slack of L = W groups
     // (the warps of a CTA); MCINV_SLOT_ORDER=level keeps plain level order (each level padded)
     const char *so = std::getenv("MCINV_SLOT_ORDER");
+    // similarity window of the list schedule (levels.h): 32 measured best on config 2 (+3%)
+    const char *se = std::getenv("MCINV_SIMILAR");
+    const int sim = se ? std::atoi(se) : 32;
     std::vector<int> order;
     if (so && !std::strcmp(so, "level")) {
         for (int l = 0; l < lv->D; ++l) {
@@ -671,7 +674,8 @@ LevelDev::Slots *get_slots(mcinv_ctx *ctx, LevelDev *lv, int R, int W, bool bloc
             while (order.size() % R) order.push_back(-1);
         }
     } else if (const char *e = std::getenv("MCINV_SLACK")) {
-        order = mcinv::schedule_slots(ctx->n, lv->h_rec, lv->h_ent_col, R, std::atoi(e), blocks ? block_entries() : 0);
+        order = mcinv::schedule_slots(ctx->n, lv->h_rec, lv->h_ent_col, R, std::atoi(e), blocks ? block_entries() : 0,
+                                      sim);
     } else {
         // the largest slack (W, 3W/4, W/2, 3W/8, ..., 1 groups) whose schedule pads at most
         // 5% of the slots (MCINV_SLACK_PAD, percent): wide DAGs (config 2: L = 24 of 32,
@@ -684,17 +688,26 @@ LevelDev::Slots *get_slots(mcinv_ctx *ctx, LevelDev *lv, int R, int W, bool bloc
             cand.push_back(L);
             if (L >= 4 && (3 * L / 4) < L) cand.push_back(3 * L / 4);
         }
-        std::vector<int> best;
+        // (the slack is chosen on schedules without the similarity window -- cheap -- and the
+        // final order is then built once with it)
+        int chosen = 1;
+        size_t best_size = 0;
         bool found = false;
         for (int L : cand) {
-            order = mcinv::schedule_slots(ctx->n, lv->h_rec, lv->h_ent_col, R, L, blocks ? block_entries() : 0);
-            if ((double)order.size() <= (double)ctx->n * (1.0 + pad / 100.0)) {
+            const std::vector<int> o = mcinv::schedule_slots(ctx->n, lv->h_rec, lv->h_ent_col, R, L,
+                                                             blocks ? block_entries() : 0, 0);
+            if ((double)o.size() <= (double)ctx->n * (1.0 + pad / 100.0)) {
+                chosen = L;
                 found = true;
                 break;
             }
-            if (best.empty() || order.size() < best.size()) best = order;
+            if (best_size == 0 || o.size() < best_size) {
+                best_size = o.size();
+                chosen = L;
+            }
         }
-        if (!found) order = best;
+        (void)found;
+        order = mcinv::schedule_slots(ctx->n, lv->h_rec, lv->h_ent_col, R, chosen, blocks ? block_entries() : 0, sim);
     }
     for (int o : order) {
         if (o < 0) {
@@ -1411,7 +1424,8 @@ mcinv_status mcinv_debug_levels(mcinv_dtype dtype, int64_t n, const int64_t *row
             while (nlow < cnt && P.ent_col[beg + nlow] < i) ++nlow;
             rec[o] = make_int4(i, beg, cnt | nlow << 16, -1);
         }
-        const std::vector<int> order = mcinv::schedule_slots(n, rec, P.ent_col, slot_R, slot_L);
+        const char *se = std::getenv("MCINV_SIMILAR");
+        const std::vector<int> order = mcinv::schedule_slots(n, rec, P.ent_col, slot_R, slot_L, 0, se ? std::atoi(se) : 32);
         if ((int64_t)order.size() > slots_capacity) return fail(ctx, MCINV_E_BUFFER, "slots", (int64_t)order.size());
         for (size_t t = 0; t < order.size(); ++t) info_slots[t] = order[t] < 0 ? -1 : P.ord_row[order[t]];
         info[6] = (int64_t)order.size();
