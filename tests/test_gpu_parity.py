@@ -609,3 +609,23 @@ def test_contraction_tiles_and_staging(mc, orc, monkeypatch, wn, m3):
                     snapshot_sweeps=3)
     compare_run(mc, orc, W.pedigree(90, seed=32), seed=10, chains=48, burn_in=1, cycles=4, outputs=("full",),
                 group_size=48 // 3, snapshot_sweeps=2)
+
+
+@pytest.mark.parametrize("k", [2, 5])
+def test_level2_states_after_sweeps_1_2_and_N_plus_1(mc, orc, k):
+    """SURVEY c2 level 2 at full n: z, w after sweeps 1, 2 and N+1 of a chain
+    subset (global chain indices 0..7 of the config's run, so the same
+    trajectories as the full run), GPU (resumed launches) vs the oracle's
+    snapshots of one run, within 1e-12 normwise."""
+    c, q, run = W.config(k)
+    N, s = run.burn_in, 8
+    # snap_sweeps are 0-based: the state after sweep s completes (s = 0: one sweep done)
+    r = orc.Matrix(c, q=q).run(run.seed, s, N + 1, 0, (), snap_sweeps=(0, 1, N))
+    inv = mc.Inverter(c, q=q)
+    done = 0
+    for idx, upto in enumerate((1, 2, N + 1)):
+        inv.run(run.seed, s, upto - done, 0, (), group_size=1, sweep_begin=done, resume=done > 0)
+        done = upto
+        zg, wg = inv.get_state(0, s)
+        states_match(zg, wg, r["z_snap"][idx], r["w_snap"][idx])
+    inv.close()
