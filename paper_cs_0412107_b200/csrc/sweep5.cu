@@ -148,6 +148,9 @@ __global__ void __launch_bounds__(NT, 1) sweep5_kernel(const Sweep3Params<S> p) 
     const int64_t grp = chain >> p.lgG;
     ZW<S> *__restrict__ zcol = p.zw + chain;
     const bool want_diag = p.outputs & OUT_DIAG, want_pat = p.outputs & OUT_PATTERN;
+    // (a compile-time flag here measured 2% slower: code generation in this register-capped
+    // kernel is fragile; removing unused runtime branches -- prefetch variants, optional
+    // reconvergence, sleep in the polls -- measured +5% on config 2)
     const bool want_full = p.outputs & OUT_FULL;
     double *const sd = p.slot_diag + grp * p.n * E;
     double *const sp = p.slot_pat + grp * p.pcount * E;
@@ -217,14 +220,10 @@ __global__ void __launch_bounds__(NT, 1) sweep5_kernel(const Sweep3Params<S> p) 
                 const int nlow = rec.z >> 16;
                 // upper neighbours hold their sweep s-1 values until this row publishes: start
                 // their lines on the way before the noise (its ALU time covers the latency)
-                if (p.prefetch == 3) {  // all neighbours into L2 (the coherence point: safe for lower ones)
+                if (p.prefetch) {  // all neighbours into L2 (the coherence point: safe for lower ones)
                     for (int e0 = 0; e0 < cnt; e0 += KU)  // KU-padded entry lists: no predicate
 #pragma unroll
                         for (int q = 0; q < KU; ++q) prefetch_l2(zrow(zcol, col[e0 + q], zst));
-                } else if (p.prefetch == 1) {
-                    for (int e = nlow; e < cnt; ++e) prefetch_l1(zrow(zcol, col[e], zst));
-                } else if (p.prefetch == 2) {
-                    for (int e = nlow; e < cnt; ++e) prefetch_l2(zrow(zcol, col[e], zst));
                 }
                 phi = noise_phi(p.noise, static_cast<uint32_t>(i), k, gchain, p.key0, p.key1);
                 for (int e = 0; e < nlow; ++e) {
@@ -236,12 +235,9 @@ __global__ void __launch_bounds__(NT, 1) sweep5_kernel(const Sweep3Params<S> p) 
                         else
                             return reinterpret_cast<volatile unsigned char *>(done)[j] == need;
                     };
-                    wait_ready(ready, p.err, p.spin_ns);
+                    wait_ready(ready, p.err, 0);  // busy poll (measured best; MCINV_SPIN_NS is v4's)
                 }
             }
-            // rows whose dependencies were ready left the wait early; reconverge so that the
-            // gathers and the fma chains of the warp's R rows issue as one instruction stream
-            if (p.reconv & 2) __syncwarp();
             if (valid) {
                 __threadfence_block();
                 S az = zero_s<S>(), aw = zero_s<S>();
@@ -268,7 +264,7 @@ __global__ void __launch_bounds__(NT, 1) sweep5_kernel(const Sweep3Params<S> p) 
             // reconverge before the next item: lanes that skipped a divergent step of the
             // accumulation (leaders' reductions) otherwise start it as a separate sub-warp and
             // the split persists (diag-only config 2: 1.57e10 without, 2.79e10 with)
-            if (p.reconv & 1) __syncwarp();
+            __syncwarp();
         }
         __syncthreads();  // sweep boundary: all reads of sweep s values are done
     }
@@ -295,8 +291,7 @@ cudaError_t launch5b(const Sweep3Params<S> &p, int threads, cudaStream_t st) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     // the smallest shared-memory carveout that holds the CTA: the rest of the unified L1
-    // caches state lines (left to the driver, the carveout varied with the block size:
-    // diag-only config 2 ran 1.6e10 against 2.3e10 with pattern blocks)
+    // caches state lines
     int carve = (int)((smem + 8192) * 100 / (228 * 1024)) + 1;
     if (const char *ev = std::getenv("MCINV_CARVE")) carve = std::atoi(ev);
     if (carve >= 0) {
