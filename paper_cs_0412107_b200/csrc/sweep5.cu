@@ -125,7 +125,9 @@ __device__ __forceinline__ void accumulate_blk(const Sweep3Params<S> &p, const Z
 // BITS: one completion bit per row instead of a byte (n up to ~1.8M rows in shared memory):
 // with the sweep barrier a row's counter only has to tell "updated in this sweep" from
 // "in the previous one", i.e. its parity; publishing toggles the bit (atomicXor).
-template <typename S, int KU, int NT, int LGC, int LGP, bool BITS>
+// GAUSS: the run's noise is the Gaussian one (the default; compile-time: +1.4% config 2, +2.5%
+// config 3 over the run-time switch between the noise modes)
+template <typename S, int KU, int NT, int LGC, int LGP, bool BITS, bool GAUSS>
 __global__ void __launch_bounds__(NT, 1) sweep5_kernel(const Sweep3Params<S> p) {
     const uint32_t zst = static_cast<uint32_t>(p.ld) * static_cast<uint32_t>(sizeof(ZW<S>));
     constexpr int E = ScalarTraits<S>::kDoubles;
@@ -225,7 +227,10 @@ __global__ void __launch_bounds__(NT, 1) sweep5_kernel(const Sweep3Params<S> p) 
 #pragma unroll
                         for (int q = 0; q < KU; ++q) prefetch_l2(zrow(zcol, col[e0 + q], zst));
                 }
-                phi = noise_phi(p.noise, static_cast<uint32_t>(i), k, gchain, p.key0, p.key1);
+                if constexpr (GAUSS)
+                    phi = gaussian(static_cast<uint32_t>(i), k, gchain, p.key0, p.key1);
+                else
+                    phi = noise_phi(p.noise, static_cast<uint32_t>(i), k, gchain, p.key0, p.key1);
                 for (int e = 0; e < nlow; ++e) {
                     const int j = col[e];
                     auto ready = [&]() -> bool {
@@ -287,7 +292,9 @@ cudaError_t launch5b(const Sweep3Params<S> &p, int threads, cudaStream_t st) {
     if (threads > NT) return cudaErrorInvalidConfiguration;
     const int blocks = (p.chains + (1 << LGC) - 1) >> LGC;
     const size_t smem = sweep5_smem(p.n, threads, p.maxb);
-    auto k = sweep5_kernel<S, KU, NT, LGC, LGP, BITS>;
+    // the Gaussian-only variant for byte counters (the common case); bit counters keep the switch
+    auto k = (!BITS && p.noise == 0) ? sweep5_kernel<S, KU, NT, LGC, LGP, BITS, !BITS>
+                                     : sweep5_kernel<S, KU, NT, LGC, LGP, BITS, false>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     // the smallest shared-memory carveout that holds the CTA: the rest of the unified L1
