@@ -33,7 +33,8 @@
 namespace mcinv {
 
 
-template <typename S, int KU, int NT, int LGP, int K>
+// GAUSS: compile-time Gaussian noise (the default mode; +2.4% config 4, +1.1% config 5)
+template <typename S, int KU, int NT, int LGP, int K, bool GAUSS = false>
 __global__ void __launch_bounds__(NT, 1) sweep3_kernel(const Sweep3Params<S> p) {
     const uint32_t zst = static_cast<uint32_t>(p.ld) * static_cast<uint32_t>(sizeof(ZW<S>));
     constexpr int E = ScalarTraits<S>::kDoubles;
@@ -84,8 +85,12 @@ __global__ void __launch_bounds__(NT, 1) sweep3_kernel(const Sweep3Params<S> p) 
                     double phi[K];
 #pragma unroll
                     for (int h = 0; h < K; ++h) {
-                        phi[h] = noise_phi(p.noise, static_cast<uint32_t>(i), k,
-                                           p.chain0 + static_cast<uint32_t>(chain + h), p.key0, p.key1);
+                        if constexpr (GAUSS)
+                            phi[h] = gaussian(static_cast<uint32_t>(i), k, p.chain0 + static_cast<uint32_t>(chain + h),
+                                              p.key0, p.key1);
+                        else
+                            phi[h] = noise_phi(p.noise, static_cast<uint32_t>(i), k,
+                                               p.chain0 + static_cast<uint32_t>(chain + h), p.key0, p.key1);
                     }
                     S az[K], aw[K];
 #pragma unroll
@@ -307,6 +312,7 @@ cudaError_t launch3k(const Sweep3Params<S> &p, int threads, cudaStream_t st) {
     const size_t smem = (p.outputs & OUT_TRACE) ? (size_t)threads * sizeof(S) : 0;
     if (threads <= 512) sweep3_kernel<S, 2 * KS, 512, LGP, K><<<blocks, threads, smem, st>>>(p);
     else if (threads <= 768) sweep3_kernel<S, KS, 768, LGP, K><<<blocks, threads, smem, st>>>(p);
+    else if (p.noise == 0) sweep3_kernel<S, KS, 1024, LGP, K, true><<<blocks, threads, smem, st>>>(p);
     else sweep3_kernel<S, KS, 1024, LGP, K><<<blocks, threads, smem, st>>>(p);
     return cudaGetLastError();
 }
