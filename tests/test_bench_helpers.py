@@ -1,0 +1,33 @@
+"""CPU checks of bench.py's roofline bookkeeping: the
+algorithmic bytes per site-update and the committed ncu summary it reads."""
+import json
+import os
+
+import numpy as np
+
+import bench
+import workloads as W
+
+
+def test_algorithmic_bytes_per_site_match_survey_d3():
+    # B_site = e (|R_i| + |K_i| + 2) averaged over rows: config 2 111.9 B (f64), config 3 160 B
+    # (c128, 4 off-diagonal entries per row and column: 16 (4 + 4 + 2))
+    c2, _, _ = W.config(2)
+    assert abs(bench.algorithmic_bytes_per_chain_sweep(c2) / c2.n - 111.9) < 0.1
+    c3, _, _ = W.config(3)
+    assert bench.algorithmic_bytes_per_chain_sweep(c3) / c3.n == 16 * (4 + 4 + 2)
+    # a diagonal matrix: only the two stores
+    d = W.diagonal(np.array([1.0, 2.0, 3.0]))
+    assert bench.algorithmic_bytes_per_chain_sweep(d) == 8 * 2 * 3
+
+
+def test_committed_ncu_summary_is_complete():
+    # the bench line's `traffic` and `roofline.issue` come from this file (one ncu --set full
+    # capture of the sweep kernel per workload); the bench workload must be in it
+    path = os.path.join(bench.ROOT, "profiles", "ncu_summary.json")
+    js = json.load(open(path))
+    s = js[W.CONFIGS[2]["name"]]
+    assert 40 < s["dram_bytes_per_site"] < 200
+    assert 5 < s["warp_inst_per_site"] < 100
+    assert bench.committed_traffic(W.CONFIGS[2]["name"]) == s["dram_bytes_per_site"]
+    assert bench.committed_summary("no such workload") == {}
