@@ -196,8 +196,7 @@ __global__ void __launch_bounds__(NT, 1) sweep5_kernel(const Sweep3Params<S> p) 
             const bool odd = item & 1;
             unsigned char *cur = odd ? buf1 : buf0;
             // stage the next group (this warp's next item, possibly in the next sweep) into the
-            // other slot: the previous item's reads of it are complete (__syncwarp)
-            __syncwarp();
+            // other slot: the previous item's reads of it are complete (its closing __syncwarp)
             const int gn = g + W < ngroups ? g + W : w;
             const bool has_next = g + W < ngroups || s + 1 < p.s_end;
             if (lane == 0 && has_next) issue(gn, odd ? buf0 : buf1, odd ? bar0 : bar1);
