@@ -267,7 +267,8 @@ __global__ void __launch_bounds__(NT, 1) sweep5_kernel(const Sweep3Params<S> p) 
                                         sp, want_diag, want_pat);
             // reconverge before the next item: lanes that skipped a divergent step of the
             // accumulation (leaders' reductions) otherwise start it as a separate sub-warp and
-            // the split persists (diag-only config 2: 1.57e10 without, 2.79e10 with)
+            // the split persists (diag-only config 2: 1.57e10 without, 2.79e10 with); it also
+            // orders every lane's reads of this item's block before the next item's TMA into it
             __syncwarp();
         }
         __syncthreads();  // sweep boundary: all reads of sweep s values are done
