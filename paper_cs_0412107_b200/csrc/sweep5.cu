@@ -243,7 +243,7 @@ __global__ void __launch_bounds__(NT, 1) sweep5_kernel(const Sweep3Params<S> p) 
                 }
             }
             if (valid) {
-                __threadfence_block();
+                __threadfence_block();  // acquire (the polls are relaxed loads; acquire loads measured ±0.5%)
                 S az = zero_s<S>(), aw = zero_s<S>();
                 row_sums_blk<S, KU>(p, zcol, col, ab, cnt, az, aw);
                 const S dl = dsg[0], sg = dsg[1];
@@ -258,9 +258,14 @@ __global__ void __launch_bounds__(NT, 1) sweep5_kernel(const Sweep3Params<S> p) 
             }
             __syncwarp();  // the row's stores are ordered before its counter update
             if (valid && c == 0) {
-                __threadfence_block();  // release
-                if constexpr (BITS) atomicXor(dbits + (i >> 5), 1u << (i & 31));
-                else *reinterpret_cast<volatile unsigned char *>(done + i) = need;
+                if constexpr (BITS) {
+                    __threadfence_block();  // release
+                    atomicXor(dbits + (i >> 5), 1u << (i & 31));
+                } else {  // a release store instead of fence + store (+0.3%, config 3 +1.7%)
+                    const unsigned short v = need;
+                    asm volatile("st.release.cta.shared::cta.u8 [%0], %1;" ::"r"(smem_addr(done + i)), "h"(v)
+                                 : "memory");
+                }
             }
             if (sampling)
                 accumulate_blk<S, P, V>(p, zcol, rec, col, pz, zi, wi, valid && active, lane, gleader, towner, sd,
