@@ -1,18 +1,25 @@
 #!/usr/bin/env python
 """Benchmark: Gibbs site-updates/s of the CC inverter on B200 (BASELINE.json metric).
 
-A "step" is one whole run of BASELINE.json configs[1] (config 2: pedigree-like
-real non-symmetric C, n = 20,000, 1024 chains per GPU, 200 burn-in + 2000
-sampling sweeps, outputs diag + pattern): every sweep of every chain, the
-fused accumulation, the moments, the all-reduce across GPUs and the on-device
-finalize. value = chains * n * sweeps (all ranks) / step time.
+A "step" is one whole run of a BASELINE.json config through the C ABI: every
+sweep of every chain (burn-in included), the fused accumulation, the moments,
+the cross-rank reduction of the moments and the on-device finalize.
+value = chains * n * sweeps (all ranks) / step time.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--scaling auto|weak|strong]
+                    [--impl ours|reference] [--no-per-config] [--no-e2e] [--no-cpu-baseline]
 
-N > 1 runs under torchrun (one process per GPU, NCCL); chains are sharded by
-global index (weak scaling: 1024 chains per GPU). Timing: CUDA events on the
-launch stream, barrier + synchronize on both sides, max over ranks. The state
-(n x chains x 16 B = 328 MB) exceeds the 126 MB L2, so no flush is needed.
+Default: config 2 (configs[1]: pedigree-like real C, n = 20,000, 1024 chains
+per GPU, 200 + 2000 sweeps, diag + pattern), weak scaling. Configs 4 and 5
+default to strong scaling: BASELINE's total chains (8192 / 16384) are split
+over the N ranks by whole SE groups (dist.shard). With --gpus N > 1 outside
+torchrun, bench.py launches itself under torch.distributed.run with N ranks
+(one process per GPU, NCCL). Timing: CUDA events on the launch stream, a
+barrier + synchronize on both sides, max over ranks. Every config's state
+exceeds the 126 MB L2 (config 2: 328 MB), so no flush is needed.
+
+At N = 1 the line also carries `per_config`: one full step of each of configs
+3, 4 and 5 (after the timed loop), with their roofline numbers.
 
 ``--impl reference`` times the oracle (oracle/, single-threaded C, one
 process per host core) on a bounded sample of the same workload: the CPU
@@ -24,6 +31,7 @@ import argparse
 import json
 import multiprocessing as mp
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -36,23 +44,44 @@ METRIC = "Gibbs site-updates/s (chains·rows/s) at 1/2/4/8 B200; % of HBM roofli
 UNIT = "site-updates/s"
 
 
-def parse():
+def parse(argv=None):
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=3)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--config", type=int, default=2, help="BASELINE.json config number (1-5)")
+    p.add_argument("--scaling", choices=["auto", "weak", "strong"], default="auto",
+                   help="weak: the config's chains per GPU; strong: its total chains split over GPUs "
+                        "(auto: strong for configs 4 and 5, weak otherwise)")
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-per-config", action="store_true", help="skip the one-step runs of configs 3, 4, 5")
     p.add_argument("--cpu-seconds", type=float, default=8.0, help="target wall time of one oracle sample")
     p.add_argument("--chains", type=int, default=0, help="override chains per GPU (diagnostics only)")
-    return p.parse_args()
+    return p.parse_args(argv)
 
 
 def env_rank():
     return (int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)),
             int(os.environ.get("WORLD_SIZE", 1)))
+
+
+def scaling_mode(args) -> str:
+    if args.scaling != "auto":
+        return args.scaling
+    return "strong" if args.config in (4, 5) else "weak"
+
+
+def self_launch(args) -> int:
+    """--gpus N > 1 outside torchrun: run this script under torch.distributed.run with
+    N ranks on this node (the driver's own launch line), passing stdout through."""
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 # ----------------------------------------------------------------- clocks
@@ -116,6 +145,21 @@ def _oracle_worker(args):
     return chains * c.n * (burn + cyc), dt
 
 
+def _cpu_clocks() -> str:
+    """lscpu's model and clock range, for the baseline's description."""
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+    except (OSError, subprocess.SubprocessError):
+        return "lscpu unavailable"
+    d = {}
+    for line in out.splitlines():
+        if ":" in line:
+            k, v = line.split(":", 1)
+            d[k.strip()] = v.strip()
+    return (f"{d.get('Model name', '?')}, {d.get('CPU(s)', '?')} CPUs, max {d.get('CPU max MHz', '?')} MHz, "
+            f"min {d.get('CPU min MHz', '?')} MHz")
+
+
 def oracle_sample(cfgk: int, target_s: float):
     """Time the oracle, as it stands, on all host cores: one process per core,
     disjoint chains, full n, sweeps sized to ~target_s; burn-in fraction as in
@@ -136,15 +180,9 @@ def oracle_sample(cfgk: int, target_s: float):
         res = pool.map(_oracle_worker, jobs)
     sites = sum(r[0] for r in res)
     wall = max(r[1] for r in res)
-    model = "?"
-    try:
-        with open("/proc/cpuinfo") as f:
-            model = next(l.split(":", 1)[1].strip() for l in f if l.startswith("model name"))
-    except (OSError, StopIteration):
-        pass
     desc = (f"{W.CONFIGS[cfgk]['name']}: {cores} processes x 1 chain x {burn}+{cyc} sweeps at full n={c.n} "
-            f"({sites:.3g} site-updates, outputs {','.join(run.outputs)} minus full when n>256) on {model}; "
-            f"single process {pilot_s / pilot_t:.3g} site-updates/s")
+            f"({sites:.3g} site-updates, outputs {','.join(run.outputs)} minus full when n>256) on "
+            f"{_cpu_clocks()}; single process {pilot_s / pilot_t:.3g} site-updates/s")
     return sites / wall, cores, desc
 
 
@@ -169,15 +207,17 @@ def load_fp64_peak():
         return 35.0, "fallback (cuBLAS DGEMM measured in round 1)"
 
 
-def algorithmic_bytes_per_chain_sweep(c) -> int:
+def algorithmic_bytes_per_chain_sweep(c, q=None) -> int:
     """per site-update, the z gathers of row i (nnz of R_i),
     the w gathers of column i (nnz of K_i) and the two stores, e bytes each:
-    sum_i e (|R_i| + |K_i| + 2) = e (2 nnz_offdiag + 2 n) per chain per sweep."""
+    sum_i e (|R_i| + |K_i| + 2) = e (2 nnz_offdiag + 2 n) per chain per sweep;
+    with the trace output also the z gathers of row i of Q (e nnz(Q): config 5's
+    352 B/site = 288 + 4 x 16)."""
     import numpy as np
     e = 16 if np.iscomplexobj(c.val) else 8
     rows = np.repeat(np.arange(c.n), np.diff(c.row_ptr))
     off = int(np.sum(rows != c.col))
-    return e * (2 * off + 2 * c.n)
+    return e * (2 * off + 2 * c.n) + (e * int(q.nnz) if q is not None else 0)
 
 
 def committed_summary(workload: str) -> dict:
@@ -197,6 +237,98 @@ def committed_traffic(workload: str):
     return committed_summary(workload).get("dram_bytes_per_site")
 
 
+KERNELS = {3: "sweep3_kernel (v3, level barriers)", 4: "sweep4_kernel (v4, dataflow)",
+           5: "sweep5_kernel (v5, dataflow + TMA-staged plan blocks)", 1: "sweep_kernel (v1)"}
+
+
+def sweep_roofline(name, c, q, outputs, chains, sweeps, st, kinfo, lconf, clk, sms_total):
+    """Roofline of the sweep kernel K1 over its launches: achieved algorithmic bytes
+     per launch / launch time against the measured HBM peak, and the
+    instruction-issue ceiling from the committed ncu warp instructions per
+    site. `bound` is the binding one: "hbm" when ncu's DRAM bandwidth at this rate
+    is at least half the peak, else "issue" (the sweep then waits on instruction
+    issue and latency, not on HBM)."""
+    launch_ms = st["sweep_ms"] / max(st["sweep_launches"], 1)
+    per_launch_sweeps = sweeps / max(st["sweep_launches"], 1)
+    sites_launch = chains * c.n * per_launch_sweeps
+    rate = sites_launch / (launch_ms / 1e3)
+    bpc = algorithmic_bytes_per_chain_sweep(c, q if "trace" in outputs else None)
+    peak, peak_src = load_peaks()
+    bytes_launch = bpc * chains * per_launch_sweeps
+    achieved = bytes_launch / (launch_ms / 1e3) / 1e9
+    summ = committed_summary(name)
+    tps = summ.get("dram_bytes_per_site")
+    hbm = {"achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+           "algorithmic_bytes_per_site": bpc / c.n, "algorithmic_bytes_per_launch": bytes_launch,
+           "peak_source": peak_src}
+    out = {"kernel": KERNELS.get(kinfo["version"], str(kinfo)), "launch": dict(kinfo, **lconf),
+           "sweep_ms_per_launch": launch_ms, "site_updates_per_s": rate,
+           "traffic": tps * sites_launch if tps else None, "traffic_bytes_per_site": tps,
+           "hbm_model": hbm}
+    ipc = summ.get("warp_inst_per_site")
+    issue = None
+    if ipc and clk.get("sm_mhz"):
+        sms = min(sms_total, lconf.get("blocks") or sms_total)
+        peak_i = sms * 4 * clk["sm_mhz"] * 1e6  # warp instructions / s: 4 schedulers per SM
+        issue = {"achieved": rate * ipc, "peak": peak_i, "unit": "warp-inst/s", "frac": rate * ipc / peak_i,
+                 "warp_inst_per_site": ipc, "sms_used": sms, "ceiling_site_updates_per_s": peak_i / ipc,
+                 "capture": summ.get("tag")}
+        out["issue"] = issue
+    dram_frac = (tps * rate / 1e9 / peak) if tps else None
+    out["dram_frac_of_peak"] = dram_frac
+    if issue is not None and dram_frac is not None and dram_frac < 0.5:
+        out.update(bound="issue", achieved=issue["achieved"], peak=issue["peak"], unit="warp-inst/s",
+                   frac=issue["frac"])
+    else:
+        out.update(bound="hbm", achieved=achieved, peak=peak, unit="GB/s", frac=achieved / peak)
+    return out
+
+
+def contract_roofline(c, chains, cycles, st, steps):
+    """K3 (X Y^dagger over snapshot chunks, FP64 DMMA): algorithmic flops 8 n^2 per
+    complex sample (2 n^2 real) against cuBLAS ZGEMM measured on this pool."""
+    import numpy as np
+    cplx = bool(np.iscomplexobj(c.val))
+    flops = (8.0 if cplx else 2.0) * c.n * c.n * chains * cycles
+    cms = st["contract_ms"] / steps
+    fp = load_fp64_peak()
+    achieved_tf = flops / (cms / 1e3) / 1e12
+    m3 = cplx and os.environ.get("MCINV_CONTRACT_3M", "1") != "0"
+    return {"bound": "tensor", "achieved": achieved_tf, "peak": fp[0], "unit": "TFLOP/s",
+            "frac": achieved_tf / fp[0] if fp[0] else None, "traffic": None, "peak_source": fp[1],
+            "kernel": "contract_kernel (K3, DMMA mma.sync.m8n8k4.f64" + (", 3-multiplication complex form)"
+                                                                         if m3 else ")"),
+            "executed_flops_per_step": flops * (0.75 if m3 else 1.0),
+            "note": ("achieved counts the algorithmic 8 flops per complex MAC; the 3-multiplication form "
+                     "executes 6, so achieved can exceed the ZGEMM peak" if m3 else None),
+            "contract_ms_per_step": cms, "algorithmic_flops_per_step": flops}
+
+
+def config_dict(args, c, q, run, world, chains_rank, total_chains, scaling):
+    """The workload description, identical in both arms."""
+    import numpy as np
+    import workloads as W
+    return {"workload": W.CONFIGS[args.config]["name"], "n": c.n, "nnz": c.nnz,
+            "chains_per_gpu": chains_rank, "total_chains": total_chains, "scaling": scaling,
+            "burn_in": run.burn_in, "cycles": run.cycles, "outputs": list(run.outputs),
+            "group_size": run.group_size, "noise": "gauss (Philox4x32-10 + Box-Muller)",
+            "l2": f"inputs larger than L2 (state {c.n * chains_rank * (32 if np.iscomplexobj(c.val) else 16) / 1e6:.0f}"
+                  f" MB per GPU > 126 MB): no flush",
+            "matrix_sha256": c.sha256()[:16], "q_nnz": int(q.nnz) if q is not None else 0}
+
+
+def shard_of(args, run, world, rank):
+    """(chain_begin, chains of this rank, total chains) for the scaling mode."""
+    from paper_cs_0412107_b200.dist import shard
+    mode = scaling_mode(args)
+    if mode == "strong":
+        total = args.chains * world if args.chains else run.chains
+        cb, ch = shard(total, world, rank, run.group_size)
+        return cb, ch, total
+    ch = args.chains or run.chains
+    return rank * ch, ch, world * ch
+
+
 # ----------------------------------------------------------------- arms
 
 def reference_arm(args):
@@ -204,6 +336,7 @@ def reference_arm(args):
     if rank != 0:
         return 0
     import workloads as W
+    world = max(world, args.gpus)
     vals = []
     cores, desc = None, None
     for s in range(args.warmup + args.steps):
@@ -211,21 +344,61 @@ def reference_arm(args):
         if s >= args.warmup:
             vals.append(rate)
     value = statistics.mean(vals)
-    c, _, run = W.config(args.config)
-    # the oracle times a bounded sample; the whole step's time at that rate (extrapolated)
-    step_sites = run.chains * c.n * (run.burn_in + run.cycles)
+    c, q, run = W.config(args.config)
+    _, ch0, total = shard_of(args, run, world, 0)
+    step_sites = total * c.n * (run.burn_in + run.cycles)
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_sites / value * 1e3,
             "ms_per_step_kind": "extrapolated from the timed sample", "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": W.CONFIGS[args.config]["dtype"], "data": "synthetic",
-            "config": {"workload": W.CONFIGS[args.config]["name"], "n": c.n, "nnz": c.nnz,
-                       "chains_per_gpu": run.chains, "burn_in": run.burn_in, "cycles": run.cycles,
-                       "outputs": list(run.outputs), "group_size": run.group_size,
-                       "matrix_sha256": c.sha256()[:16]},
+            "scaling": scaling_mode(args), "vs_baseline": None, "dtype": W.CONFIGS[args.config]["dtype"],
+            "data": "synthetic", "config": config_dict(args, c, q, run, world, ch0, total, scaling_mode(args)),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
+
+
+def one_config_step(k: int, device: int, sms: int):
+    """One full step of BASELINE config k on this GPU (the per_config block): value,
+    sweep roofline (and K3 for the full output), clocks."""
+    import torch
+    import workloads as W
+    import paper_cs_0412107_b200 as M
+    c, q, run = W.config(k)
+    name = W.CONFIGS[k]["name"]
+    inv = M.Inverter(c, device=device, q=q)
+    # lazily loaded kernel modules and the level plan: a 1-sweep run of the same layout
+    inv.run(run.seed, run.chains, 0, 1, run.outputs, group_size=run.group_size)
+    torch.cuda.synchronize()
+    inv.stats()
+    inv.set_timing(True)
+    stream = torch.cuda.current_stream()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks = Clocks(device)
+    t0.record(stream)
+    inv.run(run.seed, run.chains, run.burn_in, run.cycles, run.outputs, group_size=run.group_size)
+    res = [inv.result(o, total_chains=run.chains, on_device=True) for o in run.outputs]
+    t1.record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    inv.run_status()
+    ms = t0.elapsed_time(t1)
+    st = inv.stats()
+    kinfo, lconf = inv.kernel_info(), inv.launch_config()
+    sweeps = run.burn_in + run.cycles
+    sites = run.chains * c.n * sweeps
+    out = {"workload": name, "chains": run.chains, "burn_in": run.burn_in, "cycles": run.cycles,
+           "outputs": list(run.outputs), "value": sites / (ms / 1e3), "unit": UNIT, "ms_per_step": ms,
+           "steps": 1, "clocks": clk, "gpu_launches": st["launches"],
+           "sweep": sweep_roofline(name, c, q, run.outputs, run.chains, sweeps, st, kinfo, lconf, clk, sms)}
+    if "full" in run.outputs and st["contract_launches"]:
+        out["contraction"] = contract_roofline(c, run.chains, run.cycles, st, 1)
+        out["contraction"]["contract_share_of_step"] = st["contract_ms"] / ms
+    del res
+    inv.close()
+    del inv
+    torch.cuda.empty_cache()
+    return out
 
 
 def ours_arm(args):
@@ -234,20 +407,22 @@ def ours_arm(args):
     import torch.distributed as dist
     import workloads as W
     import paper_cs_0412107_b200 as M
-    from paper_cs_0412107_b200.dist import allreduce_moments
+    from paper_cs_0412107_b200.dist import reduce_moments
 
     rank, local, world = env_rank()
+    if "WORLD_SIZE" in os.environ and world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     c, q, run = W.config(args.config)
     name = W.CONFIGS[args.config]["name"]
-    chains = args.chains or run.chains
-    cb = rank * chains
-    total_chains = world * chains
+    mode = scaling_mode(args)
+    cb, chains, total_chains = shard_of(args, run, world, rank)
     outputs = run.outputs
     sweeps = run.burn_in + run.cycles
     inv = M.Inverter(c, device=local, q=q)
+    sms = torch.cuda.get_device_properties(local).multi_processor_count
 
     def barrier():
         if world > 1:
@@ -255,12 +430,13 @@ def ours_arm(args):
 
     def step(h: "M.Inverter"):
         h.run(run.seed, chains, run.burn_in, run.cycles, outputs, chain_begin=cb, group_size=run.group_size)
-        allreduce_moments(h.accumulators())
+        reduce_moments(h, total_chains)
         return [h.result(o, total_chains=total_chains, on_device=True) for o in outputs]
 
     for _ in range(args.warmup):
         step(inv)
     torch.cuda.synchronize()
+    inv.run_status()
     barrier()
     inv.stats()  # reset counters
     inv.set_timing(True)
@@ -277,10 +453,11 @@ def ours_arm(args):
     torch.cuda.synchronize()
     barrier()
     clk = clocks.stop()
+    inv.run_status()  # divergence / watchdog of the timed runs
     ms = t0.elapsed_time(t1) / args.steps
     st = inv.stats()
     inv.set_timing(False)
-    kinfo = inv.kernel_info()
+    kinfo, lconf = inv.kernel_info(), inv.launch_config()
     if world > 1:
         x = torch.tensor([ms], device="cuda", dtype=torch.float64)
         dist.all_reduce(x, op=dist.ReduceOp.MAX)
@@ -288,73 +465,30 @@ def ours_arm(args):
     sites = total_chains * c.n * sweeps
     value = sites / (ms / 1e3)
 
-    # dominant kernel: the sweep kernel (K1); one launch per step for diag/pattern/trace
-    b_chain_sweep = algorithmic_bytes_per_chain_sweep(c)
-    sweep_launch_ms = st["sweep_ms"] / max(st["sweep_launches"], 1)
-    sweeps_per_launch = sweeps if "full" not in outputs else None
-    peak, peak_src = load_peaks()
     roof = None
-    if sweeps_per_launch:
-        bytes_launch = b_chain_sweep * chains * sweeps_per_launch
-        achieved = bytes_launch / (sweep_launch_ms / 1e3) / 1e9
-        tps = committed_traffic(name)
-        tr = tps * chains * c.n * sweeps_per_launch if tps else None
-        roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": tr, "traffic_bytes_per_site": tps,
-                "kernel": {3: "sweep3_kernel (v3, level barriers)", 4: "sweep4_kernel (v4, dataflow)",
-                           5: "sweep5_kernel (v5, dataflow + TMA-staged plan blocks)",
-                           1: "sweep_kernel (v1)"}.get(kinfo["version"], str(kinfo)),
-                "peak_source": peak_src,
-                "algorithmic_bytes_per_launch": bytes_launch,
-                "algorithmic_bytes_per_site": b_chain_sweep / c.n,
-                "sweep_ms_per_launch": sweep_launch_ms,
-                "sweep_share_of_step": st["sweep_ms"] / (ms * args.steps)}
-        # second ceiling: instruction issue. ncu's warp instructions per
-        # site-update on this workload x the SMs holding a CTA x 4 issue slots per clock at the
-        # clock measured during the timed region
-        ipc = committed_summary(name).get("warp_inst_per_site")
-        if ipc and clk.get("sm_mhz"):
-            props = torch.cuda.get_device_properties(local)
-            sms = min(props.multi_processor_count, -(-chains // max(1, kinfo["chains_per_warp"])))
-            ceiling = sms * 4 * clk["sm_mhz"] * 1e6 / ipc
-            rate = chains * c.n * sweeps_per_launch / (sweep_launch_ms / 1e3)
-            roof["issue"] = {"warp_inst_per_site": ipc, "sms_used": sms, "ceiling": ceiling, "unit": UNIT,
-                             "frac": rate / ceiling}
+    if "full" not in outputs:
+        roof = sweep_roofline(name, c, q, outputs, chains, sweeps * args.steps, st, kinfo, lconf, clk, sms)
+        roof["sweep_share_of_step"] = st["sweep_ms"] / (ms * args.steps)
+    elif st["contract_launches"]:
+        roof = contract_roofline(c, chains, run.cycles, st, args.steps)
+        roof["contract_share_of_step"] = st["contract_ms"] / (ms * args.steps)
 
-    if "full" in outputs and st["contract_launches"]:
-        # the full-inverse contraction dominates (config 3): FP64 tensor-core (DMMA) bound;
-        # peak = cuBLAS ZGEMM measured on this box (profiles/fp64_peak.json), else cuBLAS DGEMM
-        flops = (8.0 if np.iscomplexobj(c.val) else 2.0) * c.n * c.n * chains * run.cycles
-        cms = st["contract_ms"] / args.steps
-        fp = load_fp64_peak()
-        achieved_tf = flops / (cms / 1e3) / 1e12
-        cplx = bool(np.iscomplexobj(c.val))
-        m3 = cplx and os.environ.get("MCINV_CONTRACT_3M", "1") != "0"
-        roof = {"bound": "tensor", "achieved": achieved_tf, "peak": fp[0], "unit": "TFLOP/s",
-                "frac": achieved_tf / fp[0] if fp[0] else None, "traffic": None, "peak_source": fp[1],
-                "kernel": "contract_kernel (K3, DMMA mma.sync.m8n8k4.f64" + (", 3-multiplication complex form)"
-                                                                             if m3 else ")"),
-                "executed_flops_per_step": flops * (0.75 if m3 else 1.0),
-                "note": ("achieved counts the algorithmic 8 flops per complex MAC; the 3-multiplication form "
-                         "executes 6, so achieved can exceed the ZGEMM peak" if m3 else None),
-                "contract_ms_per_step": cms,
-                "contract_share_of_step": st["contract_ms"] / (ms * args.steps),
-                "algorithmic_flops_per_step": flops}
-
-    # e2e: the public API from host CSR to host estimates, every step
+    # e2e: the public API from host CSR to host estimates, every step (mean over K steps)
     e2e = None
     if not args.no_e2e:
         h2d = c.row_ptr.nbytes + c.col.nbytes + c.val.nbytes + (q.row_ptr.nbytes + q.col.nbytes + q.val.nbytes
                                                                    if q is not None else 0)
         times = []
         d2h = 0
+        inv.close()
+        del inv
         for s in range(args.steps + 1):
             torch.cuda.synchronize()
             barrier()
             t = time.perf_counter()
             h = M.Inverter(c, device=local, q=q)
             h.run(run.seed, chains, run.burn_in, run.cycles, outputs, chain_begin=cb, group_size=run.group_size)
-            allreduce_moments(h.accumulators())
+            reduce_moments(h, total_chains)
             res = [h.result(o, total_chains=total_chains) for o in outputs]
             h.close()
             torch.cuda.synchronize()
@@ -362,32 +496,40 @@ def ours_arm(args):
             d2h = sum(e.nbytes + s_.nbytes for e, s_ in res)
             if s > 0:  # first iteration is warm-up
                 times.append(dt)
-        e2e_s = max(times) if times else float("nan")
+        e2e_s = statistics.mean(times)
         if world > 1:
-            x = torch.tensor([statistics.mean(times)], device="cuda", dtype=torch.float64)
+            x = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
             dist.all_reduce(x, op=dist.ReduceOp.MAX)
             e2e_s = float(x.item())
-        else:
-            e2e_s = statistics.mean(times)
         e2e = {"value": sites / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-               "ms_per_step": e2e_s * 1e3}
+               "ms_per_step": e2e_s * 1e3, "statistic": "mean over the timed steps, max over ranks"}
+    else:
+        inv.close()
+        del inv
+    torch.cuda.empty_cache()
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         rate, cores, desc = oracle_sample(args.config, args.cpu_seconds)
         cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc}
 
+    per_config = None
+    if world == 1 and not args.no_per_config and args.config == 2 and not args.chains:
+        per_config = {}
+        for k in (3, 4, 5):
+            try:
+                per_config[W.CONFIGS[k]["name"]] = one_config_step(k, local, sms)
+            except Exception as e:  # reported, never silently dropped
+                per_config[W.CONFIGS[k]["name"]] = {"error": repr(e)}
+
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": mode,
                 "vs_baseline": None, "dtype": W.CONFIGS[args.config]["dtype"], "data": "synthetic",
-                "config": {"workload": name, "n": c.n, "nnz": c.nnz, "chains_per_gpu": chains,
-                           "total_chains": total_chains, "burn_in": run.burn_in, "cycles": run.cycles,
-                           "outputs": list(outputs), "group_size": run.group_size,
-                           "l2": f"inputs larger than L2 (state {c.n * chains * (32 if np.iscomplexobj(c.val) else 16) / 1e6:.0f} MB > 126 MB)",
-                           "matrix_sha256": c.sha256()[:16], "kernel": kinfo},
+                "config": config_dict(args, c, q, run, world, chains, total_chains, mode),
+                "kernel": dict(kinfo, **lconf),
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
-                "gpu_launches": st["launches"], "clocks": clk}
+                "gpu_launches": st["launches"], "clocks": clk, "per_config": per_config}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -398,6 +540,11 @@ def main():
     args = parse()
     if args.impl == "reference":
         return reference_arm(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return self_launch(args)
+    if args.gpus > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")  # NCCL's init lines (one per rank) stay visible
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     return ours_arm(args)
 
 

@@ -46,7 +46,7 @@ typedef enum {
     MCINV_E_INVALID = 1,      /* bad argument, bad CSR, non-finite value */
     MCINV_E_ZERO_DIAG = 2,    /* missing or zero c_ii: D must be non-singular */
     MCINV_E_DIAG_DOMAIN = 3,  /* real path with c_ii <= 0 (1/sqrt(c_ii) not real; use C128) */
-    MCINV_E_DIVERGED = 4,     /* non-finite or |z|,|w| > 1e12 at the end of a run: sp(T) or sp(S) >= 1 */
+    MCINV_E_DIVERGED = 4,     /* non-finite or |z|,|w| > 1e12 after any sweep: sp(T) or sp(S) >= 1 */
     MCINV_E_NOMEM = 5,        /* device or host allocation failed */
     MCINV_E_CUDA = 6,         /* CUDA runtime error (message via mcinv_error_detail) */
     MCINV_E_BUFFER = 7,       /* caller buffer too small; required size via mcinv_error_detail */
@@ -145,24 +145,47 @@ mcinv_status mcinv_run_until(mcinv_ctx *ctx, const mcinv_run_args *args, unsigne
 
 /* Borrowed device pointer to the moment vector of the last run, for an
  * all-reduce (SUM, float64) across GPUs that ran disjoint chain ranges:
- *   for each output in the order DIAG, PATTERN, FULL, TRACE present:
- *       S1[count*e], S2[count*e]   (e = 1 real, 2 complex: re and im parts)
- *   then one double: number of diverged chains.
- * S1 = sum over groups of the group sums, S2 = sum of their squares.
- * Valid until the next run or destroy. */
+ *   S1 of each output present, in the order DIAG, PATTERN, FULL, TRACE
+ *       (count*e doubles each; e = 1 real, 2 complex: re and im parts),
+ *   then M2 of each output in the same order (the same sizes),
+ *   then one double: the divergence count (non-zero if any chain diverged).
+ * S1 = sum over this run's SE groups of the group sums (Eq. 1/C numerator);
+ * M2 = sum of the squared deviations of the group sums from their mean, taken
+ * two-pass about the mean of THIS run's groups (no raw sum of squares: no
+ * cancellation). On one GPU the vector is final. Across GPUs: SUM-all-reduce
+ * the whole vector, call mcinv_recenter (M2 about the global mean), then
+ * SUM-all-reduce the M2 block it reports. Valid until the next run or destroy. */
 mcinv_status mcinv_accumulators(mcinv_ctx *ctx, double **dev_ptr, size_t *count);
+
+/* After a SUM all-reduce of the moment vector across the ranks of one job:
+ * recompute this rank's M2 block about the global mean S1 / G_total (G_total =
+ * total_chains / group_size) from its resident group sums, so that a second SUM
+ * all-reduce of the M2 block (doubles [*m2_offset, *m2_offset + *m2_count) of
+ * the vector) gives the scatter of all groups about the global mean.
+ * Asynchronous on the run's stream. Errors: E_STATE (no run), E_INVALID
+ * (total_chains smaller than this run or not a multiple of group_size). */
+mcinv_status mcinv_recenter(mcinv_ctx *ctx, int64_t total_chains, size_t *m2_offset, size_t *m2_count);
+
+/* Synchronize the last run's stream and report its device-side status:
+ * E_DIVERGED if any chain stored a non-finite value or one above 1e12 in
+ * modulus after any sweep (reading R12; *diverged, may be NULL, receives the
+ * count of affected chains x launches), E_CUDA if a dataflow dependency wait
+ * timed out (watchdog), else OK. */
+mcinv_status mcinv_run_status(mcinv_ctx *ctx, int64_t *diverged);
 
 /* Estimate and standard error of one output from the (possibly all-reduced)
  * moments: estimate = S1 / (total_chains * cycles) (Eq. 1/C), cycles =
  * all sampling sweeps since the last non-resume run; SE =
- * sd(group means)/sqrt(G), G = total_chains / group_size (R15).
+ * sd(group means)/sqrt(G) = sqrt(M2 / (G - 1) / G) / (group_size * cycles),
+ * G = total_chains / group_size (R15; NaN for G = 1).
  * estimate / std_error receive count*e doubles each (std_error may be NULL);
  * capacity is in doubles. on_device != 0: both are device pointers, written
- * asynchronously on the run's stream; otherwise host pointers and the call
- * synchronizes. Returns E_DIVERGED if any chain diverged, E_BUFFER (required
- * capacity via mcinv_error_detail's index) if capacity is too small, E_STATE
- * if no sampling sweep has run since the last fresh run (cycles = 0: a
- * burn-in-only run, to be continued with resume = 1). */
+ * asynchronously on the run's stream with no host synchronization (check the
+ * run with mcinv_run_status); otherwise host pointers, and the call
+ * synchronizes and returns mcinv_run_status's verdict (E_DIVERGED, E_CUDA).
+ * E_BUFFER (required capacity via mcinv_error_detail's index) if capacity is
+ * too small, E_STATE if no sampling sweep has run since the last fresh run
+ * (cycles = 0: a burn-in-only run, to be continued with resume = 1). */
 mcinv_status mcinv_result(mcinv_ctx *ctx, unsigned output, int64_t total_chains,
                           double *estimate, double *std_error, size_t capacity, int on_device);
 
@@ -191,6 +214,10 @@ mcinv_status mcinv_stats(mcinv_ctx *ctx, int64_t *launches, double *sweep_ms, in
  * steps_per_sweep = levels D of the row DAG. MCINV_KERNEL=v1|v3|v4|v5 in the
  * environment forces one (MCINV_E_INVALID if it does not apply). */
 mcinv_status mcinv_kernel_info(const mcinv_ctx *ctx, int *version, int *chains_per_warp, int64_t *steps_per_sweep);
+/* Launch layout of the last run's sweep kernel (the level and dataflow kernels):
+ * threads per CTA, chains per thread K (1 or 2) and CTAs; 0 threads/blocks for
+ * the row-by-row kernel. For tests and the bench line. */
+mcinv_status mcinv_launch_config(const mcinv_ctx *ctx, int *threads, int *chains_per_thread, int *blocks);
 
 /* ------------------------------------------------------------ test-only */
 
@@ -216,8 +243,14 @@ mcinv_status mcinv_debug_levels(mcinv_dtype dtype, int64_t n, const int64_t *row
                                 int slot_R, int slot_L, int32_t *slots, int64_t slots_capacity);
 /* Copy the state of chains [chain_begin, chain_begin+chains) (relative to the
  * last run's chain_begin) to host arrays z, w of shape [chains][n] (x2 doubles
- * for C128). Synchronizes. */
+ * for C128). Only those chains are copied (one strided copy). Synchronizes. */
 mcinv_status mcinv_debug_get_state(mcinv_ctx *ctx, int64_t chain_begin, int64_t chains, void *z, void *w);
+/* Per-group accumulator sums of one output of the last run (Eq. 1/C / Eq. tr
+ * numerators before the moments): groups [group_begin, group_begin + groups)
+ * of this run (0 = the group of its first chain), each count*e doubles, to the
+ * host array out[groups][count*e]. Synchronizes. */
+mcinv_status mcinv_debug_group_sums(mcinv_ctx *ctx, unsigned output, int64_t group_begin, int64_t groups,
+                                    double *out);
 /* Overwrite that state from host arrays (same layout); a following run with
  * resume = 1 continues from it. The run's workspace must still be valid. */
 mcinv_status mcinv_debug_set_state(mcinv_ctx *ctx, int64_t chain_begin, int64_t chains, const void *z,

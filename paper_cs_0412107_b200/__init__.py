@@ -63,12 +63,19 @@ SYMBOLS = {
     "mcinv_run_until": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(_RunArgs), ctypes.c_uint, ctypes.c_double,
                                        ctypes.c_int64, ctypes.c_int64, ctypes.POINTER(ctypes.c_int64),
                                        ctypes.POINTER(ctypes.c_double)]),
+    "mcinv_recenter": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.POINTER(ctypes.c_size_t),
+                                      ctypes.POINTER(ctypes.c_size_t)]),
+    "mcinv_run_status": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64)]),
+    "mcinv_debug_group_sums": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_uint, ctypes.c_int64, ctypes.c_int64,
+                                              ctypes.c_void_p]),
     "mcinv_status_string": (ctypes.c_char_p, [ctypes.c_int]),
     "mcinv_error_detail": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64),
                                           ctypes.POINTER(ctypes.c_char_p)]),
     "mcinv_destroy": (None, [ctypes.c_void_p]),
     "mcinv_kernel_info": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int),
                                          ctypes.POINTER(ctypes.c_int64)]),
+    "mcinv_launch_config": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int),
+                                           ctypes.POINTER(ctypes.c_int)]),
     "mcinv_set_timing": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
     "mcinv_stats": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_double),
                                    ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_double),
@@ -311,6 +318,32 @@ class Inverter:
         off = p.value - self._ws.data_ptr()
         return self._ws[off:off + 8 * cnt.value].view(self._torch.float64)
 
+    def recenter(self, total_chains: int):
+        """mcinv_recenter: after an all-reduce of accumulators(), recompute this rank's M2
+        block about the global mean; returns that block (torch view) for the second
+        all-reduce."""
+        off, cnt = ctypes.c_size_t(), ctypes.c_size_t()
+        _check(load().mcinv_recenter(self._h, total_chains, ctypes.byref(off), ctypes.byref(cnt)), self._h)
+        acc = self.accumulators()
+        return acc[off.value:off.value + cnt.value]
+
+    def run_status(self) -> int:
+        """mcinv_run_status: synchronize and raise on divergence / watchdog; returns the
+        divergence count (0)."""
+        d = ctypes.c_int64()
+        _check(load().mcinv_run_status(self._h, ctypes.byref(d)), self._h)
+        return d.value
+
+    def group_sums(self, output: str, group_begin: int = 0, groups: Optional[int] = None) -> np.ndarray:
+        """Per-group accumulator sums of one output (test instrumentation)."""
+        G = self.chains // self.group_size
+        groups = G - group_begin if groups is None else groups
+        comps = self.count(output) * self.e
+        out = np.zeros((groups, comps))
+        _check(load().mcinv_debug_group_sums(self._h, OUTPUTS[output], group_begin, groups, out.ctypes.data),
+               self._h)
+        return out.view(np.complex128) if self.cplx else out
+
     def count(self, output: str) -> int:
         return {"diag": self.n, "pattern": self.pcount, "full": self.n * self.n, "trace": 1}[output]
 
@@ -340,6 +373,11 @@ class Inverter:
         st = ctypes.c_int64()
         _check(load().mcinv_kernel_info(self._h, ctypes.byref(v), ctypes.byref(c), ctypes.byref(st)), self._h)
         return dict(version=v.value, chains_per_warp=c.value, steps_per_sweep=st.value)
+
+    def launch_config(self) -> dict:
+        t, k, b = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+        _check(load().mcinv_launch_config(self._h, ctypes.byref(t), ctypes.byref(k), ctypes.byref(b)), self._h)
+        return dict(threads=t.value, chains_per_thread=k.value, blocks=b.value)
 
     def set_timing(self, enable: bool = True):
         _check(load().mcinv_set_timing(self._h, int(enable)), self._h)

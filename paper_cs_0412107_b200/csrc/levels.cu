@@ -181,18 +181,18 @@ std::vector<int> schedule_slots(int64_t n, const std::vector<int4> &rec, const s
     for (int64_t o = 0; o < n; ++o) ord_of[rec[o].x] = (int)o;
     std::vector<int> up_cnt(n + 1, 0);
     for (int64_t o = 0; o < n; ++o)
-        for (int e = 0; e < (rec[o].z >> 16); ++e) up_cnt[ord_of[ent_col[rec[o].y + e]] + 1]++;
+        for (int e = 0; e < (int)((unsigned)rec[o].z >> 16); ++e) up_cnt[ord_of[ent_col[rec[o].y + e]] + 1]++;
     for (int64_t o = 0; o < n; ++o) up_cnt[o + 1] += up_cnt[o];
     std::vector<int> up(up_cnt[n]), fill(up_cnt.begin(), up_cnt.end() - 1);
     for (int64_t o = 0; o < n; ++o)
-        for (int e = 0; e < (rec[o].z >> 16); ++e) up[fill[ord_of[ent_col[rec[o].y + e]]]++] = (int)o;
+        for (int e = 0; e < (int)((unsigned)rec[o].z >> 16); ++e) up[fill[ord_of[ent_col[rec[o].y + e]]]++] = (int)o;
     // height = longest path to a sink (level order is topological: reverse sweep)
     std::vector<int> height(n, 0);
     for (int64_t o = n - 1; o >= 0; --o)
         for (int q = up_cnt[o]; q < up_cnt[o + 1]; ++q) height[o] = std::max(height[o], height[up[q]] + 1);
     // list scheduling
     std::vector<int> pending(n), ready_at(n, 0), group_of(n, -1);
-    for (int64_t o = 0; o < n; ++o) pending[o] = rec[o].z >> 16;
+    for (int64_t o = 0; o < n; ++o) pending[o] = (int)((unsigned)rec[o].z >> 16);
     // candidates keyed by (ready group, -height): rows whose lower neighbours are all placed
     using Key = std::tuple<int, int, int>;  // (ready group, -height, o)
     std::priority_queue<Key, std::vector<Key>, std::greater<Key>> waiting;  // by ready group
@@ -219,7 +219,7 @@ std::vector<int> schedule_slots(int64_t n, const std::vector<int4> &rec, const s
                 const int o0 = now[0];
                 auto dist = [&](int x) {
                     return std::abs((rec[x].z & 0xffff) - (rec[o0].z & 0xffff)) +
-                           std::abs((rec[x].z >> 16) - (rec[o0].z >> 16));
+                           std::abs((int)((unsigned)rec[x].z >> 16) - (int)((unsigned)rec[o0].z >> 16));
                 };
                 // candidates in height order; stop at the first exact match (the same choice as
                 // scanning the whole window: the first of the minimal distance)

@@ -83,6 +83,7 @@ struct Layout {
     size_t zw = 0, slot_diag = 0, slot_pat = 0, slot_full = 0, slot_trace = 0, snap_x = 0, snap_y = 0, mom = 0;
     size_t mom_count = 0;   // doubles in the moment vector
     size_t mom_diag = 0, mom_pat = 0, mom_full = 0, mom_trace = 0;  // offsets (doubles) of S1 in moments
+    size_t mom_m2 = 0;      // offset (doubles) of the M2 block: M2 of an output at mom_<output> + mom_m2
     size_t total = 0;
 };
 
@@ -115,6 +116,7 @@ struct mcinv_ctx {
     DevBuf err_flag;      // v4 watchdog flag (device unsigned)
     int last_C = 0;
     int64_t last_steps = 0;
+    int last_threads = 0, last_K = 1, last_blocks = 0;  // launch layout of the last sweep kernel
     // device C
     DevBuf u_ptr, u_col, u_a, u_b, delta, sigma;
     // pattern
@@ -529,6 +531,9 @@ Layout make_layout(const mcinv_ctx *ctx, const mcinv_run_args *a) {
         }
         if (a->cycles > 0 && T > a->cycles) T = (int)a->cycles;
         L.T = std::max(T, 1);
+        // a resumed run keeps the snapshot chunk of the run it continues: the workspace
+        // (and with it every offset) is then identical to the one the state lives in
+        if (a->resume && ctx->have_run && ctx->lay.T > 0) L.T = ctx->lay.T;
     }
     size_t off = 0;
     auto take = [&](size_t bytes) {
@@ -536,22 +541,27 @@ Layout make_layout(const mcinv_ctx *ctx, const mcinv_run_args *a) {
         off = align256(off + bytes);
         return o;
     };
+    // state and accumulators first, the snapshot chunk (size T-dependent) last, so that
+    // the offsets of everything a resumed run continues from do not depend on T
     L.zw = take((size_t)n * L.ld * 2 * sz);
     if (a->outputs & MCINV_DIAG) L.slot_diag = take((size_t)L.Gs * n * sz);
     if (a->outputs & MCINV_PATTERN) L.slot_pat = take((size_t)L.Gs * std::max<int64_t>(ctx->pcount, 1) * sz);
+    if (a->outputs & MCINV_FULL) L.slot_full = take((size_t)L.G * n * n * sz);
+    if (a->outputs & MCINV_TRACE) L.slot_trace = take((size_t)L.Gs * sz);
+    size_t m = 0;
+    // moment vector: S1 of every output, then M2 of every output (same order), then the
+    // divergence count (mcinv_accumulators)
+    if (a->outputs & MCINV_DIAG) { L.mom_diag = m; m += (size_t)n * L.e; }
+    if (a->outputs & MCINV_PATTERN) { L.mom_pat = m; m += (size_t)ctx->pcount * L.e; }
+    if (a->outputs & MCINV_FULL) { L.mom_full = m; m += (size_t)n * n * L.e; }
+    if (a->outputs & MCINV_TRACE) { L.mom_trace = m; m += (size_t)L.e; }
+    L.mom_m2 = m;
+    L.mom_count = 2 * m + 1;
+    L.mom = take(L.mom_count * 8);
     if (a->outputs & MCINV_FULL) {
-        L.slot_full = take((size_t)L.G * n * n * sz);
         L.snap_x = take((size_t)L.T * n * L.ld * sz);
         L.snap_y = take((size_t)L.T * n * L.ld * sz);
     }
-    if (a->outputs & MCINV_TRACE) L.slot_trace = take((size_t)L.Gs * sz);
-    size_t m = 0;
-    if (a->outputs & MCINV_DIAG) { L.mom_diag = m; m += 2 * (size_t)n * L.e; }
-    if (a->outputs & MCINV_PATTERN) { L.mom_pat = m; m += 2 * (size_t)ctx->pcount * L.e; }
-    if (a->outputs & MCINV_FULL) { L.mom_full = m; m += 2 * (size_t)n * n * L.e; }
-    if (a->outputs & MCINV_TRACE) { L.mom_trace = m; m += 2 * (size_t)L.e; }
-    L.mom_count = m + 1;
-    L.mom = take(L.mom_count * 8);
     L.total = off;
     return L;
 }
@@ -604,7 +614,8 @@ LevelDev *get_levels(mcinv_ctx *ctx, unsigned outputs) {
             int nlow = 0;
             while (nlow < cnt && P.ent_col[beg + nlow] < i) ++nlow;  // lower neighbours: a prefix
             if (cnt >= 65536) ld->error = "a row has 65536 or more off-diagonal entries";
-            rec[o] = make_int4(i, beg, cnt | nlow << 16, P.ord_pself[o]);
+            // packed in unsigned arithmetic (decoded as unsigned: nlow up to 65535)
+            rec[o] = make_int4(i, beg, (int)((unsigned)cnt | (unsigned)nlow << 16), P.ord_pself[o]);
         }
         std::vector<S> tqv(P.tq_val.size());
         for (size_t e = 0; e < tqv.size(); ++e) tqv[e] = to_s<S>(P.tq_val[e]);
@@ -784,6 +795,24 @@ LevelDev::Slots *get_slots(mcinv_ctx *ctx, LevelDev *lv, int R, int W, bool bloc
     return raw;
 }
 
+// K4 for every output of a run: S1 and M2 (about the local groups' mean, or with center
+// about the global mean center[S1 offset] / center_G: mcinv_recenter)
+void launch_all_moments(mcinv_ctx *ctx, const Layout &L, char *ws, unsigned outputs, const double *center,
+                        double center_G, cudaStream_t st) {
+    const int64_t n = ctx->n;
+    const int e = L.e;
+    double *mom = (double *)(ws + L.mom);
+    auto one = [&](const void *slot, int k, int64_t comps, size_t off) {
+        mcinv::launch_moments((const double *)slot, L.G, k, comps, mom + off, mom + off + L.mom_m2,
+                              center ? center + off : nullptr, center_G, st);
+        ctx->launches++;
+    };
+    if (outputs & MCINV_DIAG) one(ws + L.slot_diag, L.ksub, n * e, L.mom_diag);
+    if (outputs & MCINV_PATTERN) one(ws + L.slot_pat, L.ksub, ctx->pcount * e, L.mom_pat);
+    if (outputs & MCINV_FULL) one(ws + L.slot_full, 1, n * n * e, L.mom_full);
+    if (outputs & MCINV_TRACE) one(ws + L.slot_trace, L.ksub, e, L.mom_trace);
+}
+
 template <typename S>
 mcinv_status run_typed(mcinv_ctx *ctx, const mcinv_run_args *a, const Layout &L, char *ws, cudaStream_t st) {
     using namespace mcinv;
@@ -812,8 +841,13 @@ mcinv_status run_typed(mcinv_ctx *ctx, const mcinv_run_args *a, const Layout &L,
     p.slot_pat = (double *)(ws + L.slot_pat);
     p.slot_trace = (double *)(ws + L.slot_trace);
     const int total = (int)(a->burn_in + a->cycles);
+    // divergence count: the last double of the moment vector, incremented by the sweep kernels
+    // (every stored value is checked: reading R12's per-sweep rule); kept across resumes
+    double *const mom = (double *)(ws + L.mom);
+    p.bad = mom + L.mom_count - 1;
 
     if (!a->resume) {
+        CK(cudaMemsetAsync(p.bad, 0, sizeof(double), st));
         CK(cudaMemsetAsync(ws + L.zw, 0, (size_t)n * L.ld * sizeof(ZW<S>), st));
         if (a->outputs & MCINV_DIAG) CK(cudaMemsetAsync(p.slot_diag, 0, (size_t)L.Gs * n * sizeof(S), st));
         if (a->outputs & MCINV_PATTERN)
@@ -882,6 +916,9 @@ mcinv_status run_typed(mcinv_ctx *ctx, const mcinv_run_args *a, const Layout &L,
     ctx->last_kernel = v5 ? 5 : v4 ? 4 : L.ver;
     ctx->last_C = lv ? (1 << L.lgC) : 32;
     ctx->last_steps = lv ? lv->D : n;
+    ctx->last_K = 1 << lgK;
+    ctx->last_threads = lv ? threads3 : 0;
+    ctx->last_blocks = lv ? (int)((a->chains + (int64_t(1) << L.lgC) - 1) >> L.lgC) : 0;
     Sweep3Params<S> q3{};
     if (lv) {
         q3.ph_row = (const int *)lv->ph_row.p;
@@ -918,6 +955,7 @@ mcinv_status run_typed(mcinv_ctx *ctx, const mcinv_run_args *a, const Layout &L,
         q3.slot_diag = p.slot_diag;
         q3.slot_pat = p.slot_pat;
         q3.slot_trace = p.slot_trace;
+        q3.bad = p.bad;
         // MCINV_RECONV bits: 1 reconverge the warp at the end of each item (default: diag-only
         // config 2 1.57 -> 2.79e10), 2 also after the dependency waits (measured -6%)
         q3.reconv = 1;
@@ -988,23 +1026,8 @@ mcinv_status run_typed(mcinv_ctx *ctx, const mcinv_run_args *a, const Layout &L,
     }
     if (lerr != cudaSuccess) return fail(ctx, MCINV_E_CUDA, std::string("sweep launch: ") + cudaGetErrorString(lerr));
     CK(cudaGetLastError());
-    // moments and divergence flag
-    double *mom = (double *)(ws + L.mom);
-    CK(cudaMemsetAsync(mom + L.mom_count - 1, 0, sizeof(double), st));
-    launch_check<S>(p.zw, (int)n, L.ld, (int)a->chains, mom + L.mom_count - 1, st);
-    ctx->launches++;
-    const int e = L.e;
-    ctx->launches += __builtin_popcount(a->outputs);  // one moments kernel per output
-    if (a->outputs & MCINV_DIAG)
-        launch_moments(p.slot_diag, L.G, L.ksub, n * e, mom + L.mom_diag, mom + L.mom_diag + n * e, st);
-    if (a->outputs & MCINV_PATTERN)
-        launch_moments(p.slot_pat, L.G, L.ksub, ctx->pcount * e, mom + L.mom_pat, mom + L.mom_pat + ctx->pcount * e,
-                       st);
-    if (a->outputs & MCINV_FULL)
-        launch_moments((const double *)(ws + L.slot_full), L.G, 1, n * n * e, mom + L.mom_full,
-                       mom + L.mom_full + n * n * e, st);
-    if (a->outputs & MCINV_TRACE)
-        launch_moments(p.slot_trace, L.G, L.ksub, e, mom + L.mom_trace, mom + L.mom_trace + e, st);
+    // moments (the divergence count was produced by the sweep kernels)
+    launch_all_moments(ctx, L, ws, a->outputs, nullptr, 0.0, st);
     CK(cudaGetLastError());
     return MCINV_OK;
 }
@@ -1114,11 +1137,16 @@ mcinv_status mcinv_run(mcinv_ctx *ctx, const mcinv_run_args *args) {
         if (!ctx->have_run || ctx->last.chains != args->chains || ctx->last.outputs != args->outputs ||
             ctx->last.group_size != args->group_size || (ws && ws != ctx->ws))
             return fail(ctx, MCINV_E_STATE, "resume needs the previous run's shape and workspace");
-        if (!ws) ws = ctx->ws;
     }
     if (ws) {
         if (args->workspace_bytes < L.total || ((uintptr_t)ws & 255))
             return fail(ctx, MCINV_E_BUFFER, "workspace too small or misaligned", (int64_t)L.total);
+    } else if (args->resume) {
+        // NULL on resume: continue in the previous run's workspace (library-owned or the
+        // caller's); the resumed layout is that run's (make_layout keeps its T), so it fits
+        if (L.total > ctx->lay.total || L.zw != ctx->lay.zw || L.mom != ctx->lay.mom)
+            return fail(ctx, MCINV_E_STATE, "resume layout differs from the previous run's");
+        ws = ctx->ws;
     } else {
         if (ctx->own_ws.bytes < L.total) {
             ctx->own_ws.release();
@@ -1147,6 +1175,38 @@ mcinv_status mcinv_accumulators(mcinv_ctx *ctx, double **dev_ptr, size_t *count)
     if (!ctx || !ctx->have_run || !dev_ptr || !count) return MCINV_E_STATE;
     *dev_ptr = (double *)(ctx->ws + ctx->lay.mom);
     *count = ctx->lay.mom_count;
+    return MCINV_OK;
+}
+
+mcinv_status mcinv_run_status(mcinv_ctx *ctx, int64_t *diverged) {
+    if (!ctx || !ctx->have_run) return MCINV_E_STATE;
+    CK(cudaSetDevice(ctx->device));
+    double bad = 0.0;
+    const double *mom = (const double *)(ctx->ws + ctx->lay.mom);
+    CK(cudaMemcpyAsync(&bad, mom + ctx->lay.mom_count - 1, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (diverged) *diverged = (int64_t)bad;
+    if (ctx->last_kernel >= 4) {
+        unsigned wd = 0;
+        CK(cudaMemcpy(&wd, ctx->err_flag.p, sizeof(wd), cudaMemcpyDeviceToHost));
+        if (wd) return fail(ctx, MCINV_E_CUDA, "v4 dataflow watchdog: a dependency wait exceeded its bound");
+    }
+    if (bad > 0.0) return fail(ctx, MCINV_E_DIVERGED, "state non-finite or above 1e12", (int64_t)bad);
+    return MCINV_OK;
+}
+
+mcinv_status mcinv_recenter(mcinv_ctx *ctx, int64_t total_chains, size_t *m2_offset, size_t *m2_count) {
+    if (!ctx || !ctx->have_run) return MCINV_E_STATE;
+    const mcinv_run_args &a = ctx->last;
+    if (total_chains < a.chains || total_chains % a.group_size)
+        return fail(ctx, MCINV_E_INVALID, "total_chains");
+    CK(cudaSetDevice(ctx->device));
+    const Layout &L = ctx->lay;
+    const double *s1 = (const double *)(ctx->ws + L.mom);
+    launch_all_moments(ctx, L, ctx->ws, a.outputs, s1, (double)(total_chains / a.group_size), ctx->stream);
+    CK(cudaGetLastError());
+    if (m2_offset) *m2_offset = L.mom_m2;
+    if (m2_count) *m2_count = L.mom_m2;
     return MCINV_OK;
 }
 
@@ -1179,39 +1239,31 @@ mcinv_status mcinv_result(mcinv_ctx *ctx, unsigned output, int64_t total_chains,
     const double G = (double)(total_chains / a.group_size);
     cudaStream_t st = ctx->stream;
     if (on_device) {
-        mcinv::launch_finalize(mom + off, mom + off + comps, comps, (double)total_chains * cyc, a.group_size * cyc, G,
-                               estimate, std_error, st);
+        // asynchronous on the run's stream; divergence is reported by mcinv_run_status
+        mcinv::launch_finalize(mom + off, mom + off + L.mom_m2, comps, (double)total_chains * cyc, a.group_size * cyc,
+                               G, estimate, std_error, st);
         ctx->launches++;
         CK(cudaGetLastError());
-    } else {
-        const size_t need = 2 * comps * sizeof(double);
-        if (ctx->tmp.bytes < need) {
-            ctx->tmp.release();
-            if (dev_alloc(&ctx->tmp.p, need) != cudaSuccess || cudaStreamSynchronize(0) != cudaSuccess) {
-                cudaGetLastError();
-                ctx->tmp.p = nullptr;
-                return fail(ctx, MCINV_E_NOMEM, "result staging");
-            }
-            ctx->tmp.bytes = need;
+        return MCINV_OK;
+    }
+    const size_t need = 2 * comps * sizeof(double);
+    if (ctx->tmp.bytes < need) {
+        ctx->tmp.release();
+        if (dev_alloc(&ctx->tmp.p, need) != cudaSuccess || cudaStreamSynchronize(0) != cudaSuccess) {
+            cudaGetLastError();
+            ctx->tmp.p = nullptr;
+            return fail(ctx, MCINV_E_NOMEM, "result staging");
         }
-        double *de = (double *)ctx->tmp.p, *ds = de + comps;
-        mcinv::launch_finalize(mom + off, mom + off + comps, comps, (double)total_chains * cyc, a.group_size * cyc, G,
-                               de, ds, st);
-        ctx->launches++;
-        CK(cudaGetLastError());
-        CK(cudaMemcpyAsync(estimate, de, comps * sizeof(double), cudaMemcpyDeviceToHost, st));
-        if (std_error) CK(cudaMemcpyAsync(std_error, ds, comps * sizeof(double), cudaMemcpyDeviceToHost, st));
+        ctx->tmp.bytes = need;
     }
-    double bad = 0.0;
-    CK(cudaMemcpyAsync(&bad, mom + L.mom_count - 1, sizeof(double), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    if (ctx->last_kernel >= 4) {
-        unsigned wd = 0;
-        CK(cudaMemcpy(&wd, ctx->err_flag.p, sizeof(wd), cudaMemcpyDeviceToHost));
-        if (wd) return fail(ctx, MCINV_E_CUDA, "v4 dataflow watchdog: a dependency wait exceeded its bound");
-    }
-    if (bad > 0.0) return fail(ctx, MCINV_E_DIVERGED, "state non-finite or above 1e12", (int64_t)bad);
-    return MCINV_OK;
+    double *de = (double *)ctx->tmp.p, *ds = de + comps;
+    mcinv::launch_finalize(mom + off, mom + off + L.mom_m2, comps, (double)total_chains * cyc, a.group_size * cyc, G,
+                           de, ds, st);
+    ctx->launches++;
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(estimate, de, comps * sizeof(double), cudaMemcpyDeviceToHost, st));
+    if (std_error) CK(cudaMemcpyAsync(std_error, ds, comps * sizeof(double), cudaMemcpyDeviceToHost, st));
+    return mcinv_run_status(ctx, nullptr);  // synchronizes
 }
 
 void mcinv_destroy(mcinv_ctx *ctx) {
@@ -1237,6 +1289,14 @@ mcinv_status mcinv_kernel_info(const mcinv_ctx *ctx, int *version, int *chains_p
     if (version) *version = ctx->last_kernel;
     if (chains_per_warp) *chains_per_warp = ctx->last_C;
     if (steps_per_sweep) *steps_per_sweep = ctx->last_steps;
+    return MCINV_OK;
+}
+
+mcinv_status mcinv_launch_config(const mcinv_ctx *ctx, int *threads, int *chains_per_thread, int *blocks) {
+    if (!ctx || !ctx->have_run) return MCINV_E_STATE;
+    if (threads) *threads = ctx->last_threads;
+    if (chains_per_thread) *chains_per_thread = ctx->last_K;
+    if (blocks) *blocks = ctx->last_blocks;
     return MCINV_OK;
 }
 
@@ -1422,7 +1482,8 @@ mcinv_status mcinv_debug_levels(mcinv_dtype dtype, int64_t n, const int64_t *row
             const int i = P.ord_row[o], beg = P.ord_eptr[o], cnt = P.ord_eptr[o + 1] - beg;
             int nlow = 0;
             while (nlow < cnt && P.ent_col[beg + nlow] < i) ++nlow;
-            rec[o] = make_int4(i, beg, cnt | nlow << 16, -1);
+            if (cnt >= 65536) return fail(ctx, MCINV_E_INVALID, "a row has 65536 or more off-diagonal entries", i);
+            rec[o] = make_int4(i, beg, (int)((unsigned)cnt | (unsigned)nlow << 16), -1);
         }
         const char *se = std::getenv("MCINV_SIMILAR");
         const std::vector<int> order = mcinv::schedule_slots(n, rec, P.ent_col, slot_R, slot_L, 0, se ? std::atoi(se) : 32);
@@ -1479,16 +1540,22 @@ static mcinv_status state_io(mcinv_ctx *ctx, int64_t chain_begin, int64_t chains
     if (!ctx || !ctx->have_run) return MCINV_E_STATE;
     if (chain_begin < 0 || chains < 0 || chain_begin + chains > ctx->last.chains || !z || !w)
         return fail(ctx, MCINV_E_INVALID, "state range");
+    if (chains == 0) return MCINV_OK;
     CK(cudaSetDevice(ctx->device));
     const int64_t n = ctx->n, ld = ctx->lay.ld, e = ctx->lay.e;
-    std::vector<double> buf((size_t)n * ld * 2 * e);
+    // only the requested chains cross the bus: one strided 2-D copy of n rows of `chains`
+    // contiguous (z, w) elements (config 4: 3 chains x 1e6 rows = 48 MB, not the 131 GB state)
+    const size_t elem = 2 * (size_t)e * sizeof(double);  // one ZW<S>
+    std::vector<double> buf((size_t)n * chains * 2 * e);
+    char *dev = ctx->ws + ctx->lay.zw + (size_t)chain_begin * elem;
     CK(cudaStreamSynchronize(ctx->stream));
-    CK(cudaMemcpy(buf.data(), ctx->ws + ctx->lay.zw, buf.size() * 8, cudaMemcpyDeviceToHost));
+    if (get)
+        CK(cudaMemcpy2D(buf.data(), chains * elem, dev, ld * elem, chains * elem, n, cudaMemcpyDeviceToHost));
     double *zd = (double *)z, *wd = (double *)w;
     for (int64_t c = 0; c < chains; ++c)
         for (int64_t i = 0; i < n; ++i)
             for (int64_t q = 0; q < e; ++q) {
-                double *src = &buf[((i * ld + chain_begin + c) * 2) * e + q];
+                double *src = &buf[((i * chains + c) * 2) * e + q];
                 double *hz = &zd[(c * n + i) * e + q], *hw = &wd[(c * n + i) * e + q];
                 if (get) {
                     *hz = src[0];
@@ -1498,7 +1565,31 @@ static mcinv_status state_io(mcinv_ctx *ctx, int64_t chain_begin, int64_t chains
                     src[e] = *hw;
                 }
             }
-    if (!get) CK(cudaMemcpy(ctx->ws + ctx->lay.zw, buf.data(), buf.size() * 8, cudaMemcpyHostToDevice));
+    if (!get)
+        CK(cudaMemcpy2D(dev, ld * elem, buf.data(), chains * elem, chains * elem, n, cudaMemcpyHostToDevice));
+    return MCINV_OK;
+}
+
+mcinv_status mcinv_debug_group_sums(mcinv_ctx *ctx, unsigned output, int64_t group_begin, int64_t groups,
+                                    double *out) {
+    if (!ctx || !ctx->have_run) return MCINV_E_STATE;
+    const Layout &L = ctx->lay;
+    const mcinv_run_args &a = ctx->last;
+    if (!(a.outputs & output) || (output & (output - 1)) || !out || group_begin < 0 || groups < 0 ||
+        group_begin + groups > L.G)
+        return fail(ctx, MCINV_E_INVALID, "group range or output");
+    CK(cudaSetDevice(ctx->device));
+    int64_t count = 0;
+    size_t slot = 0;
+    switch (output) {
+        case MCINV_DIAG: count = ctx->n; slot = L.slot_diag; break;
+        case MCINV_PATTERN: count = ctx->pcount; slot = L.slot_pat; break;
+        case MCINV_FULL: count = ctx->n * ctx->n; slot = L.slot_full; break;
+        default: count = 1; slot = L.slot_trace; break;
+    }
+    const size_t row = (size_t)count * L.e * sizeof(double);  // one group's accumulators (ksub == 1)
+    CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaMemcpy(out, ctx->ws + slot + (size_t)group_begin * row, (size_t)groups * row, cudaMemcpyDeviceToHost));
     return MCINV_OK;
 }
 

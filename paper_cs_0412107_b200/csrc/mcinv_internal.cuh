@@ -80,6 +80,7 @@ template <typename S> struct SweepParams {
     double *slot_trace;   // [G] * e
     S *snap_x, *snap_y;   // [T][n][ld]
     int snap_s0;          // local sweep stored at snapshot slot 0
+    double *bad;          // divergence count (+1 per active lane that stored a value above 1e12 or non-finite)
 };
 
 template <typename S>
@@ -128,6 +129,8 @@ struct Sweep3Params {
     int spin_ns;          // dataflow waits: __nanosleep between counter polls (0: none)
     int reconv;           // v5: __syncwarp at the item end (bit 0) / after the dependency waits (bit 1)
     int prefetch;         // v5: prefetch upper neighbours' lines before the noise (0 off, 1 L1, 2 L2)
+    double *bad;          // divergence count: +1 per active lane that stored a non-finite value or one
+                          // above 1e12 in modulus (checked at every update = every sweep's end state)
 };
 
 template <typename S>
@@ -146,11 +149,12 @@ void launch_contract(const S *x, const S *y, double *acc, int n, int ld, int cha
                      cudaStream_t st);
 
 // slot layout [G * k][comps]: group g is the sum of sub-slots g*k .. g*k+k-1
-void launch_moments(const double *slot, int G, int k, int64_t comps, double *s1, double *s2, cudaStream_t st);
-void launch_finalize(const double *s1, const double *s2, int64_t comps, double m_cycles, double gs_cycles,
+// s1 = sum of the group sums, m2 = their scatter about the mean of these groups (center ==
+// nullptr) or about center[c] / center_G (the global mean after an all-reduce; s1 untouched)
+void launch_moments(const double *slot, int G, int k, int64_t comps, double *s1, double *m2, const double *center,
+                    double center_G, cudaStream_t st);
+void launch_finalize(const double *s1, const double *m2, int64_t comps, double m_cycles, double gs_cycles,
                      double G, double *est, double *se, cudaStream_t st);
-template <typename S>
-void launch_check(const ZW<S> *zw, int n, int ld, int chains, double *flag, cudaStream_t st);
 template <typename S>
 void launch_max_modulus(const ZW<S> *zw, int n, int ld, double *out, cudaStream_t st);
 void launch_philox(const uint32_t *ctr, int64_t count, uint32_t k0, uint32_t k1, uint32_t *out,

@@ -38,6 +38,15 @@ __device__ __forceinline__ PhiloxOut philox4x32_10(uint32_t c0, uint32_t c1, uin
     return PhiloxOut{c0, c1, c2, c3};
 }
 
+// log_unit and cos_0_2pi below follow fdlibm's e_log.c and k_cos.c / k_sin.c
+// (argument reduction and the published minimax coefficients Lg1-Lg7, C1-C6,
+// S1-S6, ln2_hi / ln2_lo), restructured into fma-Horner form for these
+// argument ranges. fdlibm's notice, as its licence asks:
+//   Copyright (C) 1993 by Sun Microsystems, Inc. All rights reserved.
+//   Developed at SunPro, a Sun Microsystems, Inc. business.
+//   Permission to use, copy, modify, and distribute this software is freely
+//   granted, provided that this notice is preserved.
+//
 // ln(x) for x in (0, 1] (normal doubles only): the fdlibm method (reduce to
 // m in [sqrt(2)/2, sqrt(2)), s = f / (2 + f), ln(1 + f) = f - f^2/2 +
 // s (f^2/2 + R(s^2)) with a degree-14 minimax R); < 1 ulp, no special cases.

@@ -1,5 +1,5 @@
 // reduce.cu -- K4: group moments, finalize (estimate + standard error),
-// divergence check, and the test-only Philox/Gaussian dump kernels.
+// the coupled-burn-in reduction, and the test-only Philox/Gaussian dump kernels.
 //
 // Estimate (Eq. 1/C):  est = S1 / (m (M-N)).
 // Standard error (reading R15, replacing the Geyer error of
@@ -10,54 +10,54 @@
 
 namespace mcinv {
 
-// slot layout [G * k][comps]: the sum of group g is the sum of its k
-// sub-slots; s1[c] = sum_g group sum, s2[c] = sum_g (group sum)^2.
+// slot layout [G * k][comps]: the sum of group g is the sum of its k sub-slots.
+// s1[c] = sum_g (group sum g); m2[c] = sum_g (group sum - mean)^2, two-pass about the
+// mean of these G groups (no cancellation of a raw sum of squares). With `center`
+// (after a cross-rank all-reduce of s1): s1 is left alone and m2 is taken about the
+// global mean center[c] / center_G instead, so that a SUM of the ranks' m2 is the
+// scatter of all groups about the global mean (mcinv_recenter).
 __global__ void moments_kernel(const double *__restrict__ slot, int G, int k, int64_t comps,
-                               double *__restrict__ s1, double *__restrict__ s2) {
+                               double *__restrict__ s1, double *__restrict__ m2,
+                               const double *__restrict__ center, double center_G) {
     for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < comps;
          c += (int64_t)gridDim.x * blockDim.x) {
-        double a = 0.0, b = 0.0;
+        double mean;
+        if (center) {
+            mean = center[c] / center_G;
+        } else {
+            double a = 0.0;
+            for (int g = 0; g < G; ++g) {
+                double v = 0.0;
+                for (int h = 0; h < k; ++h) v += slot[((int64_t)g * k + h) * comps + c];
+                a += v;
+            }
+            s1[c] = a;
+            mean = a / (double)G;
+        }
+        double b = 0.0;
         for (int g = 0; g < G; ++g) {
             double v = 0.0;
             for (int h = 0; h < k; ++h) v += slot[((int64_t)g * k + h) * comps + c];
-            a += v;
-            b = fma(v, v, b);
+            const double d = v - mean;
+            b = fma(d, d, b);
         }
-        s1[c] = a;
-        s2[c] = b;
+        m2[c] = b;
     }
 }
 
-__global__ void finalize_kernel(const double *__restrict__ s1, const double *__restrict__ s2, int64_t comps,
+// estimate = S1 / (m (M-N)); SE = sqrt(var(group means) / G) with
+// var(group means) = M2 / ((gs (M-N))^2 (G - 1))  (reading R15)
+__global__ void finalize_kernel(const double *__restrict__ s1, const double *__restrict__ m2, int64_t comps,
                                 double m_cycles, double gs_cycles, double G, double *__restrict__ est,
                                 double *__restrict__ se) {
     for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < comps;
          c += (int64_t)gridDim.x * blockDim.x) {
         est[c] = s1[c] / m_cycles;
         if (se) {
-            // sum of squared group means minus G * (mean of group means)^2
-            const double mean = s1[c] / (G * gs_cycles);
-            const double sq = s2[c] / (gs_cycles * gs_cycles);
-            const double var = G > 1.0 ? (sq - G * mean * mean) / (G - 1.0) : NAN;
-            se[c] = var > 0.0 ? sqrt(var / G) : (var == var ? 0.0 : NAN);
+            const double var = G > 1.0 ? m2[c] / (gs_cycles * gs_cycles * (G - 1.0)) : NAN;
+            se[c] = sqrt(var / G);
         }
     }
-}
-
-// Count state values that are non-finite or exceed 1e12 in magnitude
-// (SPEC S:234 divergence rule; sp(T) >= 1 or sp(S) >= 1).
-template <typename S>
-__global__ void check_kernel(const ZW<S> *__restrict__ zw, int n, int ld, int chains, double *flag) {
-    int bad = 0;
-    const int64_t total = (int64_t)n * ld;
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-         e += (int64_t)gridDim.x * blockDim.x) {
-        if ((int)(e % ld) >= chains) continue;
-        const ZW<S> v = zw[e];
-        bad += bad_s(v.z) || bad_s(v.w);
-    }
-    bad = __reduce_add_sync(0xffffffffu, bad);
-    if ((threadIdx.x & 31) == 0 && bad) atomicAdd(flag, (double)bad);
 }
 
 // max over rows of the (z, w) moduli of chain 0 (the coupled-burn-in difference)
@@ -116,21 +116,15 @@ static int grid_for(int64_t work, int threads) {
     return b < 1 ? 1 : (int)b;
 }
 
-void launch_moments(const double *slot, int G, int k, int64_t comps, double *s1, double *s2, cudaStream_t st) {
-    moments_kernel<<<grid_for(comps, 256), 256, 0, st>>>(slot, G, k, comps, s1, s2);
+void launch_moments(const double *slot, int G, int k, int64_t comps, double *s1, double *m2, const double *center,
+                    double center_G, cudaStream_t st) {
+    moments_kernel<<<grid_for(comps, 256), 256, 0, st>>>(slot, G, k, comps, s1, m2, center, center_G);
 }
 
-void launch_finalize(const double *s1, const double *s2, int64_t comps, double m_cycles, double gs_cycles, double G,
+void launch_finalize(const double *s1, const double *m2, int64_t comps, double m_cycles, double gs_cycles, double G,
                      double *est, double *se, cudaStream_t st) {
-    finalize_kernel<<<grid_for(comps, 256), 256, 0, st>>>(s1, s2, comps, m_cycles, gs_cycles, G, est, se);
+    finalize_kernel<<<grid_for(comps, 256), 256, 0, st>>>(s1, m2, comps, m_cycles, gs_cycles, G, est, se);
 }
-
-template <typename S>
-void launch_check(const ZW<S> *zw, int n, int ld, int chains, double *flag, cudaStream_t st) {
-    check_kernel<S><<<grid_for((int64_t)n * ld, 256), 256, 0, st>>>(zw, n, ld, chains, flag);
-}
-template void launch_check<double>(const ZW<double> *, int, int, int, double *, cudaStream_t);
-template void launch_check<cd>(const ZW<cd> *, int, int, int, double *, cudaStream_t);
 
 void launch_philox(const uint32_t *ctr, int64_t count, uint32_t k0, uint32_t k1, uint32_t *out, double *gauss,
                    cudaStream_t st) {

@@ -45,6 +45,7 @@ __global__ void __launch_bounds__(128) sweep_kernel(const SweepParams<S> p) {
     const bool leader = (lane & (p.gs - 1)) == 0;
     const int g = c / p.gs;
     S tr = zero_s<S>();
+    bool dv = false;  // divergence seen (reading R12: every stored value is a sweep-end value)
 
     for (int s = p.s_begin; s < p.s_end; ++s) {
         const uint32_t k = p.sweep_abs0 + static_cast<uint32_t>(s);
@@ -63,6 +64,7 @@ __global__ void __launch_bounds__(128) sweep_kernel(const SweepParams<S> p) {
             const S zi = fma_s(neg_s(dl), az, scale_s(sg, phi));
             const S wi = fma_s(neg_s(conj_s(dl)), aw, scale_s(conj_s(sg), phi));
             zw[static_cast<int64_t>(i) * ld + c] = ZW<S>{zi, wi};
+            dv = dv || bad_s(zi) || bad_s(wi);
             if (!sampling) continue;
 
             if (p.outputs & OUT_DIAG) {
@@ -114,6 +116,7 @@ __global__ void __launch_bounds__(128) sweep_kernel(const SweepParams<S> p) {
         v = group_sum(v, p.gs);
         if (leader && active) slot_add(p.slot_trace, g, v);
     }
+    if (dv && active) atomicAdd(p.bad, 1.0);
 }
 
 template <typename S>

@@ -60,6 +60,7 @@ __global__ void __launch_bounds__(NT, 1) sweep3_kernel(const Sweep3Params<S> p) 
     double *const sd = p.slot_diag + grp * p.n * E;
     double *const sp = p.slot_pat + grp * p.pcount * E;
     S tr = zero_s<S>();  // K == 1 only (trace runs use K = 1)
+    bool dv = false;     // divergence seen (reading R12)
 
     for (int s = p.s_begin; s < p.s_end; ++s) {
         const uint32_t k = p.sweep_abs0 + static_cast<uint32_t>(s);
@@ -105,6 +106,8 @@ __global__ void __launch_bounds__(NT, 1) sweep3_kernel(const Sweep3Params<S> p) 
                         out.v[h] = ZW<S>{zi[h], wi[h]};
                     }
                     st_zwk<S, K>(zrow(zcol, i, zst), out);
+#pragma unroll
+                    for (int h = 0; h < K; ++h) dv = dv | (active[h] & (bad_s(zi[h]) | bad_s(wi[h])));
                     if (want_full && sampling) {
                         const int64_t ts = s - p.snap_s0;
 #pragma unroll
@@ -161,6 +164,7 @@ __global__ void __launch_bounds__(NT, 1) sweep3_kernel(const Sweep3Params<S> p) 
         }
     }
 
+    if (dv) atomicAdd(p.bad, 1.0);
     if constexpr (K == 1) {
         if (want_tr) {
             // per-chain trace: sum over the threads of each chain, then over the P chains of a group
@@ -225,6 +229,7 @@ __global__ void __launch_bounds__(NT, 1) sweep4_kernel(const Sweep3Params<S> p) 
 
     for (int j = tid; j < p.n; j += B) done[j] = static_cast<unsigned char>(p.s_begin);
     __syncthreads();
+    bool dv = false;  // divergence seen (reading R12)
 
     const int R = 32 >> lgL;  // rows per warp group
     const int ngroups = p.nslots / R;
@@ -254,7 +259,7 @@ __global__ void __launch_bounds__(NT, 1) sweep4_kernel(const Sweep3Params<S> p) 
                 }
                 // wait for the lower neighbours (the first nlow entries; all lanes of the
                 // row read the same counters: smem broadcast), then acquire
-                const int nlow = rec.z >> 16;
+                const int nlow = static_cast<int>(static_cast<unsigned>(rec.z) >> 16);
                 for (int e = 0; e < nlow; ++e) {
                     const volatile unsigned char *f = done + __ldg(p.ent_col + beg + e);
                     wait_ready([&] { return *f == need; }, p.err, p.spin_ns);
@@ -273,6 +278,8 @@ __global__ void __launch_bounds__(NT, 1) sweep4_kernel(const Sweep3Params<S> p) 
                     out.v[h] = ZW<S>{zi[h], wi[h]};
                 }
                 st_zwk<S, K>(zrow(zcol, i, zst), out);
+#pragma unroll
+                for (int h = 0; h < K; ++h) dv = dv | (active[h] & (bad_s(zi[h]) | bad_s(wi[h])));
                 if (want_full && sampling) {
                     const int64_t ts = s - p.snap_s0;
 #pragma unroll
@@ -298,6 +305,7 @@ __global__ void __launch_bounds__(NT, 1) sweep4_kernel(const Sweep3Params<S> p) 
         }
         __syncthreads();  // sweep boundary: all reads of sweep s values are done
     }
+    if (dv) atomicAdd(p.bad, 1.0);
 }
 
 namespace {

@@ -87,7 +87,7 @@ __device__ __forceinline__ void accumulate_blk(const Sweep3Params<S> &p, const Z
         }
     }
     if (!want_pat) return;
-    const int nlow = acc ? rec.z >> 16 : 0;
+    const int nlow = acc ? static_cast<int>(static_cast<unsigned>(rec.z) >> 16) : 0;
     if constexpr (P == 1) {
         for (int e = 0; e < nlow; ++e) {
             const ZW<S> u = ld_zw(zrow(zcol, col[e], zst));
@@ -188,6 +188,7 @@ __global__ void __launch_bounds__(NT, 1) sweep5_kernel(const Sweep3Params<S> p) 
     if (lane == 0 && w < ngroups) issue(w, buf0, bar0);
     uint32_t ph0 = 0, ph1 = 0;
     int item = 0;
+    bool dv = false;  // divergence seen (reading R12: every stored value is a sweep-end value)
     for (int s = p.s_begin; s < p.s_end; ++s) {
         const uint32_t k = p.sweep_abs0 + static_cast<uint32_t>(s);
         const bool sampling = s >= p.burn_in;
@@ -218,7 +219,7 @@ __global__ void __launch_bounds__(NT, 1) sweep5_kernel(const Sweep3Params<S> p) 
             S zi = zero_s<S>(), wi = zero_s<S>();
             double phi = 0.0;
             if (valid) {
-                const int nlow = rec.z >> 16;
+                const int nlow = static_cast<int>(static_cast<unsigned>(rec.z) >> 16);
                 // upper neighbours hold their sweep s-1 values until this row publishes: start
                 // their lines on the way before the noise (its ALU time covers the latency)
                 if (p.prefetch) {  // all neighbours into L2 (the coherence point: safe for lower ones)
@@ -250,6 +251,7 @@ __global__ void __launch_bounds__(NT, 1) sweep5_kernel(const Sweep3Params<S> p) 
                 zi = fma_s(neg_s(dl), az, scale_s(sg, phi));
                 wi = fma_s(neg_s(conj_s(dl)), aw, scale_s(conj_s(sg), phi));
                 *zrow(zcol, i, zst) = ZW<S>{zi, wi};
+                dv = dv | bad_s(zi) | bad_s(wi);
                 if (want_full && sampling) {
                     const int64_t ts = s - p.snap_s0;
                     p.snap_x[(ts * p.n + i) * p.ld + chain] = zi;
@@ -278,6 +280,7 @@ __global__ void __launch_bounds__(NT, 1) sweep5_kernel(const Sweep3Params<S> p) 
         }
         __syncthreads();  // sweep boundary: all reads of sweep s values are done
     }
+    if (dv && active) atomicAdd(p.bad, 1.0);
 }
 
 size_t sweep5_smem(int n, int threads, int maxb) {

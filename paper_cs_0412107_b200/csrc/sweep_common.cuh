@@ -199,7 +199,7 @@ __device__ __forceinline__ void accumulate_row(const Sweep3Params<S> &p, const Z
     }
     if (!want_pat) return;
     // z_i w_j^* and z_j w_i^* for the lower neighbours j = col[beg + e], e < nlow
-    const int nlow = any ? rec.z >> 16 : 0;
+    const int nlow = any ? static_cast<int>(static_cast<unsigned>(rec.z) >> 16) : 0;
     if constexpr (P == 1) {
         for (int e = 0; e < nlow; ++e) {
             const ZWK<S, K> u = ld_zwk<S, K>(zrow(zcol, __ldg(p.ent_col + beg + e), zst));

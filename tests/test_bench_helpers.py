@@ -31,3 +31,26 @@ def test_committed_ncu_summary_is_complete():
     assert 5 < s["warp_inst_per_site"] < 100
     assert bench.committed_traffic(W.CONFIGS[2]["name"]) == s["dram_bytes_per_site"]
     assert bench.committed_summary("no such workload") == {}
+
+
+def test_config5_bytes_include_the_trace_gathers():
+    # config 5 352 B/site = 16 (8 + 8 + 2) + 16 x 4 Q gathers (288 without Q)
+    c5, q5, _ = W.config(5)
+    assert bench.algorithmic_bytes_per_chain_sweep(c5) / c5.n == 288
+    assert bench.algorithmic_bytes_per_chain_sweep(c5, q5) / c5.n == 352
+
+
+def test_scaling_modes_shard_the_chains():
+    """Weak: the config's chains on every rank; strong (default for configs 4
+    and 5): BASELINE's total split by whole SE groups, covering it once."""
+    for k, total in ((4, 8192), (5, 16384)):
+        a = bench.parse(["--config", str(k), "--gpus", "8"])
+        assert bench.scaling_mode(a) == "strong"
+        _, _, run = W.config(k)
+        got = [bench.shard_of(a, run, 8, r) for r in range(8)]
+        assert all(t == total for _, _, t in got) and sum(ch for _, ch, _ in got) == total
+        assert [cb for cb, _, _ in got] == [r * total // 8 for r in range(8)]
+    a = bench.parse(["--gpus", "4"])
+    assert bench.scaling_mode(a) == "weak"
+    _, _, run = W.config(2)
+    assert bench.shard_of(a, run, 4, 3) == (3 * 1024, 1024, 4096)

@@ -70,8 +70,9 @@ def compare_run(mc, orc, c, q=None, pattern=None, seed=1, chains=64, burn_in=5, 
         eg, sg = res[o]
         est_match(eg, eo, what=o)
         if chains // group_size >= 2:
-            # SE via sum of squares (GPU) vs two-pass (oracle): cancellation-limited
-            assert normwise(sg, so) < 1e-6, f"{o} SE {normwise(sg, so)}"
+            # both two-pass about the groups' mean (GPU: moments_kernel; oracle: np.std); they
+            # differ only by the summation order of the group sums (atomics)
+            assert normwise(sg, so) < 1e-10, f"{o} SE {normwise(sg, so)}"
     inv.close()
     return res
 
@@ -222,7 +223,8 @@ def test_sharding_invariance_and_resume(mc):
         parts.append(b.accumulators().cpu().numpy().copy())
         zb, wb = b.get_state()
         assert np.array_equal(zb, z_all[cb:cb + 64]) and np.array_equal(wb, w_all[cb:cb + 64])
-    np.testing.assert_allclose(parts[0] + parts[1], full, rtol=1e-12, atol=1e-300)
+    nS1 = (full.size - 1) // 2  # [S1 | M2 | divergence]: the S1 blocks of the shards add up
+    np.testing.assert_allclose(parts[0][:nS1] + parts[1][:nS1], full[:nS1], rtol=1e-12, atol=1e-300)
     # resume: 8 sweeps == 3 + 5
     b.run(9, 128, 3, 0, ("diag",), group_size=32)
     b.run(9, 128, 0, 5, ("diag",), group_size=32, sweep_begin=3, resume=True)

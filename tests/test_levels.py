@@ -140,3 +140,25 @@ def test_v4_slot_schedule(mc, make, R, L):
     # every group holds at least one row (padding only completes groups)
     assert slots.size <= R * c.n
     assert np.all((slots.reshape(-1, R) >= 0).any(axis=1))
+
+
+def test_arrow_row_with_many_lower_neighbours(mc):
+    """A row with more than 32767 lower neighbours (an arrow matrix: the last
+    row and column couple to every earlier row). Its record packs the lower
+    count in the upper 16 bits; decoded as unsigned, the planner still places
+    every row exactly once and the arrow row after all of them (a signed
+    decode would make the count negative: the row never becomes ready)."""
+    n = 40001
+    rows = np.concatenate([np.arange(n), np.full(n - 1, n - 1), np.arange(n - 1)])
+    cols = np.concatenate([np.arange(n), np.arange(n - 1), np.full(n - 1, n - 1)])
+    vals = np.concatenate([np.full(n, 4.0), np.full(n - 1, -1e-5), np.full(n - 1, -2e-5)])
+    order = np.lexsort((cols, rows))
+    rp = np.zeros(n + 1, np.int64)
+    np.add.at(rp, rows + 1, 1)
+    c = W.CSR(n, np.cumsum(rp), cols[order].astype(np.int32), vals[order])
+    lev, info = mc.debug_levels(c, slot_R=4, slot_L=8)
+    assert info["levels"] == 2 and lev[-1] == 1 and not lev[:-1].any()
+    slots = info["slots"]
+    placed = slots[slots >= 0]
+    assert np.array_equal(np.sort(placed), np.arange(n))
+    assert np.nonzero(slots == n - 1)[0][0] // 4 > np.max(np.nonzero((slots >= 0) & (slots < n - 1))[0]) // 4

@@ -91,6 +91,23 @@ def test_box_muller_closed_forms(orc):
     assert orc.gaussian_from_words(w) == pytest.approx(np.sqrt(2 * np.log(2)) * np.sqrt(0.5), rel=1e-15)
 
 
+def test_gaussian_counter_layout(orc):
+    """Reading R4's counter layout, pinned on the CPU: the noise of (chain c,
+    sweep k, row i) is Box-Muller of the Philox block of counter {i, k, c, 0}
+    under key {seed lo, seed hi} -- composed here from the two separately
+    pinned pieces (KAT-pinned Philox, closed-form-pinned Box-Muller), so a
+    swapped or misplaced counter word inside orc_gaussian fails."""
+    rng = np.random.default_rng(11)
+    for seed in (0, 0x5EED0002, 2**64 - 1, 0x123456789ABCDEF):
+        key = [seed & 0xFFFFFFFF, seed >> 32]
+        for i, k, c in rng.integers(0, 2**32, size=(40, 3), dtype=np.uint64).tolist() + [[0, 0, 0], [5, 0, 1]]:
+            want = orc.gaussian_from_words(orc.philox([i, k, c, 0], key))
+            assert orc.gaussian(seed, i, k, c) == want
+            # a transposed layout gives a different value
+            if len({i, k, c}) == 3:
+                assert orc.gaussian(seed, i, k, c) != orc.gaussian_from_words(orc.philox([k, i, c, 0], key))
+
+
 def test_gaussian_is_standard_normal(orc):
     """E(Phi) = 0, E(Phi Phi^T) = I (Eq. 5a/5b)."""
     from scipy import stats
