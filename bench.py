@@ -238,16 +238,17 @@ def committed_traffic(workload: str):
 
 
 KERNELS = {3: "sweep3_kernel (v3, level barriers)", 4: "sweep4_kernel (v4, dataflow)",
-           5: "sweep5_kernel (v5, dataflow + TMA-staged plan blocks)", 1: "sweep_kernel (v1)"}
+           5: "sweep5_kernel (v5, dataflow + TMA-staged plan blocks)",
+           6: "sweep6_kernel (v6, dataflow + TMA-staged plan blocks, two chains per thread)",
+           1: "sweep_kernel (v1)"}
 
 
 def sweep_roofline(name, c, q, outputs, chains, sweeps, st, kinfo, lconf, clk, sms_total):
     """Roofline of the sweep kernel K1 over its launches: achieved algorithmic bytes
      per launch / launch time against the measured HBM peak, and the
     instruction-issue ceiling from the committed ncu warp instructions per
-    site. `bound` is the binding one: "hbm" when ncu's DRAM bandwidth at this rate
-    is at least half the peak, else "issue" (the sweep then waits on instruction
-    issue and latency, not on HBM)."""
+    site. `bound` names the nearer of the two ceilings (the larger fraction); the
+    other stays in the object, with ncu's actual DRAM bandwidth at this rate."""
     launch_ms = st["sweep_ms"] / max(st["sweep_launches"], 1)
     per_launch_sweeps = sweeps / max(st["sweep_launches"], 1)
     sites_launch = chains * c.n * per_launch_sweeps
@@ -276,7 +277,7 @@ def sweep_roofline(name, c, q, outputs, chains, sweeps, st, kinfo, lconf, clk, s
         out["issue"] = issue
     dram_frac = (tps * rate / 1e9 / peak) if tps else None
     out["dram_frac_of_peak"] = dram_frac
-    if issue is not None and dram_frac is not None and dram_frac < 0.5:
+    if issue is not None and issue["frac"] > hbm["frac"]:
         out.update(bound="issue", achieved=issue["achieved"], peak=issue["peak"], unit="warp-inst/s",
                    frac=issue["frac"])
     else:

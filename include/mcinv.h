@@ -104,6 +104,10 @@ typedef struct {
                                NULL to let the library allocate (and own) it */
     size_t workspace_bytes;
     void *stream;           /* cudaStream_t; NULL = legacy default stream */
+    int64_t trace_series;   /* MCINV_TRACE: capacity (sampling sweeps since the fresh run) of the
+                               series of realized traces, one per sampling sweep summed over the
+                               run's chains, for Geyer's effective length (mcinv_geyer); 0 = off.
+                               A resumed run must pass the capacity of the run it continues. */
 } mcinv_run_args;
 
 /* Device workspace needed by mcinv_run with these arguments (state Z/W,
@@ -142,6 +146,28 @@ mcinv_status mcinv_coupled_burn_in(mcinv_ctx *ctx, double tol, int64_t max_sweep
  * Synchronizes; mcinv_result then reads the final estimate. */
 mcinv_status mcinv_run_until(mcinv_ctx *ctx, const mcinv_run_args *args, unsigned output, double rel_se,
                              int64_t check_cycles, int64_t max_cycles, int64_t *cycles_done, double *rel_se_out);
+
+/* Geyer's effective sample size of the trace (the paper's standard
+ * errors): from the series of realized traces w^dagger Q z, one value per
+ * sampling sweep since the last fresh run summed over the run's chains (a run
+ * with MCINV_TRACE and trace_series > 0), Geyer's initial positive sequence
+ * estimator gives per component (re; and im for C128) out[4c .. 4c+3] =
+ * {series mean, gamma_0, sigma2 = M Var(series mean), effective length
+ * M gamma_0 / sigma2}, M = the sampling sweeps so far. The trace estimate is
+ * mean / chains with Geyer standard error sqrt(sigma2 / M) / chains.
+ * Synchronizes. Errors: E_STATE (no series: TRACE with trace_series = 0, or no
+ * sampling sweep yet), E_INVALID (null out). */
+mcinv_status mcinv_geyer(mcinv_ctx *ctx, double *out);
+
+/* Adaptive stopping with the paper's rule: run `args` (burn_in
+ * included, args->cycles ignored, TRACE required) and resume in blocks of
+ * check_cycles (the paper: 100) until the trace's Geyer relative standard
+ * error |SE| / |estimate| (moduli for complex; SE from mcinv_geyer)
+ * is below rel_se, or max_cycles sampling sweeps are done. *cycles_done and
+ * *rel_se_out (may be NULL) receive the sweeps run and the final relative SE.
+ * The series capacity is max_cycles. Synchronizes. */
+mcinv_status mcinv_run_until_geyer(mcinv_ctx *ctx, const mcinv_run_args *args, double rel_se, int64_t check_cycles,
+                                   int64_t max_cycles, int64_t *cycles_done, double *rel_se_out);
 
 /* Borrowed device pointer to the moment vector of the last run, for an
  * all-reduce (SUM, float64) across GPUs that ran disjoint chain ranges:
@@ -225,7 +251,9 @@ mcinv_status mcinv_launch_config(const mcinv_ctx *ctx, int *threads, int *chains
  * (host), key = seed; out4[4*count] host. */
 mcinv_status mcinv_debug_philox(int device, uint64_t seed, int64_t count, const uint32_t *ctr4,
                                 uint32_t *out4);
-/* Box-Muller Gaussian of Philox(ctr, seed) for each counter (host arrays). */
+/* The sweep kernels' Gaussian noise phi(row = ctr4[4t], sweep = ctr4[4t+1], chain =
+ * ctr4[4t+2]) for each t (ctr4[4t+3] ignored): output chain%2 of the Box-Muller pair
+ * of Philox({row, sweep, chain/2, 0}, seed) (reading R4). Host arrays. */
 mcinv_status mcinv_debug_gaussian(int device, uint64_t seed, int64_t count, const uint32_t *ctr4,
                                   double *out);
 /* Host-only (no GPU needed): mcinv_create's preprocessing and the level

@@ -57,6 +57,8 @@ def lib():
         L.orc_philox4x32_10.restype = None
         L.orc_gaussian_from_words.argtypes = [u32p]
         L.orc_gaussian_from_words.restype = ctypes.c_double
+        L.orc_gaussian_pair_from_words.argtypes = [u32p, P(ctypes.c_double)]
+        L.orc_gaussian_pair_from_words.restype = None
         L.orc_gaussian.argtypes = [ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32]
         L.orc_gaussian.restype = ctypes.c_double
         L.orc_z2.argtypes = [ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32]
@@ -66,7 +68,9 @@ def lib():
         L.orc_matrix_free.argtypes = [ctypes.c_void_p]
         L.orc_set_q.argtypes = [ctypes.c_void_p] * 4
         L.orc_set_pattern.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]
-        L.orc_run.argtypes = [ctypes.c_void_p, ctypes.c_void_p] + [ctypes.c_void_p] * 8 + \
+        L.orc_geyer.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p]
+        L.orc_geyer.restype = None
+        L.orc_run.argtypes = [ctypes.c_void_p, ctypes.c_void_p] + [ctypes.c_void_p] * 9 + \
             [ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
         _lib = L
     return _lib
@@ -93,6 +97,13 @@ def philox(ctr, key) -> np.ndarray:
 def gaussian_from_words(r) -> float:
     w = (ctypes.c_uint32 * 4)(*[int(x) & 0xFFFFFFFF for x in r])
     return lib().orc_gaussian_from_words(w)
+
+
+def gaussian_pair_from_words(r):
+    w = (ctypes.c_uint32 * 4)(*[int(x) & 0xFFFFFFFF for x in r])
+    g = (ctypes.c_double * 2)()
+    lib().orc_gaussian_pair_from_words(w, g)
+    return g[0], g[1]
 
 
 def gaussian(seed: int, row: int, sweep: int, chain: int) -> float:
@@ -161,6 +172,7 @@ class Matrix:
         pat = np.zeros((ch, self.pcount), dt) if bits & PATTERN else None
         full = np.zeros((ch, n, n), dt) if bits & FULL else None
         trace = np.zeros((ch,), dt) if bits & TRACE else None
+        series = np.zeros((max(cycles, 1),), dt) if bits & TRACE else None
         zo = np.zeros((ch, n), dt)
         wo = np.zeros((ch, n), dt)
         snaps = np.asarray(list(snap_sweeps), np.int64)
@@ -172,11 +184,12 @@ class Matrix:
             wi = np.ascontiguousarray(np.broadcast_to(np.asarray(w_init, dt), (ch, n)))
         fail = np.zeros(2, np.int64)
         st = lib().orc_run(self.h, ctypes.byref(a), _ptr(zi), _ptr(wi), _ptr(diag), _ptr(pat), _ptr(full),
-                           _ptr(trace), zo.ctypes.data, wo.ctypes.data, snaps.size, _ptr(snaps),
+                           _ptr(trace), _ptr(series), zo.ctypes.data, wo.ctypes.data, snaps.size, _ptr(snaps),
                            zs.ctypes.data, ws.ctypes.data, fail.ctypes.data)
         if st:
             raise OracleError(st, f"chain {fail[0]} sweep {fail[1]}")
-        return dict(diag=diag, pattern=pat, full=full, trace=trace, z=zo, w=wo, z_snap=zs, w_snap=ws)
+        return dict(diag=diag, pattern=pat, full=full, trace=trace, z=zo, w=wo, z_snap=zs, w_snap=ws,
+                    trace_series=series[:cycles] if series is not None else None)
 
 
 def estimate(sums: np.ndarray, cycles: int, group_size: int = 1, chain_begin: int = 0):
@@ -195,3 +208,14 @@ def estimate(sums: np.ndarray, cycles: int, group_size: int = 1, chain_begin: in
     else:
         se = np.std(g, axis=0, ddof=1) / np.sqrt(G)
     return est, se
+
+
+def geyer(x) -> dict:
+    """Geyer's initial positive sequence estimator (orc_geyer) of a real
+    series: mean, gamma_0, sigma2 (= m Var(mean)), effective length, and the
+    standard error of the mean sqrt(sigma2 / m) = sqrt(gamma_0 / ESS)."""
+    x = np.ascontiguousarray(x, np.float64)
+    out = np.zeros(4)
+    lib().orc_geyer(x.ctypes.data, x.size, out.ctypes.data)
+    return dict(mean=out[0], gamma0=out[1], sigma2=out[2], ess=out[3],
+                se=np.sqrt(out[2] / x.size) if out[2] > 0 else 0.0)

@@ -62,15 +62,34 @@ double orc_gaussian_from_words(const uint32_t r[4])
     return sqrt(-2.0 * log(u1)) * cos(6.283185307179586 * u2);
 }
 
+/* Both outputs of the Box-Muller transform of one block (Box & Muller 1958:
+ * two independent N(0,1) from one pair of uniforms; reading R4):
+ *   g[0] = sqrt(-2 ln u1) cos(2 pi u2),  g[1] = sqrt(-2 ln u1) sin(2 pi u2). */
+void orc_gaussian_pair_from_words(const uint32_t r[4], double g[2])
+{
+    uint64_t a = ((uint64_t)r[0] << 32) | (uint64_t)r[1];
+    uint64_t b = ((uint64_t)r[2] << 32) | (uint64_t)r[3];
+    double u1 = (double)((a >> 11) + 1u) * 0x1p-53;
+    double u2 = (double)(b >> 11) * 0x1p-53;
+    double rad = sqrt(-2.0 * log(u1));
+    g[0] = rad * cos(6.283185307179586 * u2);
+    g[1] = rad * sin(6.283185307179586 * u2);
+}
+
 /* One real N(0,1) per (chain, sweep, row), shared by z_i and w_i: "the noise
- * term in (4) and in (5) are both the same". */
+ * term in (4) and in (5) are both the same". Chains 2m and 2m+1
+ * take the two outputs of one Box-Muller pair, from the Philox block of
+ * counter {row, sweep, m, 0} (reading R4): independent N(0,1), as Eq. (5a/5b)
+ * require across chains. */
 double orc_gaussian(uint64_t seed, uint32_t row, uint32_t sweep, uint32_t chain)
 {
     uint32_t ctr[4], key[2], r[4];
-    ctr[0] = row; ctr[1] = sweep; ctr[2] = chain; ctr[3] = 0u;
+    double g[2];
+    ctr[0] = row; ctr[1] = sweep; ctr[2] = chain >> 1; ctr[3] = 0u;
     key[0] = (uint32_t)seed; key[1] = (uint32_t)(seed >> 32);
     orc_philox4x32_10(ctr, key, r);
-    return orc_gaussian_from_words(r);
+    orc_gaussian_pair_from_words(r, g);
+    return g[chain & 1u];
 }
 
 /* Z2 noise, the paper's preferred bounded noise "phi = 2B - 1" with B a
@@ -360,7 +379,7 @@ static void put(double *dst, int64_t idx, cx v, int cplx)
  * reading R2), instead of the printed z^dagger Q w. */
 int orc_run(const orc_matrix *m, const orc_args *a,
             const double *z_init, const double *w_init,
-            double *diag, double *pat, double *full, double *trace,
+            double *diag, double *pat, double *full, double *trace, double *trace_series,
             double *z_out, double *w_out,
             int64_t n_snap, const int64_t *snap_sweeps, double *z_snap, double *w_snap,
             int64_t fail[2])
@@ -422,6 +441,8 @@ int orc_run(const orc_matrix *m, const orc_args *a,
                     t.re += wc.re; t.im += wc.im;
                 }
                 put(trace, ci, t, m->cplx);
+                /* the realized value of this sampling sweep, summed over the run's chains */
+                if (trace_series) put(trace_series, s - a->burn_in, t, m->cplx);
             }
         }
         if (z_out && w_out) {
@@ -433,4 +454,45 @@ int orc_run(const orc_matrix *m, const orc_args *a,
     }
     free(z); free(w);
     return ORC_OK;
+}
+
+/* ------------------------------------------------------------ Geyer ----- */
+
+/* Effective sample size of a serially correlated series x[0..m-1] by Geyer's
+ * initial positive sequence estimator (Geyer 1992, "Practical Markov chain
+ * Monte Carlo", the method the paper uses for its standard errors, P:354-360,
+ * P:553-557): with the mean xbar and the lag-k autocovariances
+ *   gamma_k = (1/m) sum_{t=0}^{m-1-k} (x_t - xbar)(x_{t+k} - xbar),
+ * the pair sums Gamma_j = gamma_{2j} + gamma_{2j+1} are summed for
+ * j = 0, 1, ... while positive (stopping before the first Gamma_j <= 0 or when
+ * 2j + 1 reaches m), the asymptotic variance of the mean times m is
+ *   sigma2 = -gamma_0 + 2 sum_j Gamma_j,
+ * and ESS = m gamma_0 / sigma2, so that SE(mean) = sqrt(gamma_0 / ESS) =
+ * sqrt(sigma2 / m) (the paper's "MC St. error" = sqrt(Var / Eff. length),
+ * Table 2). out = {xbar, gamma_0, sigma2, ESS}. */
+void orc_geyer(const double *x, int64_t m, double out[4])
+{
+    int64_t t, k, j;
+    double xbar = 0.0, g0, sigma2;
+    for (t = 0; t < m; ++t) xbar += x[t];
+    xbar /= (double)m;
+    g0 = 0.0;
+    for (t = 0; t < m; ++t) g0 += (x[t] - xbar) * (x[t] - xbar);
+    g0 /= (double)m;
+    sigma2 = -g0;
+    for (j = 0; 2 * j + 1 < m; ++j) {
+        double gam[2];
+        for (k = 0; k < 2; ++k) {
+            int64_t lag = 2 * j + k;
+            double acc = 0.0;
+            for (t = 0; t + lag < m; ++t) acc += (x[t] - xbar) * (x[t + lag] - xbar);
+            gam[k] = acc / (double)m;
+        }
+        if (!(gam[0] + gam[1] > 0.0)) break;
+        sigma2 += 2.0 * (gam[0] + gam[1]);
+    }
+    out[0] = xbar;
+    out[1] = g0;
+    out[2] = sigma2;
+    out[3] = sigma2 > 0.0 ? (double)m * g0 / sigma2 : 0.0;
 }

@@ -32,7 +32,11 @@ void orc_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t ou
 /* Box-Muller transform of one Philox output block (reading R4). */
 double orc_gaussian_from_words(const uint32_t r[4]);
 
-/* phi(c,k,i) = Gaussian(Philox(ctr={row, sweep, chain, 0}, key=seed)). */
+/* Both Box-Muller outputs of one block: g[0] the cosine, g[1] the sine branch. */
+void orc_gaussian_pair_from_words(const uint32_t r[4], double g[2]);
+
+/* phi(c,k,i) = Box-Muller pair of Philox(ctr={row, sweep, chain/2, 0}, key=seed),
+ * the cosine output for even chains, the sine output for odd ones (reading R4). */
 double orc_gaussian(uint64_t seed, uint32_t row, uint32_t sweep, uint32_t chain);
 
 /* Z2 noise phi = +-1 (reading R21): the top bit of
@@ -68,16 +72,22 @@ typedef struct {
  *   pat   [chains][count]                            sum_k z_i conj(w_j)
  *   full  [chains][n][n]                             sum_k z conj(w)^T
  *   trace [chains]                                   sum_k w^dagger Q z
+ *   trace_series [cycles]   the realized w^dagger Q z of each sampling sweep,
+ *                           summed over the run's chains (Geyer's series)
  * Any of them may be NULL when not requested. z_out/w_out [chains][n]
  * receive the final state. snap_sweeps (n_snap local sweep indices s, the
  * state after sweep s completes) fill z_snap/w_snap [n_snap][chains][n].
  * On divergence returns ORC_E_DIVERGED with *fail (chain, sweep) set. */
 int orc_run(const orc_matrix *m, const orc_args *a,
             const double *z_init, const double *w_init,
-            double *diag, double *pat, double *full, double *trace,
+            double *diag, double *pat, double *full, double *trace, double *trace_series,
             double *z_out, double *w_out,
             int64_t n_snap, const int64_t *snap_sweeps, double *z_snap, double *w_snap,
             int64_t fail[2]);
+
+/* Geyer's initial positive sequence estimator of a series:
+ * out = {mean, gamma_0, sigma2 = m Var(mean), effective length m gamma_0 / sigma2}. */
+void orc_geyer(const double *x, int64_t m, double out[4]);
 
 #ifdef __cplusplus
 }

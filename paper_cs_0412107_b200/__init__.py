@@ -43,7 +43,7 @@ class _RunArgs(ctypes.Structure):
                 ("burn_in", ctypes.c_int64), ("cycles", ctypes.c_int64), ("sweep_begin", ctypes.c_int64),
                 ("outputs", ctypes.c_uint), ("noise", ctypes.c_int), ("group_size", ctypes.c_int),
                 ("resume", ctypes.c_int), ("snapshot_sweeps", ctypes.c_int), ("workspace", ctypes.c_void_p),
-                ("workspace_bytes", ctypes.c_size_t), ("stream", ctypes.c_void_p)]
+                ("workspace_bytes", ctypes.c_size_t), ("stream", ctypes.c_void_p), ("trace_series", ctypes.c_int64)]
 
 
 SYMBOLS = {
@@ -68,6 +68,10 @@ SYMBOLS = {
     "mcinv_run_status": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64)]),
     "mcinv_debug_group_sums": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_uint, ctypes.c_int64, ctypes.c_int64,
                                               ctypes.c_void_p]),
+    "mcinv_geyer": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p]),
+    "mcinv_run_until_geyer": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(_RunArgs), ctypes.c_double,
+                                             ctypes.c_int64, ctypes.c_int64, ctypes.POINTER(ctypes.c_int64),
+                                             ctypes.POINTER(ctypes.c_double)]),
     "mcinv_status_string": (ctypes.c_char_p, [ctypes.c_int]),
     "mcinv_error_detail": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64),
                                           ctypes.POINTER(ctypes.c_char_p)]),
@@ -218,12 +222,12 @@ class Inverter:
 
     # ------------------------------------------------------------------ run
     def _make_args(self, seed, chains, burn_in, cycles, outputs, chain_begin, sweep_begin, group_size, noise,
-                   resume, snapshot_sweeps, stream) -> _RunArgs:
+                   resume, snapshot_sweeps, stream, trace_series=0) -> _RunArgs:
         bits = 0
         for o in outputs:
             bits |= OUTPUTS[o]
         return _RunArgs(seed & 0xFFFFFFFFFFFFFFFF, chain_begin, chains, burn_in, cycles, sweep_begin, bits,
-                        NOISE[noise], group_size, int(resume), snapshot_sweeps, None, 0, stream)
+                        NOISE[noise], group_size, int(resume), snapshot_sweeps, None, 0, stream, trace_series)
 
     def workspace_size(self, **kw) -> int:
         a = self._make_args(**self._defaults(kw))
@@ -240,15 +244,16 @@ class Inverter:
 
     def run(self, seed: int, chains: int, burn_in: int, cycles: int, outputs: Sequence[str] = ("diag",),
             chain_begin: int = 0, sweep_begin: int = 0, group_size: int = 32, noise: str = "gauss",
-            resume: bool = False, snapshot_sweeps: int = 0, stream=None) -> "Inverter":
+            resume: bool = False, snapshot_sweeps: int = 0, stream=None, trace_series: int = 0) -> "Inverter":
         """Enqueue one run (Alg. 1, fixed burn-in) on ``stream`` (torch stream or
-        None = current). Returns self; read results with ``result``."""
+        None = current). Returns self; read results with ``result``. trace_series > 0
+        (with "trace") keeps the per-sweep realized traces for ``geyer``."""
         torch = self._torch
         if stream is None:
             stream = torch.cuda.current_stream(self.device)
         sp = stream.cuda_stream if hasattr(stream, "cuda_stream") else stream
         a = self._make_args(seed, chains, burn_in, cycles, tuple(outputs), chain_begin, sweep_begin, group_size,
-                            noise, resume, snapshot_sweeps, sp)
+                            noise, resume, snapshot_sweeps, sp, trace_series)
         b = ctypes.c_size_t()
         _check(load().mcinv_workspace_size(self._h, ctypes.byref(a), ctypes.byref(b)), self._h)
         need = max(int(b.value), 256)
@@ -264,6 +269,7 @@ class Inverter:
         self.outputs = tuple(outputs)
         self.chains = chains
         self.cycles = cycles
+        self.acc_cycles = (getattr(self, "acc_cycles", 0) + cycles) if resume else cycles
         self.group_size = group_size
         return self
 
@@ -306,7 +312,52 @@ class Inverter:
         self._args = a
         self.outputs = tuple(outputs)
         self.chains = chains
-        self.cycles = done.value
+        self.cycles = self.acc_cycles = done.value
+        self.group_size = group_size
+        return done.value, rse.value
+
+    def geyer(self) -> dict:
+        """mcinv_geyer: Geyer's effective length of the trace series; per
+        component (re, im): series mean, gamma_0, sigma2, ess; plus the trace estimate
+        and its Geyer standard error."""
+        out = np.zeros(8)
+        _check(load().mcinv_geyer(self._h, out.ctypes.data), self._h)
+        m = self.acc_cycles
+        comps = []
+        for c in range(self.e):
+            mean, g0, s2, ess = out[4 * c:4 * c + 4]
+            comps.append(dict(mean=mean, gamma0=g0, sigma2=s2, ess=ess,
+                              se=np.sqrt(s2 / m) / self.chains if s2 > 0 else 0.0, estimate=mean / self.chains))
+        return dict(re=comps[0], im=comps[1] if self.e == 2 else None)
+
+    def run_until_geyer(self, seed: int, chains: int, burn_in: int, outputs: Sequence[str], rel_se: float,
+                        check_cycles: int = 100, max_cycles: int = 100000, group_size: int = 32,
+                        chain_begin: int = 0, noise: str = "gauss", stream=None):
+        """The paper's stopping rule (mcinv_run_until_geyer): blocks of check_cycles
+        sampling sweeps until the trace's Geyer relative SE is below rel_se. Returns
+        (cycles run, relative SE)."""
+        torch = self._torch
+        if stream is None:
+            stream = torch.cuda.current_stream(self.device)
+        sp = stream.cuda_stream if hasattr(stream, "cuda_stream") else stream
+        a = self._make_args(seed, chains, burn_in, check_cycles, tuple(outputs), chain_begin, 0, group_size, noise,
+                            False, 0, sp, max_cycles)
+        b = ctypes.c_size_t()
+        _check(load().mcinv_workspace_size(self._h, ctypes.byref(a), ctypes.byref(b)), self._h)
+        need = max(int(b.value), 256)
+        if self._ws is None or self._ws.numel() < need:
+            self._ws = None
+            self._ws = torch.empty(need, dtype=torch.uint8, device=f"cuda:{self.device}")
+        a.workspace = self._ws.data_ptr()
+        a.workspace_bytes = self._ws.numel()
+        done = ctypes.c_int64()
+        rse = ctypes.c_double()
+        _check(load().mcinv_run_until_geyer(self._h, ctypes.byref(a), rel_se, check_cycles, max_cycles,
+                                            ctypes.byref(done), ctypes.byref(rse)), self._h)
+        self._args = a
+        self.outputs = tuple(outputs)
+        self.chains = chains
+        self.cycles = self.acc_cycles = done.value
         self.group_size = group_size
         return done.value, rse.value
 

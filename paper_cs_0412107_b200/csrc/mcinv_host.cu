@@ -17,6 +17,7 @@
 #include <map>
 #include <memory>
 #include <tuple>
+#include <type_traits>
 
 #include "../../include/mcinv.h"
 #include "mcinv_internal.cuh"
@@ -71,7 +72,8 @@ struct LevelDev {
         DevBuf blob, gofs;
         int maxb = 0;
     };
-    std::map<int, std::unique_ptr<Slots>> slots;  // (rows per warp group R, warps W) -> slot arrays
+    // (rows per warp group R, warps W, TMA blocks, entry padding, block entry cap) -> slot arrays
+    std::map<std::tuple<int, int, int, int, int>, std::unique_ptr<Slots>> slots;
 };
 
 struct Layout {
@@ -81,6 +83,8 @@ struct Layout {
     int ld = 0, G = 0, T = 0;
     int e = 1;              // doubles per scalar
     size_t zw = 0, slot_diag = 0, slot_pat = 0, slot_full = 0, slot_trace = 0, snap_x = 0, snap_y = 0, mom = 0;
+    size_t series = 0;      // TRACE: Geyer's series [series_cap][e] (0 bytes when off)
+    int64_t series_cap = 0;
     size_t mom_count = 0;   // doubles in the moment vector
     size_t mom_diag = 0, mom_pat = 0, mom_full = 0, mom_trace = 0;  // offsets (doubles) of S1 in moments
     size_t mom_m2 = 0;      // offset (doubles) of the M2 block: M2 of an output at mom_<output> + mom_m2
@@ -434,11 +438,13 @@ mcinv_status check_args(const mcinv_ctx *ctx_c, const mcinv_run_args *a) {
     if (a->outputs & ~15u) return fail(ctx, MCINV_E_INVALID, "unknown output bit");
     if ((a->outputs & MCINV_TRACE) && !ctx->have_q) return fail(ctx, MCINV_E_STATE, "TRACE needs mcinv_set_trace_q");
     if (a->noise < 0 || a->noise > 3) return fail(ctx, MCINV_E_INVALID, "noise mode");
+    if (a->trace_series < 0 || a->trace_series > (int64_t(1) << 31))
+        return fail(ctx, MCINV_E_INVALID, "trace_series capacity");
     if (a->chains > (int64_t(1) << 30)) return fail(ctx, MCINV_E_INVALID, "too many chains for one call");
     return MCINV_OK;
 }
 
-int kernel_pref() {  // 0 auto, 1 force v1, 3 force v3, 4 force v4, 5 force v5
+int kernel_pref() {  // 0 auto, 1 force v1, 3 force v3, 4 force v4, 5 force v5, 6 force v6
     const char *e = std::getenv("MCINV_KERNEL");
     if (!e) return 0;
     const char *d = e[0] == 'v' ? e + 1 : e;  // "v3" or "3"
@@ -446,6 +452,7 @@ int kernel_pref() {  // 0 auto, 1 force v1, 3 force v3, 4 force v4, 5 force v5
     if (!std::strcmp(d, "3")) return 3;
     if (!std::strcmp(d, "4")) return 4;
     if (!std::strcmp(d, "5")) return 5;
+    if (!std::strcmp(d, "6")) return 6;
     return 0;
 }
 
@@ -548,6 +555,10 @@ Layout make_layout(const mcinv_ctx *ctx, const mcinv_run_args *a) {
     if (a->outputs & MCINV_PATTERN) L.slot_pat = take((size_t)L.Gs * std::max<int64_t>(ctx->pcount, 1) * sz);
     if (a->outputs & MCINV_FULL) L.slot_full = take((size_t)L.G * n * n * sz);
     if (a->outputs & MCINV_TRACE) L.slot_trace = take((size_t)L.Gs * sz);
+    if ((a->outputs & MCINV_TRACE) && a->trace_series > 0) {
+        L.series_cap = a->trace_series;
+        L.series = take((size_t)a->trace_series * sz);
+    }
     size_t m = 0;
     // moment vector: S1 of every output, then M2 of every output (same order), then the
     // divergence count (mcinv_accumulators)
@@ -663,10 +674,28 @@ int block_entries() {  // MCINV_BLOCK_ENTRIES overrides (experiments)
     return e ? std::atoi(e) : kBlockEntries;
 }
 constexpr bool kV5Default = true;  // v5 by default where it applies (measured: config 2 +5%, config 3 +24%)
+// v6 (two chains per thread) by default where it applies (MCINV_V6=0/1 overrides); its
+// threads per CTA (MCINV_V6_THREADS)
+bool v6_default() {  // config 2: 2.55 -> 2.77e10 site-updates/s over v5 (profiles/r02_v6*.log)
+    const char *e = std::getenv("MCINV_V6");
+    return e ? std::atoi(e) != 0 : true;
+}
+int v6_threads() {  // 512 (128 registers: the gathers of 4 entries of both chains in flight) measured best
+    const char *e = std::getenv("MCINV_V6_THREADS");
+    return e ? std::atoi(e) : 512;
+}
 
+// pad_ku: each row's entries in a block padded to a multiple of the kernel's gather unroll
+// (0: the scalar type's default); ecap: entries per warp-group block (0: block_entries())
+// wmask (v6): each row of a block also carries a 32-bit mask of the lower-neighbour
+// entries it must wait for (see below)
 template <typename S>
-LevelDev::Slots *get_slots(mcinv_ctx *ctx, LevelDev *lv, int R, int W, bool blocks) {
-    auto it = lv->slots.find(R * 4096 + W + (blocks ? (1 << 28) : 0));
+LevelDev::Slots *get_slots(mcinv_ctx *ctx, LevelDev *lv, int R, int W, bool blocks, int pad_ku = 0, int ecap = 0,
+                           bool wmask = false) {
+    if (ecap <= 0) ecap = block_entries();
+    const int KU = pad_ku > 0 ? pad_ku : (sizeof(S) == sizeof(double) ? 4 : 2);
+    const auto key = std::make_tuple(R, W, (blocks ? 1 : 0) | (wmask ? 2 : 0), KU, ecap);
+    auto it = lv->slots.find(key);
     if (it != lv->slots.end()) return it->second.get();
     std::unique_ptr<LevelDev::Slots> sl(new LevelDev::Slots());
     std::vector<int4> rec;
@@ -685,8 +714,7 @@ LevelDev::Slots *get_slots(mcinv_ctx *ctx, LevelDev *lv, int R, int W, bool bloc
             while (order.size() % R) order.push_back(-1);
         }
     } else if (const char *e = std::getenv("MCINV_SLACK")) {
-        order = mcinv::schedule_slots(ctx->n, lv->h_rec, lv->h_ent_col, R, std::atoi(e), blocks ? block_entries() : 0,
-                                      sim);
+        order = mcinv::schedule_slots(ctx->n, lv->h_rec, lv->h_ent_col, R, std::atoi(e), blocks ? ecap : 0, sim);
     } else {
         // the largest slack (W, 3W/4, W/2, 3W/8, ..., 1 groups) whose schedule pads at most
         // 5% of the slots (MCINV_SLACK_PAD, percent): wide DAGs (config 2: L = 24 of 32,
@@ -706,7 +734,7 @@ LevelDev::Slots *get_slots(mcinv_ctx *ctx, LevelDev *lv, int R, int W, bool bloc
         bool found = false;
         for (int L : cand) {
             const std::vector<int> o = mcinv::schedule_slots(ctx->n, lv->h_rec, lv->h_ent_col, R, L,
-                                                             blocks ? block_entries() : 0, 0);
+                                                             blocks ? ecap : 0, 0);
             if ((double)o.size() <= (double)ctx->n * (1.0 + pad / 100.0)) {
                 chosen = L;
                 found = true;
@@ -718,7 +746,7 @@ LevelDev::Slots *get_slots(mcinv_ctx *ctx, LevelDev *lv, int R, int W, bool bloc
             }
         }
         (void)found;
-        order = mcinv::schedule_slots(ctx->n, lv->h_rec, lv->h_ent_col, R, chosen, blocks ? block_entries() : 0, sim);
+        order = mcinv::schedule_slots(ctx->n, lv->h_rec, lv->h_ent_col, R, chosen, blocks ? ecap : 0, sim);
     }
     for (int o : order) {
         if (o < 0) {
@@ -742,10 +770,50 @@ LevelDev::Slots *get_slots(mcinv_ctx *ctx, LevelDev *lv, int R, int W, bool bloc
         // predicate, and fma(0, v, a) == a for the finite states of a converging run (only the
         // sign of an exact zero sum can differ). EP a multiple of 4; sections 16-B aligned.
         const bool pat = !lv->h_pz.empty();
-        const int KU = sizeof(S) == sizeof(double) ? 4 : 2;
         auto padded = [KU](int c) { return (c + KU - 1) / KU * KU; };
         const ZW<S> *hab = reinterpret_cast<const ZW<S> *>(lv->h_ab.data());
         const size_t ng = rec.size() / R;
+        // Wait masks (v6): row i must see its lower neighbours j final before its update.
+        // Waiting on j is implied, and dropped, when (a) j is itself a lower neighbour of
+        // another lower neighbour j' of i that i does wait on (j' published only after
+        // seeing j final, or after its own implied waits: completion is transitive through
+        // the release/acquire pairs of the counters), or (b) j sits in an earlier group of
+        // the same warp in the slot schedule (program order of that warp). Bit e of the mask
+        // covers lower entry e < 32; entries from 32 on are always waited for.
+        std::vector<int> ord_of, grp_of;
+        if (wmask) {
+            ord_of.assign(ctx->n, -1);
+            grp_of.assign(ctx->n, -1);
+            for (int64_t o = 0; o < ctx->n; ++o) ord_of[lv->h_rec[o].x] = (int)o;
+            for (size_t t = 0; t < order.size(); ++t)
+                if (order[t] >= 0) grp_of[lv->h_rec[order[t]].x] = (int)(t / R);
+        }
+        auto lower_has = [&](int jp, int j) {  // is j a lower neighbour of jp?
+            const int4 r = lv->h_rec[ord_of[jp]];
+            const int nl = (int)((unsigned)r.z >> 16);
+            const int *b = lv->h_ent_col.data() + r.y;
+            return std::binary_search(b, b + nl, j);
+        };
+        const char *wm_env = std::getenv("MCINV_WAITMASK");  // 0: wait on every lower neighbour (A/B)
+        const bool prune = !(wm_env && std::atoi(wm_env) == 0);
+        auto wait_mask = [&](const int4 q) -> unsigned {
+            const int nl = (int)((unsigned)q.z >> 16);
+            if (!prune) return nl >= 32 ? 0xffffffffu : (1u << nl) - 1u;
+            const int *cols = lv->h_ent_col.data() + q.y;
+            std::vector<int> kept;
+            unsigned m = 0;
+            for (int e = nl - 1; e >= 0; --e) {
+                const int j = cols[e];
+                bool implied = e < 32 && grp_of[j] < grp_of[q.x] && (grp_of[j] % W) == (grp_of[q.x] % W);
+                for (size_t k = 0; !implied && e < 32 && k < kept.size(); ++k) implied = lower_has(kept[k], j);
+                if (!implied) {
+                    kept.push_back(j);
+                    if (e < 32) m |= 1u << e;
+                }
+            }
+            return m;
+        };
+        const size_t mask_bytes = wmask ? ((size_t)4 * R + 15) / 16 * 16 : 0;
         std::vector<int64_t> gofs(ng + 1, 0);
         std::vector<unsigned char> blob;
         for (size_t g = 0; g < ng; ++g) {
@@ -753,7 +821,8 @@ LevelDev::Slots *get_slots(mcinv_ctx *ctx, LevelDev *lv, int R, int W, bool bloc
             for (int r = 0; r < R; ++r)
                 if (rec[g * R + r].x >= 0) E += padded(rec[g * R + r].z & 0xffff);
             const int EP = (E + 3) / 4 * 4;
-            const size_t off_col = 16 + 16 * (size_t)R + 2 * sizeof(S) * R;
+            const size_t off_wm = 16 + 16 * (size_t)R + 2 * sizeof(S) * R;  // masks (wmask) before the columns
+            const size_t off_col = off_wm + mask_bytes;
             const size_t off_ab = off_col + 4 * (size_t)EP;
             const size_t off_pz = off_ab + sizeof(ZW<S>) * EP;
             const size_t bytes = (off_pz + (pat ? 8 * (size_t)EP : 0) + 15) / 16 * 16;
@@ -768,6 +837,7 @@ LevelDev::Slots *get_slots(mcinv_ctx *ctx, LevelDev *lv, int R, int W, bool bloc
                 reinterpret_cast<int4 *>(b + 16)[r] = make_int4(q.x, e, q.x >= 0 ? q.z : 0, q.w);
                 reinterpret_cast<S *>(b + 16 + 16 * R)[2 * r] = dsg[2 * (g * R + r)];
                 reinterpret_cast<S *>(b + 16 + 16 * R)[2 * r + 1] = dsg[2 * (g * R + r) + 1];
+                if (wmask) reinterpret_cast<unsigned *>(b + off_wm)[r] = q.x >= 0 ? wait_mask(q) : 0u;
                 for (int t = 0; t < cnt; ++t) {
                     reinterpret_cast<int *>(b + off_col)[e + t] = lv->h_ent_col[q.y + t];
                     reinterpret_cast<ZW<S> *>(b + off_ab)[e + t] = hab[q.y + t];
@@ -791,7 +861,7 @@ LevelDev::Slots *get_slots(mcinv_ctx *ctx, LevelDev *lv, int R, int W, bool bloc
         if (upload(ctx, sl->blob, blob) != MCINV_OK || upload(ctx, sl->gofs, gofs) != MCINV_OK) return nullptr;
     }
     LevelDev::Slots *raw = sl.get();
-    lv->slots[R * 4096 + W + (blocks ? (1 << 28) : 0)] = std::move(sl);
+    lv->slots[key] = std::move(sl);
     return raw;
 }
 
@@ -854,7 +924,14 @@ mcinv_status run_typed(mcinv_ctx *ctx, const mcinv_run_args *a, const Layout &L,
             CK(cudaMemsetAsync(p.slot_pat, 0, (size_t)L.Gs * std::max<int64_t>(ctx->pcount, 1) * sizeof(S), st));
         if (a->outputs & MCINV_FULL) CK(cudaMemsetAsync(ws + L.slot_full, 0, (size_t)L.G * n * n * sizeof(S), st));
         if (a->outputs & MCINV_TRACE) CK(cudaMemsetAsync(p.slot_trace, 0, (size_t)L.Gs * sizeof(S), st));
+        if (L.series_cap) CK(cudaMemsetAsync(ws + L.series, 0, (size_t)L.series_cap * sizeof(S), st));
     }
+    // Geyer's series: sampling sweeps since the fresh run index it; it must hold them all
+    const int64_t series_base = a->resume ? ctx->acc_cycles : 0;
+    if (L.series_cap && series_base + a->cycles > L.series_cap)
+        return fail(ctx, MCINV_E_INVALID, "trace_series capacity below the sampling sweeps", L.series_cap);
+    p.series = L.series_cap ? (double *)(ws + L.series) : nullptr;
+    p.series_base = (int)series_base;
     // kernel choice (Layout::ver): v3 level schedule (default), v1 row by row
     LevelDev *lv = L.ver == 3 ? get_levels<S>(ctx, a->outputs) : nullptr;
     if (lv && !lv->error.empty()) return fail(ctx, MCINV_E_INVALID, "level schedule: " + lv->error);
@@ -866,11 +943,16 @@ mcinv_status run_typed(mcinv_ctx *ctx, const mcinv_run_args *a, const Layout &L,
     // MCINV_KERNEL=v3|v4|v5 forces one (error if it does not apply).
     const int pref = kernel_pref();
     const bool flow_ok = lv && L.lgC <= 5 && !lv->deferred;
-    if ((pref == 4 || pref == 5) && !flow_ok) return fail(ctx, MCINV_E_INVALID, "v4/v5 kernel not applicable to this run");
+    if ((pref == 4 || pref == 5 || pref == 6) && !flow_ok)
+        return fail(ctx, MCINV_E_INVALID, "dataflow kernel not applicable to this run");
+    // v6 (v5 with the two chains of a Box-Muller pair per thread): real C, at least 2 chains
+    // per CTA, both chains of a thread in one SE group (group_size >= 2: even chain_begin)
+    const bool v6_ok = flow_ok && ctx->dtype == MCINV_F64 && L.lgC >= 1 && L.lgP >= 1 && a->group_size >= 2;
+    if (pref == 6 && !v6_ok) return fail(ctx, MCINV_E_INVALID, "v6 kernel not applicable to this run");
     // auto: dataflow only up to 200k rows -- beyond, v3 (level barriers, K = 2 chains per
     // thread) measured 15-20% faster than v5 with bit counters at n = 1e6 (C = 8/16/32:
     // 3.04/3.45/3.69e10 vs 2.64/2.57/3.00e10 site-updates/s; profiles/r01_bigsmall.log)
-    bool v4 = flow_ok && (pref == 4 || pref == 5 || (pref == 0 && n <= 200000));  // v4 or v5
+    bool v4 = flow_ok && (pref == 4 || pref == 5 || pref == 6 || (pref == 0 && n <= 200000));  // v4, v5 or v6
     // chains per thread K (register blocking; real C, both chains in one SE group, no
     // trace / deferred items): default 2 for v3 (config 4 +19%), 1 for the dataflow kernels
     // (config 2 measured faster with more threads than with blocking, profiles/); MCINV_K
@@ -889,13 +971,38 @@ mcinv_status run_typed(mcinv_ctx *ctx, const mcinv_run_args *a, const Layout &L,
         return (int)((want + 31) / 32 * 32);
     };
     int threads3 = lv ? threads_for(v4) : 0;
-    bool v5 = v4 && (pref == 5 || (pref == 0 && kV5Default));
-    LevelDev::Slots *sl = v5 ? get_slots<S>(ctx, lv, 32 >> L.lgC, threads3 / 32, true) : nullptr;
+    bool v6 = v4 && v6_ok && (pref == 6 || (pref == 0 && v6_default()));
+    LevelDev::Slots *sl = nullptr;
+    if (v6) {
+        // R = 64 / C rows per warp group (C / 2 lanes per row); each row's entries padded to
+        // the kernel's gather unroll; the block entry cap scaled with R, within the
+        // shared-memory budget of two block slots per warp next to the counters
+        if (!std::getenv("MCINV_THREADS")) threads3 = v6_threads();
+        const int R = 64 >> L.lgC, W = threads3 / 32, ku = mcinv::sweep6_ku(threads3);
+        const size_t counters = n > mcinv::kByteCounters ? ((size_t)n + 127) / 128 * 16 : ((size_t)n + 15) / 16 * 16;
+        const long budget = ((long)(220 * 1024) - (long)counters) / (2 * W) - 16 - 36 * R - 64;
+        int ecap = std::max(8, std::min<int>(block_entries() * R / 4, (int)(budget / 28)));
+        if (const char *e = std::getenv("MCINV_BLOCK_ENTRIES")) ecap = std::atoi(e);
+        // the cap counts unpadded entries: shrink it until the padded blocks fit
+        for (int tries = 0; tries < 6; ++tries, ecap = std::max(8, ecap * 3 / 4)) {
+            sl = get_slots<S>(ctx, lv, R, W, true, ku, ecap, true);
+            if (!sl || mcinv::sweep6_smem((int)n, threads3, sl->maxb) <= 227 * 1024) break;
+        }
+        if (sl && mcinv::sweep6_smem((int)n, threads3, sl->maxb) > 227 * 1024) {
+            if (pref == 6) return fail(ctx, MCINV_E_INVALID, "v6 blocks do not fit shared memory");
+            v6 = false;
+            sl = nullptr;
+            threads3 = threads_for(v4);
+        }
+    }
+    bool v5 = v4 && !v6 && (pref == 5 || (pref == 0 && kV5Default));
+    if (v5) sl = get_slots<S>(ctx, lv, 32 >> L.lgC, threads3 / 32, true);
     if (v5 && sl && mcinv::sweep5_smem((int)n, threads3, sl->maxb) > 227 * 1024) {
         if (pref == 5) return fail(ctx, MCINV_E_INVALID, "v5 blocks do not fit shared memory");
         v5 = false;
     }
-    if (v4 && !v5) {
+    if (v6) lgK = 1;
+    if (v4 && !v5 && !v6) {
         if (n > 200000) {  // v4's byte counters do not fit: level kernel (its layout is the same)
             if (pref == 4) return fail(ctx, MCINV_E_INVALID, "v4 counters do not fit shared memory");
             v4 = false;
@@ -913,7 +1020,7 @@ mcinv_status run_typed(mcinv_ctx *ctx, const mcinv_run_args *a, const Layout &L,
         ctx->err_flag.bytes = 16;
     }
     if (v4) CK(cudaMemsetAsync(ctx->err_flag.p, 0, 16, st));
-    ctx->last_kernel = v5 ? 5 : v4 ? 4 : L.ver;
+    ctx->last_kernel = v6 ? 6 : v5 ? 5 : v4 ? 4 : L.ver;
     ctx->last_C = lv ? (1 << L.lgC) : 32;
     ctx->last_steps = lv ? lv->D : n;
     ctx->last_K = 1 << lgK;
@@ -956,6 +1063,8 @@ mcinv_status run_typed(mcinv_ctx *ctx, const mcinv_run_args *a, const Layout &L,
         q3.slot_pat = p.slot_pat;
         q3.slot_trace = p.slot_trace;
         q3.bad = p.bad;
+        q3.series = p.series;
+        q3.series_base = p.series_base;
         // MCINV_RECONV bits: 1 reconverge the warp at the end of each item (default: diag-only
         // config 2 1.57 -> 2.79e10), 2 also after the dependency waits (measured -6%)
         q3.reconv = 1;
@@ -993,8 +1102,15 @@ mcinv_status run_typed(mcinv_ctx *ctx, const mcinv_run_args *a, const Layout &L,
             q.snap_x = (S *)(ws + L.snap_x);
             q.snap_y = (S *)(ws + L.snap_y);
             timed(ctx, 0, st, [&] {
-                cudaError_t e = v5 ? launch_sweep5<S>(q, threads3, st)
-                                : v4 ? launch_sweep4<S>(q, threads3, st) : launch_sweep3<S>(q, threads3, st);
+                cudaError_t e;
+                if constexpr (std::is_same<S, double>::value) {
+                    if (v6) e = launch_sweep6(q, threads3, st);
+                    else e = v5 ? launch_sweep5<S>(q, threads3, st)
+                            : v4 ? launch_sweep4<S>(q, threads3, st) : launch_sweep3<S>(q, threads3, st);
+                } else {
+                    e = v5 ? launch_sweep5<S>(q, threads3, st)
+                           : v4 ? launch_sweep4<S>(q, threads3, st) : launch_sweep3<S>(q, threads3, st);
+                }
                 if (e != cudaSuccess) lerr = e;
             });
         } else {
@@ -1135,7 +1251,8 @@ mcinv_status mcinv_run(mcinv_ctx *ctx, const mcinv_run_args *args) {
     char *ws = (char *)args->workspace;
     if (args->resume) {
         if (!ctx->have_run || ctx->last.chains != args->chains || ctx->last.outputs != args->outputs ||
-            ctx->last.group_size != args->group_size || (ws && ws != ctx->ws))
+            ctx->last.group_size != args->group_size || ctx->last.trace_series != args->trace_series ||
+            (ws && ws != ctx->ws))
             return fail(ctx, MCINV_E_STATE, "resume needs the previous run's shape and workspace");
     }
     if (ws) {
@@ -1207,6 +1324,29 @@ mcinv_status mcinv_recenter(mcinv_ctx *ctx, int64_t total_chains, size_t *m2_off
     CK(cudaGetLastError());
     if (m2_offset) *m2_offset = L.mom_m2;
     if (m2_count) *m2_count = L.mom_m2;
+    return MCINV_OK;
+}
+
+mcinv_status mcinv_geyer(mcinv_ctx *ctx, double *out) {
+    if (!ctx || !ctx->have_run) return MCINV_E_STATE;
+    if (!out) return fail(ctx, MCINV_E_INVALID, "null out");
+    const Layout &L = ctx->lay;
+    if (!L.series_cap || ctx->acc_cycles < 1) return fail(ctx, MCINV_E_STATE, "no trace series (trace_series = 0)");
+    CK(cudaSetDevice(ctx->device));
+    if (ctx->tmp.bytes < 64) {
+        ctx->tmp.release();
+        if (dev_alloc(&ctx->tmp.p, 64) != cudaSuccess || cudaStreamSynchronize(0) != cudaSuccess) {
+            cudaGetLastError();
+            ctx->tmp.p = nullptr;
+            return fail(ctx, MCINV_E_NOMEM, "geyer staging");
+        }
+        ctx->tmp.bytes = 64;
+    }
+    mcinv::launch_geyer((const double *)(ctx->ws + L.series), ctx->acc_cycles, L.e, (double *)ctx->tmp.p, ctx->stream);
+    ctx->launches++;
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(out, ctx->tmp.p, 4 * L.e * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
     return MCINV_OK;
 }
 
@@ -1437,6 +1577,44 @@ mcinv_status mcinv_run_until(mcinv_ctx *ctx, const mcinv_run_args *args, unsigne
             const double s_ = e == 2 ? std::hypot(se[2 * c], se[2 * c + 1]) : se[c];
             worst = std::max(worst, s_ / (m > 0.0 ? m : 1.0));
         }
+        if (worst < rel_se || done >= max_cycles) break;
+        mcinv_run_args r = a;
+        r.resume = 1;
+        r.burn_in = 0;
+        r.sweep_begin = a.sweep_begin + a.burn_in + done;
+        r.cycles = std::min(check_cycles, max_cycles - done);
+        TRY(mcinv_run(ctx, &r));
+        done += r.cycles;
+    }
+    *cycles_done = done;
+    if (rel_se_out) *rel_se_out = worst;
+    return MCINV_OK;
+}
+
+mcinv_status mcinv_run_until_geyer(mcinv_ctx *ctx, const mcinv_run_args *args, double rel_se, int64_t check_cycles,
+                                   int64_t max_cycles, int64_t *cycles_done, double *rel_se_out) {
+    // The paper's stopping rule: after the burn-in, realized traces every
+    // cycle; every check_cycles (100 in the paper) the Geyer standard error of their mean
+    // relative to the estimate; stop below the tolerance.
+    if (!ctx || !ctx->valid || !args || !cycles_done || !(rel_se > 0.0) || check_cycles < 1 ||
+        max_cycles < check_cycles || !(args->outputs & MCINV_TRACE))
+        return MCINV_E_INVALID;
+    mcinv_run_args a = *args;
+    a.cycles = check_cycles;
+    a.resume = 0;
+    a.trace_series = max_cycles;
+    TRY(mcinv_run(ctx, &a));
+    int64_t done = check_cycles;
+    double worst = 0.0;
+    const int e = ctx->dtype == MCINV_C128 ? 2 : 1;
+    for (;;) {
+        double g[8];
+        TRY(mcinv_geyer(ctx, g));
+        TRY(mcinv_run_status(ctx, nullptr));
+        const double mre = g[0], sre = g[2] > 0.0 ? std::sqrt(g[2] / (double)done) : 0.0;
+        const double mim = e == 2 ? g[4] : 0.0, sim = (e == 2 && g[6] > 0.0) ? std::sqrt(g[6] / (double)done) : 0.0;
+        const double m = std::hypot(mre, mim), se = std::hypot(sre, sim);
+        worst = se / (m > 0.0 ? m : 1.0);
         if (worst < rel_se || done >= max_cycles) break;
         mcinv_run_args r = a;
         r.resume = 1;

@@ -81,6 +81,8 @@ template <typename S> struct SweepParams {
     S *snap_x, *snap_y;   // [T][n][ld]
     int snap_s0;          // local sweep stored at snapshot slot 0
     double *bad;          // divergence count (+1 per active lane that stored a value above 1e12 or non-finite)
+    double *series;       // TRACE: per sampling sweep, the run's summed w^dagger Q z (Geyer's series), or null
+    int series_base;      // series index of this launch's first sampling sweep
 };
 
 template <typename S>
@@ -131,6 +133,8 @@ struct Sweep3Params {
     int prefetch;         // v5: prefetch upper neighbours' lines before the noise (0 off, 1 L1, 2 L2)
     double *bad;          // divergence count: +1 per active lane that stored a non-finite value or one
                           // above 1e12 in modulus (checked at every update = every sweep's end state)
+    double *series;       // TRACE: per sampling sweep, the run's summed w^dagger Q z (Geyer's series), or null
+    int series_base;      // series index of this launch's first sampling sweep
 };
 
 template <typename S>
@@ -142,6 +146,11 @@ cudaError_t launch_sweep4(const Sweep3Params<S> &p, int threads, cudaStream_t st
 template <typename S>
 cudaError_t launch_sweep5(const Sweep3Params<S> &p, int threads, cudaStream_t st);
 size_t sweep5_smem(int n, int threads, int maxb);
+constexpr int kByteCounters = 160000;  // dataflow kernels: above, one completion bit per row in shared memory
+// v6: v5 with two chains per thread (real C; the chain pair shares one Box-Muller pair)
+cudaError_t launch_sweep6(const Sweep3Params<double> &p, int threads, cudaStream_t st);
+int sweep6_ku(int threads);
+size_t sweep6_smem(int n, int threads, int maxb);  // two block slots per warp  // v6's gather unroll for a thread count (the blocks' entry padding)
 
 // A_g[i][j] += sum_{t < T, c in group g} X[t][i][c] conj(Y[t][j][c]).
 template <typename S>
@@ -157,6 +166,9 @@ void launch_finalize(const double *s1, const double *m2, int64_t comps, double m
                      double G, double *est, double *se, cudaStream_t st);
 template <typename S>
 void launch_max_modulus(const ZW<S> *zw, int n, int ld, double *out, cudaStream_t st);
+// Geyer's initial positive sequence estimator of each component of a series x[m][e]:
+// out[c * 4 + {0..3}] = {mean, gamma_0, sigma2 = m Var(mean), effective length}
+void launch_geyer(const double *x, int64_t m, int e, double *out, cudaStream_t st);
 void launch_philox(const uint32_t *ctr, int64_t count, uint32_t k0, uint32_t k1, uint32_t *out,
                    double *gauss, cudaStream_t st);
 

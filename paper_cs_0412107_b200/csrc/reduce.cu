@@ -106,7 +106,8 @@ __global__ void philox_kernel(const uint32_t *__restrict__ ctr, int64_t count, u
             out[4 * t + 2] = r.z;
             out[4 * t + 3] = r.w;
         }
-        if (gauss) gauss[t] = box_muller(r);
+        // the kernels' noise of (row, sweep, chain) = (ctr[0], ctr[1], ctr[2]) (reading R4)
+        if (gauss) gauss[t] = gaussian(ctr[4 * t], ctr[4 * t + 1], ctr[4 * t + 2], k0, k1);
     }
 }
 
@@ -124,6 +125,63 @@ void launch_moments(const double *slot, int G, int k, int64_t comps, double *s1,
 void launch_finalize(const double *s1, const double *m2, int64_t comps, double m_cycles, double gs_cycles, double G,
                      double *est, double *se, cudaStream_t st) {
     finalize_kernel<<<grid_for(comps, 256), 256, 0, st>>>(s1, m2, comps, m_cycles, gs_cycles, G, est, se);
+}
+
+// Geyer's initial positive sequence estimator (Geyer 1992; the paper's standard errors,
+// PAPER.md:354-360) of component c = blockIdx.x of the series x[t * e + c], t < m: mean,
+// lag-k autocovariances gamma_k = (1/m) sum_t (x_t - mean)(x_{t+k} - mean) (each summed in
+// t order by one thread, a batch of 1024 lags at a time), pair sums gamma_2j + gamma_2j+1
+// while positive, sigma2 = -gamma_0 + 2 sum, ESS = m gamma_0 / sigma2.
+__global__ void geyer_kernel(const double *__restrict__ x, int64_t m, int e, double *__restrict__ out) {
+    const int c = blockIdx.x;
+    __shared__ double gam[1024 + 1];
+    __shared__ double s_mean, s_sigma2;
+    __shared__ int s_done;
+    if (threadIdx.x == 0) {
+        double a = 0.0;
+        for (int64_t t = 0; t < m; ++t) a += x[t * e + c];
+        s_mean = a / (double)m;
+        s_sigma2 = 0.0;
+        s_done = 0;
+    }
+    __syncthreads();
+    const double mean = s_mean;
+    double g0 = 0.0;
+    for (int64_t l0 = 0; !s_done; l0 += 1024) {
+        const int64_t lag = l0 + threadIdx.x;
+        double acc = 0.0;
+        if (lag < m)
+            for (int64_t t = 0; t + lag < m; ++t) acc += (x[t * e + c] - mean) * (x[(t + lag) * e + c] - mean);
+        gam[threadIdx.x] = acc / (double)m;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            if (l0 == 0) {
+                g0 = gam[0];
+                s_sigma2 = -g0;
+                gam[1024] = g0;
+            }
+            for (int q = 0; q < 1024; q += 2) {
+                const int64_t j2 = l0 + q;  // pair (j2, j2 + 1)
+                if (j2 + 1 >= m || !(gam[q] + gam[q + 1] > 0.0)) {
+                    s_done = 1;
+                    break;
+                }
+                s_sigma2 += 2.0 * (gam[q] + gam[q + 1]);
+            }
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        const double gg0 = gam[1024];
+        out[4 * c] = mean;
+        out[4 * c + 1] = gg0;
+        out[4 * c + 2] = s_sigma2;
+        out[4 * c + 3] = s_sigma2 > 0.0 ? (double)m * gg0 / s_sigma2 : 0.0;
+    }
+}
+
+void launch_geyer(const double *x, int64_t m, int e, double *out, cudaStream_t st) {
+    geyer_kernel<<<e, 1024, 0, st>>>(x, m, e, out);
 }
 
 void launch_philox(const uint32_t *ctr, int64_t count, uint32_t k0, uint32_t k1, uint32_t *out, double *gauss,

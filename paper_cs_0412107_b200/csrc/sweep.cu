@@ -44,7 +44,7 @@ __global__ void __launch_bounds__(128) sweep_kernel(const SweepParams<S> p) {
     ZW<S> *__restrict__ zw = p.zw;
     const bool leader = (lane & (p.gs - 1)) == 0;
     const int g = c / p.gs;
-    S tr = zero_s<S>();
+    S tr = zero_s<S>(), trs = zero_s<S>();  // trace over the launch / the current sweep
     bool dv = false;  // divergence seen (reading R12: every stored value is a sweep-end value)
 
     for (int s = p.s_begin; s < p.s_end; ++s) {
@@ -102,13 +102,22 @@ __global__ void __launch_bounds__(128) sweep_kernel(const SweepParams<S> p) {
                     const int r = __ldg(p.Q.qc_row + q);
                     qw = add_s(qw, mul_s(ldg_s(p.Q.qc_val + q), conj_s(zw[static_cast<int64_t>(r) * ld + c].w)));
                 }
-                tr = add_s(tr, add_s(zwc_s(qz, wi), mul_s(zi, qw)));
+                trs = add_s(trs, add_s(zwc_s(qz, wi), mul_s(zi, qw)));
             }
             if (p.outputs & OUT_FULL) {
                 const int64_t t = s - p.snap_s0;
                 p.snap_x[(t * n + i) * ld + c] = zi;
                 p.snap_y[(t * n + i) * ld + c] = wi;
             }
+        }
+        if ((p.outputs & OUT_TRACE) && sampling) {
+            if (p.series) {  // the sweep's realized trace of this warp's chains (Geyer's series)
+                S v = active ? trs : zero_s<S>();
+                v = group_sum(v, 32);
+                if (lane == 0) atomic_add_to(p.series + (int64_t)(p.series_base + s - p.burn_in) * ScalarTraits<S>::kDoubles, v);
+            }
+            tr = add_s(tr, trs);
+            trs = zero_s<S>();
         }
     }
     if (p.outputs & OUT_TRACE) {

@@ -59,7 +59,8 @@ __global__ void __launch_bounds__(NT, 1) sweep3_kernel(const Sweep3Params<S> p) 
     const bool want_tr = p.outputs & OUT_TRACE, want_full = p.outputs & OUT_FULL;
     double *const sd = p.slot_diag + grp * p.n * E;
     double *const sp = p.slot_pat + grp * p.pcount * E;
-    S tr = zero_s<S>();  // K == 1 only (trace runs use K = 1)
+    S tr = zero_s<S>();   // K == 1 only (trace runs use K = 1): the chain's trace over the launch
+    S trs = zero_s<S>();  // ... and over the current sweep (Geyer's series)
     bool dv = false;     // divergence seen (reading R12)
 
     for (int s = p.s_begin; s < p.s_end; ++s) {
@@ -84,14 +85,21 @@ __global__ void __launch_bounds__(NT, 1) sweep3_kernel(const Sweep3Params<S> p) 
                         for (int e = 0; e < cnt; ++e) prefetch_l2(zrow(zcol, __ldg(p.ent_col + beg + e), zst));
                     // noise first: its temporaries are dead before the gathers are in flight
                     double phi[K];
+                    if constexpr (GAUSS && K == 2) {
+                        // the thread's chains are a Box-Muller pair (2m, 2m + 1; reading R4): one
+                        // Philox block, one ln and sqrt for both
+                        gaussian2(static_cast<uint32_t>(i), k, p.chain0 + static_cast<uint32_t>(chain), p.key0, p.key1,
+                                  phi[0], phi[K - 1]);
+                    } else {
 #pragma unroll
-                    for (int h = 0; h < K; ++h) {
-                        if constexpr (GAUSS)
-                            phi[h] = gaussian(static_cast<uint32_t>(i), k, p.chain0 + static_cast<uint32_t>(chain + h),
-                                              p.key0, p.key1);
-                        else
-                            phi[h] = noise_phi(p.noise, static_cast<uint32_t>(i), k,
-                                               p.chain0 + static_cast<uint32_t>(chain + h), p.key0, p.key1);
+                        for (int h = 0; h < K; ++h) {
+                            if constexpr (GAUSS)
+                                phi[h] = gaussian(static_cast<uint32_t>(i), k,
+                                                  p.chain0 + static_cast<uint32_t>(chain + h), p.key0, p.key1);
+                            else
+                                phi[h] = noise_phi(p.noise, static_cast<uint32_t>(i), k,
+                                                   p.chain0 + static_cast<uint32_t>(chain + h), p.key0, p.key1);
+                        }
                     }
                     S az[K], aw[K];
 #pragma unroll
@@ -138,7 +146,7 @@ __global__ void __launch_bounds__(NT, 1) sweep3_kernel(const Sweep3Params<S> p) 
                             for (int e = __ldg(p.tq_eptr + o); e < __ldg(p.tq_eptr + o + 1); ++e)
                                 qz = add_s(qz, mul_s(ldg_s(p.tq_val + e),
                                                      ld_zw(zrow(zcol, __ldg(p.tq_col + e), zst)).z));
-                            tr = add_s(tr, zwc_s(qz, ld_zw(zrow(zcol, i, zst)).w));
+                            trs = add_s(trs, zwc_s(qz, ld_zw(zrow(zcol, i, zst)).w));
                         }
                     }
                     // ---- deferred pattern pairs z_i w_j^*
@@ -161,6 +169,17 @@ __global__ void __launch_bounds__(NT, 1) sweep3_kernel(const Sweep3Params<S> p) 
                 }
             }
             __syncthreads();
+        }
+        if constexpr (K == 1) {
+            if (want_tr && sampling) {
+                // the sweep's realized trace of this warp's chains into Geyer's series
+                if (p.series) {
+                    const S v = group_sum<32>(active[0] ? trs : zero_s<S>());
+                    if (lane == 0) slot_red(p.series + (int64_t)(p.series_base + s - p.burn_in) * E, v);
+                }
+                tr = add_s(tr, trs);
+                trs = zero_s<S>();
+            }
         }
     }
 

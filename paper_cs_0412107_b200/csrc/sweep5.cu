@@ -9,7 +9,6 @@
 
 namespace mcinv {
 // ---------------------------------------------------------------- v5: v4 + TMA-staged plan
-constexpr int kByteCounters = 160000;  // larger n: one completion bit per row
 //
 // The dataflow kernel of v4 with the plan data of every warp group (row
 // records, delta/sigma, entry columns, coefficient pairs, pattern slots)
@@ -19,32 +18,6 @@ constexpr int kByteCounters = 160000;  // larger n: one completion bit per row
 // addresses and coefficients and the accumulation's partners and slots then
 // read shared memory, and the unified L1 is left to the state lines.
 namespace {
-
-__device__ __forceinline__ uint32_t smem_addr(const void *p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-    uint32_t ok = 0;
-    while (!ok) {
-        asm volatile(
-            "{\n\t.reg .pred q;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 q, [%1], %2;\n\t"
-            "selp.u32 %0, 1, 0, q;\n}"
-            : "=r"(ok)
-            : "r"(bar), "r"(parity)
-            : "memory");
-    }
-}
-__device__ __forceinline__ void tma_block(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar) {
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // our generic reads of this slot precede
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-                 "l"(src), "r"(bytes), "r"(bar)
-                 : "memory");
-}
 
 // Eq. (4)/(5) fma chains from a staged block (see row_sums): the host padded the row's
 // entries to a multiple of KU with zero coefficients on a valid column, so the unrolled

@@ -55,6 +55,8 @@ def oracle_chains(k: int, chains, burn: int, cycles: int, outputs=(), seed: int 
             out[key] = None
         elif key in ("z_snap", "w_snap"):
             out[key] = np.concatenate([r[key] for r in res], axis=1)
+        elif key == "trace_series":  # per-sweep sums over the run's chains
+            out[key] = np.sum([r[key] for r in res], axis=0)
         else:
             out[key] = np.concatenate([r[key] for r in res], axis=0)
     return out

@@ -292,13 +292,34 @@ def test_v4_dataflow(mc, orc, monkeypatch, kernel):
     monkeypatch.delenv("MCINV_C")
     monkeypatch.delenv("MCINV_THREADS")
     # automatic choice: v4 where it applies (configs 2, 3), v3 for C > 32 or trace (configs 4, 5)
-    for k, ver in ((3, (4, 5)), (2, (4, 5)), (5, (3,))):
+    for k, ver in ((3, (4, 5)), (2, (4, 5, 6)), (5, (3,))):
         c, q, run = W.config(k)
         inv = mc.Inverter(c, q=q)
         inv.run(run.seed, run.chains, 0, 1, tuple(o for o in run.outputs if o != "full") or ("diag",),
                 group_size=run.group_size)
         assert inv.kernel_info()["version"] in ver, k
         inv.close()
+
+
+@pytest.mark.parametrize("threads", ["512", "768", "1024", "256"])
+def test_v6_two_chains_per_thread(mc, orc, monkeypatch, threads):
+    """v6 (the dataflow kernel with the two chains of a Box-Muller pair per
+    thread, reading R4) for every chains-per-CTA layout C = 2..32 (R = 64/C rows
+    per warp item), SE groups smaller than, equal to and larger than C, a
+    ragged chain count, an odd-group shard start, and diag / pattern / full."""
+    monkeypatch.setenv("MCINV_KERNEL", "v6")
+    monkeypatch.setenv("MCINV_THREADS", threads)
+    for C, gs, chains, cb in ((2, 2, 62, 0), (4, 4, 68, 4), (8, 32, 96, 32), (8, 2, 64, 6), (16, 8, 48, 0),
+                              (32, 32, 64, 64)):
+        monkeypatch.setenv("MCINV_C", str(C))
+        compare_run(mc, orc, W.pedigree(700, seed=25), seed=13, chains=chains, burn_in=3, cycles=4,
+                    outputs=("diag", "pattern"), group_size=gs, chain_begin=cb)
+    monkeypatch.setenv("MCINV_C", "8")
+    compare_run(mc, orc, W.dense_config1(24, seed=26), seed=14, chains=64, burn_in=1, cycles=3,
+                outputs=("diag", "full"), group_size=8, snapshot_sweeps=2)
+    for noise in ("z2",):
+        compare_run(mc, orc, W.pedigree(300, seed=27), seed=15, chains=64, burn_in=2, cycles=3,
+                    outputs=("diag", "pattern"), group_size=16, noise=noise)
 
 
 @pytest.mark.parametrize("kernel", ["v3", "v4"])
@@ -354,7 +375,7 @@ def test_bench_configs_use_level_kernels(mc):
         inv = mc.Inverter(c, q=q)
         inv.run(run.seed, run.chains, 0, 1, tuple(o for o in run.outputs if o != "full") or ("diag",),
                 group_size=run.group_size)
-        assert inv.kernel_info()["version"] in (3, 4, 5), k
+        assert inv.kernel_info()["version"] in (3, 4, 5, 6), k
         inv.close()
 
 
@@ -516,13 +537,15 @@ def test_config3_full_size_dense_lu(mc, orc):
     inv.close()
 
 
-@pytest.mark.parametrize("kernel", ["v1", "v3", "v4", "v5"])
+@pytest.mark.parametrize("kernel", ["v1", "v3", "v4", "v5", "v6"])
 def test_irregular_structure(mc, orc, kernel, monkeypatch):
     """An unsorted CSR with duplicate entries (summed), explicit zeros (kept),
     rows with no off-diagonal entry and a few dense rows (long entry lists:
     several gather chunks), a non-symmetric pattern, and a shard that starts
     at chain 64: every kernel vs the oracle."""
     monkeypatch.setenv("MCINV_KERNEL", kernel)
+    if kernel == "v6":
+        monkeypatch.setenv("MCINV_C", "4")  # v6 holds two chains per thread: C >= 2
     rng = np.random.default_rng(77)
     n = 150
     rows, cols, vals = [], [], []
@@ -570,7 +593,7 @@ def test_v5_bit_counters_large_n(mc, orc):
     inv.close()
 
 
-@pytest.mark.parametrize("kernel", ["v4", "v5"])
+@pytest.mark.parametrize("kernel", ["v4", "v5", "v6"])
 def test_dataflow_long_dependency_chain(mc, orc, monkeypatch, kernel):
     """Worst case for the dataflow kernels: a non-symmetric tridiagonal C
     (every row depends on the previous one, a dependency chain of depth n in
@@ -589,7 +612,7 @@ def test_dataflow_long_dependency_chain(mc, orc, monkeypatch, kernel):
             a[i, i + 150] = 0.4
             a[i + 150, i] = -0.3
     c = W.CSR.from_dense(a)
-    for C, th in ((8, "1024"), (32, "1024"), (1, "256")):
+    for C, th in ((8, "1024"), (32, "1024"), (1 if kernel != "v6" else 2, "256")):
         monkeypatch.setenv("MCINV_C", str(C))
         monkeypatch.setenv("MCINV_THREADS", th)
         compare_run(mc, orc, c, seed=12, chains=64, burn_in=7, cycles=13, outputs=("diag", "pattern"),

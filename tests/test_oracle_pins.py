@@ -91,21 +91,50 @@ def test_box_muller_closed_forms(orc):
     assert orc.gaussian_from_words(w) == pytest.approx(np.sqrt(2 * np.log(2)) * np.sqrt(0.5), rel=1e-15)
 
 
+def test_box_muller_pair_closed_forms(orc):
+    """The pair (reading R4): g0 = sqrt(-2 ln u1) cos(2 pi u2) (the cosine output
+    above), g1 = sqrt(-2 ln u1) sin(2 pi u2); exact u's again."""
+    rad = np.sqrt(2 * np.log(2))
+    a = (2**52 - 1) << 11  # u1 = 1/2
+    for u2_bits, want_c, want_s in ((2**50, np.sqrt(0.5), np.sqrt(0.5)),   # u2 = 1/8
+                                    (2**51, 0.0, 1.0),                    # u2 = 1/4
+                                    (3 * 2**51, 0.0, -1.0),               # u2 = 3/4
+                                    (2**52, -1.0, 0.0),                   # u2 = 1/2
+                                    (0, 1.0, 0.0)):                       # u2 = 0
+        b = u2_bits << 11
+        w = [a >> 32, a & 0xFFFFFFFF, b >> 32, b & 0xFFFFFFFF]
+        g0, g1 = orc.gaussian_pair_from_words(w)
+        assert g0 == orc.gaussian_from_words(w)
+        assert g0 == pytest.approx(rad * want_c, rel=1e-15, abs=1e-15)
+        assert g1 == pytest.approx(rad * want_s, rel=1e-15, abs=1e-15)
+    # one radius for both outputs: g0^2 + g1^2 = -2 ln u1 at random words
+    rng = np.random.default_rng(3)
+    for w in rng.integers(0, 2**32, size=(200, 4), dtype=np.uint64).tolist():
+        g0, g1 = orc.gaussian_pair_from_words(w)
+        aa = (int(w[0]) << 32 | int(w[1])) >> 11
+        u1 = (aa + 1) * 2.0**-53
+        assert g0 * g0 + g1 * g1 == pytest.approx(-2 * np.log(u1), rel=1e-13)
+
+
 def test_gaussian_counter_layout(orc):
     """Reading R4's counter layout, pinned on the CPU: the noise of (chain c,
-    sweep k, row i) is Box-Muller of the Philox block of counter {i, k, c, 0}
-    under key {seed lo, seed hi} -- composed here from the two separately
-    pinned pieces (KAT-pinned Philox, closed-form-pinned Box-Muller), so a
-    swapped or misplaced counter word inside orc_gaussian fails."""
+    sweep k, row i) is output c mod 2 (cosine for even, sine for odd chains)
+    of the Box-Muller pair of the Philox block of counter {i, k, c / 2, 0}
+    under key {seed lo, seed hi} -- composed here from the separately pinned
+    pieces (KAT-pinned Philox, closed-form-pinned Box-Muller pair), so a
+    swapped or misplaced counter word, or a wrong branch, inside orc_gaussian
+    fails."""
     rng = np.random.default_rng(11)
     for seed in (0, 0x5EED0002, 2**64 - 1, 0x123456789ABCDEF):
         key = [seed & 0xFFFFFFFF, seed >> 32]
         for i, k, c in rng.integers(0, 2**32, size=(40, 3), dtype=np.uint64).tolist() + [[0, 0, 0], [5, 0, 1]]:
-            want = orc.gaussian_from_words(orc.philox([i, k, c, 0], key))
-            assert orc.gaussian(seed, i, k, c) == want
+            pair = orc.gaussian_pair_from_words(orc.philox([i, k, c >> 1, 0], key))
+            assert orc.gaussian(seed, i, k, c) == pair[c & 1]
+            assert orc.gaussian(seed, i, k, c ^ 1) == pair[(c & 1) ^ 1]  # the partner chain
             # a transposed layout gives a different value
-            if len({i, k, c}) == 3:
-                assert orc.gaussian(seed, i, k, c) != orc.gaussian_from_words(orc.philox([k, i, c, 0], key))
+            if len({i, k, c >> 1}) == 3:
+                assert orc.gaussian(seed, i, k, c) != orc.gaussian_pair_from_words(
+                    orc.philox([k, i, c >> 1, 0], key))[c & 1]
 
 
 def test_gaussian_is_standard_normal(orc):
@@ -121,6 +150,10 @@ def test_gaussian_is_standard_normal(orc):
     for a, b in ((y[:, :, 1:], y[:, :, :-1]), (y[:, 1:], y[:, :-1]), (y[1:], y[:-1])):
         r = np.corrcoef(a.ravel(), b.ravel())[0, 1]
         assert abs(r) < 5 / np.sqrt(a.size)
+    # the two chains of one Box-Muller pair (R4) are independent, not merely uncorrelated:
+    # their squares (which share the radius) are uncorrelated too
+    r2 = np.corrcoef((y[0::2] ** 2).ravel(), (y[1::2] ** 2).ravel())[0, 1]
+    assert abs(r2) < 5 / np.sqrt(y[0::2].size)
 
 
 # ---------------------------------------------------------- sweep structure
@@ -556,3 +589,57 @@ def test_coupled_burn_in_four_chains(orc, cplx):
             first = k + 1  # snapshot k is taken after sweep k + 1
             break
     assert first == p_gs
+
+
+# ------------------------------------------------------------------ Geyer ESS (NEXT-2)
+
+def test_geyer_hand_computed(orc):
+    """orc_geyer on x = 1, 2, 3, 4 worked by hand: xbar 2.5, gamma = (1.25,
+    0.3125, -0.375, -0.5625) (lag sums over m - k terms, divided by m), pair
+    sums 1.5625 (kept) and -0.9375 (stop), sigma2 = -1.25 + 2 x 1.5625 = 1.875,
+    ESS = 4 x 1.25 / 1.875 = 8/3."""
+    g = orc.geyer([1.0, 2.0, 3.0, 4.0])
+    assert g["mean"] == 2.5 and g["gamma0"] == 1.25
+    assert g["sigma2"] == pytest.approx(1.875, rel=1e-15)
+    assert g["ess"] == pytest.approx(8 / 3, rel=1e-15)
+    assert g["se"] == pytest.approx(np.sqrt(1.875 / 4), rel=1e-15)
+
+
+@pytest.mark.parametrize("rho", [0.0, 0.9, -0.5])
+def test_geyer_ar1_closed_form(orc, rho):
+    """AR(1) x_t = rho x_{t-1} + e_t: the integrated autocorrelation time is
+    (1 + rho) / (1 - rho), so ESS / m -> (1 - rho) / (1 + rho) (Geyer 1992,
+    the estimator of P:354-360); a long series lands within a few percent."""
+    rng = np.random.default_rng(31)
+    m = 400000
+    e = rng.standard_normal(m)
+    x = np.empty(m)
+    x[0] = e[0] / np.sqrt(1 - rho * rho)
+    for t in range(1, m):
+        x[t] = rho * x[t - 1] + e[t]
+    g = orc.geyer(x)
+    want = (1 - rho) / (1 + rho)
+    assert g["ess"] / m == pytest.approx(want, rel=0.08)
+    assert g["se"] == pytest.approx(np.sqrt(g["gamma0"] / g["ess"]), rel=1e-12)
+
+
+def test_geyer_identity_matches_the_papers_tables(orc):
+    """The paper's standard errors are sqrt(Var / Eff. length) (Table 2,
+    P:618-648: 3932 / 15788 -> 0.499, 8123 / 8163 -> 0.998; Table 4,
+    P:898-924): the same identity orc_geyer's se = sqrt(gamma_0 / ESS) obeys."""
+    for var, ess, se in ((3932.0, 15788.0, 0.499), (8123.0, 8163.0, 0.998)):
+        assert np.sqrt(var / ess) == pytest.approx(se, abs=6e-4)
+    g = orc.geyer(np.sin(np.arange(5000) * 0.37) + np.random.default_rng(2).standard_normal(5000))
+    assert g["se"] == pytest.approx(np.sqrt(g["gamma0"] / g["ess"]), rel=1e-12)
+
+
+def test_trace_series_sums_to_the_trace(orc):
+    """The per-sweep realized traces (Geyer's series) of a run add up to the
+    per-chain trace sums, and their mean is the Eq. (tr) estimate."""
+    c = W.lattice(3, 2, 0.2, seed=35)
+    q = W.random_q(c.n, 36, 2)
+    r = orc.Matrix(c, q=q).run(5, 6, 3, 40, ("trace",))
+    assert r["trace_series"].shape == (40,)
+    assert r["trace_series"].sum() == pytest.approx(r["trace"].sum(), rel=1e-12)
+    est, _ = orc.estimate(r["trace"], 40, group_size=6)
+    assert r["trace_series"].mean() / 6 == pytest.approx(est, rel=1e-12)

@@ -1,0 +1,12 @@
+#!/bin/bash
+# v6 parity + timings + one ncu capture of v6 at 512 threads (config 2)
+cd "$GRAFT_REPO_ROOT" || exit 1
+mkdir -p gpurun_out
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || { echo build failed; exit 1; }
+timeout 900 python -m pytest tests -m gpu -q -x -k "v6 or gaussian or philox or config2_reduced or irregular or long_dependency or config1_full or chains_per_thread or z2 or config4_production" > gpurun_out/pytest_v6.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_v6.log
+: > gpurun_out/v6_time.log
+for k in "v5 1024" "v6 512" "v6 768" "v6 640" "v6 384"; do
+  set -- $k
+  MCINV_KERNEL=$1 MCINV_THREADS=$2 timeout 120 python tools/run_one.py --config 2 --sweeps 220 --burn 20 --repeat 3 >> gpurun_out/v6_time.log 2>&1; echo "$k rc=$?" >> gpurun_out/v6_time.log
+done
+MCINV_KERNEL=v6 MCINV_THREADS=512 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"sweep6" -c 1 -o gpurun_out/ncu_v6 -f python tools/run_one.py --config 2 --sweeps 12 --burn 2 > gpurun_out/ncu_v6.log 2>&1; echo "ncu rc=$?" >> gpurun_out/ncu_v6.log
