@@ -177,8 +177,10 @@ std::vector<int> schedule_slots(int64_t n, const std::vector<int4> &rec, const s
                                 int L, int ecap, int similar) {
     // row i -> level-order index o; lower neighbours (the first nlow entries) and the
     // reverse edges (upper neighbours)
+    // (records with x < 0 are not rows -- the trace items of v5 -- and nothing waits on them)
     std::vector<int> ord_of(n);
-    for (int64_t o = 0; o < n; ++o) ord_of[rec[o].x] = (int)o;
+    for (int64_t o = 0; o < n; ++o)
+        if (rec[o].x >= 0) ord_of[rec[o].x] = (int)o;
     std::vector<int> up_cnt(n + 1, 0);
     for (int64_t o = 0; o < n; ++o)
         for (int e = 0; e < (int)((unsigned)rec[o].z >> 16); ++e) up_cnt[ord_of[ent_col[rec[o].y + e]] + 1]++;

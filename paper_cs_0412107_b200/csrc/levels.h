@@ -75,6 +75,8 @@ std::string build_levels(const LevelInput &in, LevelPlan &out);
 // earliest, and padded (-1) only when no row is left. Input: the level-order
 // records (i, entry begin, count | lower << 16) and entry columns of the plan.
 // Output: slot -> level-order index (or -1 for padding); size a multiple of R.
+// n counts the records; records with x < 0 are items that wait on their entries like
+// rows but that nothing waits on (v5's trace items).
 // ecap > 0: a group takes no further row once its entries would exceed ecap (a
 // single row may exceed it alone): bounds the group blocks staged by v5.
 // similar > 0: a group's rows after the first are chosen among the next `similar`

@@ -54,8 +54,9 @@ struct Entry {
 struct LevelDev {
     DevBuf ph_row, ord_rec, ent_col, ent_ab, ent_pz, ord_dsg;
     DevBuf ph_tq, tq_row, tq_eptr, tq_col, tq_val, ph_pp, pp_i, pp_j, pp_slot;
-    int D = 0, max_rows = 0;
-    bool deferred = false;                   // deferred items exist (v4 cannot run this plan)
+    int D = 0, max_rows = 0, ntq = 0;
+    bool deferred = false;                   // deferred items exist (v4 / v6 cannot run this plan)
+    bool deferred_pairs = false;             // deferred pattern pairs exist (v5 cannot run this plan)
     std::string error;
     mcinv::LevelPlan host;                   // kept only for mcinv_debug_levels
     std::vector<int4> h_rec;                 // level-order records, for the v4 slot arrays
@@ -64,6 +65,8 @@ struct LevelDev {
     std::vector<int> h_ent_col;              // level-order entry columns (v4 slot ordering)
     std::vector<unsigned char> h_ab;         // level-order {a, b} pairs (raw bytes of S), for v5 blocks
     std::vector<int> h_pz;                   // level-order pattern slot pairs (empty without pattern)
+    std::vector<int> h_tq_row, h_tq_eptr, h_tq_col;  // trace items (v5 schedules them as dataflow items)
+    std::vector<unsigned char> h_tq_val;     // their Q values (raw bytes of S)
     struct Slots {
         DevBuf rec, dsg;
         int nslots = 0;
@@ -651,6 +654,8 @@ LevelDev *get_levels(mcinv_ctx *ctx, unsigned outputs) {
         up(ld->pp_slot, P.pp_slot);
         if (st != MCINV_OK && ld->error.empty()) ld->error = "level plan upload failed";
         ld->deferred = !P.pp_i.empty() || !P.tq_row.empty();
+        ld->deferred_pairs = !P.pp_i.empty();
+        ld->ntq = (int)P.tq_row.size();
         ld->h_rec = rec;
         ld->h_dsg.assign(reinterpret_cast<const unsigned char *>(dsg.data()),
                          reinterpret_cast<const unsigned char *>(dsg.data() + dsg.size()));
@@ -659,6 +664,11 @@ LevelDev *get_levels(mcinv_ctx *ctx, unsigned outputs) {
         ld->h_ab.assign(reinterpret_cast<const unsigned char *>(ab.data()),
                         reinterpret_cast<const unsigned char *>(ab.data() + ab.size()));
         ld->h_pz = P.ent_pz;
+        ld->h_tq_row = P.tq_row;
+        ld->h_tq_eptr = P.tq_eptr;
+        ld->h_tq_col = P.tq_col;
+        ld->h_tq_val.assign(reinterpret_cast<const unsigned char *>(tqv.data()),
+                            reinterpret_cast<const unsigned char *>(tqv.data() + tqv.size()));
         if (!ctx->host_only) P = mcinv::LevelPlan();  // device copy only
     }
     LevelDev *raw = ld.get();
@@ -700,7 +710,38 @@ LevelDev::Slots *get_slots(mcinv_ctx *ctx, LevelDev *lv, int R, int W, bool bloc
     std::unique_ptr<LevelDev::Slots> sl(new LevelDev::Slots());
     std::vector<int4> rec;
     std::vector<S> dsg;
-    const S *hd = reinterpret_cast<const S *>(lv->h_dsg.data());
+    // v5 with trace: each trace item (Eq. tr, reading R2: conj(w_i) sum_j Q_ij z_j) joins the
+    // schedule as a record that waits on rows i and j of its Q row (entries [i, Q cols..],
+    // all waited for; coefficients {0, Q_ij}), is placed after them like a row after its
+    // lower neighbours, and that no row waits on: record x = -2 - i
+    const bool trace_items = blocks && !lv->h_tq_row.empty();
+    std::vector<int4> xrec = lv->h_rec;
+    std::vector<int> xcol = lv->h_ent_col;
+    std::vector<unsigned char> xab = lv->h_ab;
+    std::vector<int> xpz = lv->h_pz;
+    std::vector<unsigned char> xdsg = lv->h_dsg;
+    if (trace_items) {
+        const S *qv = reinterpret_cast<const S *>(lv->h_tq_val.data());
+        for (size_t t = 0; t < lv->h_tq_row.size(); ++t) {
+            const int i = lv->h_tq_row[t], b = lv->h_tq_eptr[t], e = lv->h_tq_eptr[t + 1];
+            const int cnt = 1 + (e - b);
+            xrec.push_back(make_int4(-2 - i, (int)xcol.size(), (int)((unsigned)cnt | (unsigned)cnt << 16), -1));
+            xcol.push_back(i);
+            const ZW<S> zero{};
+            xab.insert(xab.end(), reinterpret_cast<const unsigned char *>(&zero),
+                       reinterpret_cast<const unsigned char *>(&zero) + sizeof(zero));
+            for (int q = b; q < e; ++q) {
+                xcol.push_back(lv->h_tq_col[q]);
+                const ZW<S> c{qv[q], S{}};
+                xab.insert(xab.end(), reinterpret_cast<const unsigned char *>(&c),
+                           reinterpret_cast<const unsigned char *>(&c) + sizeof(c));
+            }
+            if (!xpz.empty()) xpz.insert(xpz.end(), 2 * (size_t)cnt, -1);
+            xdsg.insert(xdsg.end(), 2 * sizeof(S), 0);
+        }
+    }
+    const int64_t nrec = (int64_t)xrec.size();
+    const S *hd = reinterpret_cast<const S *>(xdsg.data());
     // slot order: the list schedule (levels.h schedule_slots) with a slack of L = W groups
     // (the warps of a CTA); MCINV_SLOT_ORDER=level keeps plain level order (each level padded)
     const char *so = std::getenv("MCINV_SLOT_ORDER");
@@ -714,7 +755,7 @@ LevelDev::Slots *get_slots(mcinv_ctx *ctx, LevelDev *lv, int R, int W, bool bloc
             while (order.size() % R) order.push_back(-1);
         }
     } else if (const char *e = std::getenv("MCINV_SLACK")) {
-        order = mcinv::schedule_slots(ctx->n, lv->h_rec, lv->h_ent_col, R, std::atoi(e), blocks ? ecap : 0, sim);
+        order = mcinv::schedule_slots(nrec, xrec, xcol, R, std::atoi(e), blocks ? ecap : 0, sim);
     } else {
         // the largest slack (W, 3W/4, W/2, 3W/8, ..., 1 groups) whose schedule pads at most
         // 5% of the slots (MCINV_SLACK_PAD, percent): wide DAGs (config 2: L = 24 of 32,
@@ -733,9 +774,8 @@ LevelDev::Slots *get_slots(mcinv_ctx *ctx, LevelDev *lv, int R, int W, bool bloc
         size_t best_size = 0;
         bool found = false;
         for (int L : cand) {
-            const std::vector<int> o = mcinv::schedule_slots(ctx->n, lv->h_rec, lv->h_ent_col, R, L,
-                                                             blocks ? ecap : 0, 0);
-            if ((double)o.size() <= (double)ctx->n * (1.0 + pad / 100.0)) {
+            const std::vector<int> o = mcinv::schedule_slots(nrec, xrec, xcol, R, L, blocks ? ecap : 0, 0);
+            if ((double)o.size() <= (double)nrec * (1.0 + pad / 100.0)) {
                 chosen = L;
                 found = true;
                 break;
@@ -746,7 +786,7 @@ LevelDev::Slots *get_slots(mcinv_ctx *ctx, LevelDev *lv, int R, int W, bool bloc
             }
         }
         (void)found;
-        order = mcinv::schedule_slots(ctx->n, lv->h_rec, lv->h_ent_col, R, chosen, blocks ? ecap : 0, sim);
+        order = mcinv::schedule_slots(nrec, xrec, xcol, R, chosen, blocks ? ecap : 0, sim);
     }
     for (int o : order) {
         if (o < 0) {
@@ -754,7 +794,7 @@ LevelDev::Slots *get_slots(mcinv_ctx *ctx, LevelDev *lv, int R, int W, bool bloc
             dsg.push_back(S{});
             dsg.push_back(S{});
         } else {
-            rec.push_back(lv->h_rec[o]);
+            rec.push_back(xrec[o]);
             dsg.push_back(hd[2 * o]);
             dsg.push_back(hd[2 * o + 1]);
         }
@@ -769,9 +809,9 @@ LevelDev::Slots *get_slots(mcinv_ctx *ctx, LevelDev *lv, int R, int W, bool bloc
         // row's last column (its own row if it has none): the unrolled fma chain then needs no
         // predicate, and fma(0, v, a) == a for the finite states of a converging run (only the
         // sign of an exact zero sum can differ). EP a multiple of 4; sections 16-B aligned.
-        const bool pat = !lv->h_pz.empty();
+        const bool pat = !xpz.empty();
         auto padded = [KU](int c) { return (c + KU - 1) / KU * KU; };
-        const ZW<S> *hab = reinterpret_cast<const ZW<S> *>(lv->h_ab.data());
+        const ZW<S> *hab = reinterpret_cast<const ZW<S> *>(xab.data());
         const size_t ng = rec.size() / R;
         // Wait masks (v6): row i must see its lower neighbours j final before its update.
         // Waiting on j is implied, and dropped, when (a) j is itself a lower neighbour of
@@ -786,7 +826,7 @@ LevelDev::Slots *get_slots(mcinv_ctx *ctx, LevelDev *lv, int R, int W, bool bloc
             grp_of.assign(ctx->n, -1);
             for (int64_t o = 0; o < ctx->n; ++o) ord_of[lv->h_rec[o].x] = (int)o;
             for (size_t t = 0; t < order.size(); ++t)
-                if (order[t] >= 0) grp_of[lv->h_rec[order[t]].x] = (int)(t / R);
+                if (order[t] >= 0 && xrec[order[t]].x >= 0) grp_of[xrec[order[t]].x] = (int)(t / R);
         }
         auto lower_has = [&](int jp, int j) {  // is j a lower neighbour of jp?
             const int4 r = lv->h_rec[ord_of[jp]];
@@ -819,7 +859,7 @@ LevelDev::Slots *get_slots(mcinv_ctx *ctx, LevelDev *lv, int R, int W, bool bloc
         for (size_t g = 0; g < ng; ++g) {
             int E = 0;
             for (int r = 0; r < R; ++r)
-                if (rec[g * R + r].x >= 0) E += padded(rec[g * R + r].z & 0xffff);
+                if (rec[g * R + r].x != -1) E += padded(rec[g * R + r].z & 0xffff);
             const int EP = (E + 3) / 4 * 4;
             const size_t off_wm = 16 + 16 * (size_t)R + 2 * sizeof(S) * R;  // masks (wmask) before the columns
             const size_t off_col = off_wm + mask_bytes;
@@ -833,20 +873,19 @@ LevelDev::Slots *get_slots(mcinv_ctx *ctx, LevelDev *lv, int R, int W, bool bloc
             int e = 0;
             for (int r = 0; r < R; ++r) {
                 const int4 q = rec[g * R + r];
-                const int cnt = q.x >= 0 ? q.z & 0xffff : 0;
-                reinterpret_cast<int4 *>(b + 16)[r] = make_int4(q.x, e, q.x >= 0 ? q.z : 0, q.w);
+                const int cnt = q.x != -1 ? q.z & 0xffff : 0;  // rows and trace items carry entries
+                reinterpret_cast<int4 *>(b + 16)[r] = make_int4(q.x, e, q.x != -1 ? q.z : 0, q.w);
                 reinterpret_cast<S *>(b + 16 + 16 * R)[2 * r] = dsg[2 * (g * R + r)];
                 reinterpret_cast<S *>(b + 16 + 16 * R)[2 * r + 1] = dsg[2 * (g * R + r) + 1];
                 if (wmask) reinterpret_cast<unsigned *>(b + off_wm)[r] = q.x >= 0 ? wait_mask(q) : 0u;
                 for (int t = 0; t < cnt; ++t) {
-                    reinterpret_cast<int *>(b + off_col)[e + t] = lv->h_ent_col[q.y + t];
+                    reinterpret_cast<int *>(b + off_col)[e + t] = xcol[q.y + t];
                     reinterpret_cast<ZW<S> *>(b + off_ab)[e + t] = hab[q.y + t];
                     if (pat) {
-                        reinterpret_cast<int2 *>(b + off_pz)[e + t] =
-                            make_int2(lv->h_pz[2 * (q.y + t)], lv->h_pz[2 * (q.y + t) + 1]);
+                        reinterpret_cast<int2 *>(b + off_pz)[e + t] = make_int2(xpz[2 * (q.y + t)], xpz[2 * (q.y + t) + 1]);
                     }
                 }
-                const int last = cnt > 0 ? lv->h_ent_col[q.y + cnt - 1] : q.x;
+                const int last = cnt > 0 ? xcol[q.y + cnt - 1] : (q.x >= 0 ? q.x : 0);
                 for (int t = cnt; t < padded(cnt); ++t) {
                     reinterpret_cast<int *>(b + off_col)[e + t] = last;  // ab[e + t] stays zero
                     if (pat) reinterpret_cast<int2 *>(b + off_pz)[e + t] = make_int2(-1, -1);
@@ -942,12 +981,16 @@ mcinv_status run_typed(mcinv_ctx *ctx, const mcinv_run_args *a, const Layout &L,
     // slots per warp) fits, else v4 when its byte counters fit (n <= 200k), else v3.
     // MCINV_KERNEL=v3|v4|v5 forces one (error if it does not apply).
     const int pref = kernel_pref();
-    const bool flow_ok = lv && L.lgC <= 5 && !lv->deferred;
+    // v5 also runs trace items (as a phase after each sampling sweep); v4 / v6 need a plan
+    // without deferred items
+    const bool trace_flow = lv && L.lgC <= 5 && lv->deferred && !lv->deferred_pairs;
+    const bool flow_ok = lv && L.lgC <= 5 && (!lv->deferred || (trace_flow && pref != 4 && pref != 6));
     if ((pref == 4 || pref == 5 || pref == 6) && !flow_ok)
         return fail(ctx, MCINV_E_INVALID, "dataflow kernel not applicable to this run");
     // v6 (v5 with the two chains of a Box-Muller pair per thread): real C, at least 2 chains
     // per CTA, both chains of a thread in one SE group (group_size >= 2: even chain_begin)
-    const bool v6_ok = flow_ok && ctx->dtype == MCINV_F64 && L.lgC >= 1 && L.lgP >= 1 && a->group_size >= 2;
+    const bool v6_ok = flow_ok && !lv->deferred && ctx->dtype == MCINV_F64 && L.lgC >= 1 && L.lgP >= 1 &&
+                       a->group_size >= 2;
     if (pref == 6 && !v6_ok) return fail(ctx, MCINV_E_INVALID, "v6 kernel not applicable to this run");
     // auto: dataflow only up to 200k rows -- beyond, v3 (level barriers, K = 2 chains per
     // thread) measured 15-20% faster than v5 with bit counters at n = 1e6 (C = 8/16/32:
@@ -1002,6 +1045,11 @@ mcinv_status run_typed(mcinv_ctx *ctx, const mcinv_run_args *a, const Layout &L,
         v5 = false;
     }
     if (v6) lgK = 1;
+    if (v4 && !v5 && !v6 && lv->deferred) {  // trace items need v5 (its smem did not fit): level kernel
+        if (pref == 5) return fail(ctx, MCINV_E_INVALID, "v5 blocks do not fit shared memory");
+        v4 = false;
+        threads3 = threads_for(false);
+    }
     if (v4 && !v5 && !v6) {
         if (n > 200000) {  // v4's byte counters do not fit: level kernel (its layout is the same)
             if (pref == 4) return fail(ctx, MCINV_E_INVALID, "v4 counters do not fit shared memory");

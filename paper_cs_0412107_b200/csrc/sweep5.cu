@@ -162,6 +162,8 @@ __global__ void __launch_bounds__(NT, 1) sweep5_kernel(const Sweep3Params<S> p) 
     uint32_t ph0 = 0, ph1 = 0;
     int item = 0;
     bool dv = false;  // divergence seen (reading R12: every stored value is a sweep-end value)
+    const bool want_tr = p.outputs & OUT_TRACE;
+    S tr = zero_s<S>(), trs = zero_s<S>();  // the chain's trace over the launch / over the current sweep
     for (int s = p.s_begin; s < p.s_end; ++s) {
         const uint32_t k = p.sweep_abs0 + static_cast<uint32_t>(s);
         const bool sampling = s >= p.burn_in;
@@ -191,6 +193,31 @@ __global__ void __launch_bounds__(NT, 1) sweep5_kernel(const Sweep3Params<S> p) 
             const int i = rec.x, cnt = valid ? rec.z & 0xffff : 0;
             S zi = zero_s<S>(), wi = zero_s<S>();
             double phi = 0.0;
+            if (rec.x <= -2) {
+                // a trace item of row -2 - rec.x (scheduled after rows i and j of its Q row, whose
+                // sweep-s values then hold until the sweep barrier): entries [i, Q cols], waited
+                // for, then conj(w_i) sum_j Q_ij z_j (Eq. tr, reading R2). Sampling sweeps only.
+                if (sampling) {
+                    const int tc = rec.z & 0xffff;
+                    for (int e = 0; e < tc; ++e) {
+                        const int j = col[e];
+                        auto ready = [&]() -> bool {
+                            if constexpr (BITS)
+                                return ((reinterpret_cast<volatile unsigned *>(dbits)[j >> 5] >> (j & 31)) & 1u) ==
+                                       (need & 1u);
+                            else
+                                return reinterpret_cast<volatile unsigned char *>(done)[j] == need;
+                        };
+                        wait_ready(ready, p.err, 0);
+                    }
+                    __threadfence_block();  // acquire
+                    S qz = zero_s<S>();
+                    for (int e = 1; e < tc; ++e) qz = add_s(qz, mul_s(ab[e].z, ld_zw(zrow(zcol, col[e], zst)).z));
+                    trs = add_s(trs, zwc_s(qz, ld_zw(zrow(zcol, col[0], zst)).w));
+                }
+                // (then on through the warp's collective steps as an invalid row: no update,
+                // no publication, zero products)
+            }
             if (valid) {
                 const int nlow = static_cast<int>(static_cast<unsigned>(rec.z) >> 16);
                 // upper neighbours hold their sweep s-1 values until this row publishes: start
@@ -251,9 +278,31 @@ __global__ void __launch_bounds__(NT, 1) sweep5_kernel(const Sweep3Params<S> p) 
             // orders every lane's reads of this item's block before the next item's TMA into it
             __syncwarp();
         }
+        if (want_tr && sampling) {  // Geyer's series: this sweep's realized trace of the warp's chains
+            if (p.series) {
+                const S v = group_sum<32>(active ? trs : zero_s<S>());
+                if (lane == 0) slot_red(p.series + (int64_t)(p.series_base + s - p.burn_in) * E, v);
+            }
+            tr = add_s(tr, trs);
+            trs = zero_s<S>();
+        }
         __syncthreads();  // sweep boundary: all reads of sweep s values are done
     }
     if (dv && active) atomicAdd(p.bad, 1.0);
+    if (want_tr) {
+        // per-chain trace: sum over the threads of each chain (shared memory, the block area is
+        // free after the last barrier), then over the P chains of a group, one red per group
+        S *red = reinterpret_cast<S *>(sm5);
+        red[tid] = active ? tr : zero_s<S>();
+        __syncthreads();
+        if (w == 0) {  // C <= 32: the chains' sums in the lanes c < C of warp 0
+            S v = zero_s<S>();
+            if (lane < C)
+                for (int h = lane; h < B; h += C) v = add_s(v, red[h]);
+            v = group_sum<P>(v);
+            if (lane < C && gleader && active) slot_red(p.slot_trace + grp * E, v);
+        }
+    }
 }
 
 size_t sweep5_smem(int n, int threads, int maxb) {
@@ -272,7 +321,8 @@ cudaError_t launch5b(const Sweep3Params<S> &p, int threads, cudaStream_t st) {
     constexpr int NT = kReal ? 1024 : 768, KU = kReal ? 4 : 2;
     if (threads > NT) return cudaErrorInvalidConfiguration;
     const int blocks = (p.chains + (1 << LGC) - 1) >> LGC;
-    const size_t smem = sweep5_smem(p.n, threads, p.maxb);
+    size_t smem = sweep5_smem(p.n, threads, p.maxb);
+    if ((p.outputs & OUT_TRACE) && smem < (size_t)threads * sizeof(S)) smem = (size_t)threads * sizeof(S);
     // the Gaussian-only variant for byte counters (the common case); bit counters keep the switch
     auto k = (!BITS && p.noise == 0) ? sweep5_kernel<S, KU, NT, LGC, LGP, BITS, !BITS>
                                      : sweep5_kernel<S, KU, NT, LGC, LGP, BITS, false>;

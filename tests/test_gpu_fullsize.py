@@ -86,8 +86,8 @@ def test_config4_production_layout(mc):
 
 
 def test_config5_production_layout(mc):
-    """Config 5 (16^4 complex lattice, 16384 chains, diag + trace: the level
-    kernel with L2-blocked waves of C = 16 chains per CTA) for 2 burn-in + 1
+    """Config 5 (16^4 complex lattice, 16384 chains, diag + trace: the dataflow
+    kernel v5 with its trace phase, L2-blocked waves of C = 16 chains per CTA) for 2 burn-in + 1
     sampling sweep: chains 0, 8191, 16383 vs the oracle, and the diag and
     trace (w^dagger Q z, reading R2) sums of SE groups 0 and 511."""
     c, q, run = W.config(5)
@@ -283,3 +283,23 @@ def test_recenter_protocol_on_one_gpu(mc):
     nS1 = m2[0].numel()
     assert normwise(tot.cpu().numpy()[:nS1], want[:nS1]) < 1e-12
     assert normwise(m2sum, want[nS1:2 * nS1]) < 1e-10
+
+
+def test_config2_production_layout(mc):
+    """Config 2 as bench.py times it (1024 chains: the v6 dataflow kernel, C = 8,
+    two chains per thread, 512 threads) for 2 burn-in + 1 sampling sweep: chains
+    0, 513, 1023 vs the oracle, and the diag and pattern sums of SE groups 0 and
+    31 vs the oracle's."""
+    c, _, run = W.config(2)
+    inv = mc.Inverter(c)
+    inv.run(run.seed, run.chains, 2, 1, run.outputs, group_size=run.group_size)
+    info, lc = inv.kernel_info(), inv.launch_config()
+    assert info["version"] == 6 and lc["chains_per_thread"] == 2, (info, lc)
+    picks = [0, 513, 1023]
+    r = oracle_chains(2, picks, 2, 1)
+    check_states(inv, r, picks)
+    chains = list(range(32)) + list(range(1024 - 32, 1024))
+    rg = oracle_chains(2, chains, 2, 1, ("diag", "pattern"))
+    check_groups(inv, "diag", [0, 31], rg, 32)
+    check_groups(inv, "pattern", [0, 31], rg, 32)
+    inv.close()

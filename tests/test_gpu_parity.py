@@ -292,13 +292,32 @@ def test_v4_dataflow(mc, orc, monkeypatch, kernel):
     monkeypatch.delenv("MCINV_C")
     monkeypatch.delenv("MCINV_THREADS")
     # automatic choice: v4 where it applies (configs 2, 3), v3 for C > 32 or trace (configs 4, 5)
-    for k, ver in ((3, (4, 5)), (2, (4, 5, 6)), (5, (3,))):
+    for k, ver in ((3, (4, 5)), (2, (4, 5, 6)), (5, (5,))):
         c, q, run = W.config(k)
         inv = mc.Inverter(c, q=q)
         inv.run(run.seed, run.chains, 0, 1, tuple(o for o in run.outputs if o != "full") or ("diag",),
                 group_size=run.group_size)
         assert inv.kernel_info()["version"] in ver, k
         inv.close()
+
+
+@pytest.mark.parametrize("threads", ["768", "512", "96"])
+def test_v5_trace_phase(mc, orc, monkeypatch, threads):
+    """v5 with trace items (w^dagger Q z, reading R2) as a phase after every
+    sampling sweep: complex and real C, every chains-per-CTA layout up to a
+    warp, Gaussian and Z2 noise, the per-sweep series, several launches."""
+    monkeypatch.setenv("MCINV_KERNEL", "v5")
+    monkeypatch.setenv("MCINV_THREADS", threads)
+    c = W.lattice(4, 3, 0.15, seed=81)
+    q = W.random_q(c.n, 82, 4)
+    p = W.pedigree(500, seed=83)
+    qp = W.random_q(p.n, 84, 3, complex_=False)
+    for C in (1, 4, 16, 32):
+        monkeypatch.setenv("MCINV_C", str(C))
+        compare_run(mc, orc, c, q=q, seed=21, chains=64, burn_in=2, cycles=5, outputs=("diag", "trace"),
+                    group_size=8)
+        compare_run(mc, orc, p, q=qp, seed=22, chains=96, burn_in=3, cycles=4, outputs=("trace", "diag", "pattern"),
+                    group_size=16, noise="z2" if C == 4 else "gauss")
 
 
 @pytest.mark.parametrize("threads", ["512", "768", "1024", "256"])

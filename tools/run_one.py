@@ -43,7 +43,8 @@ def main():
         st = inv.stats()
         sites = chains * c.n * a.sweeps
         print(f"config {a.config} chains {chains} sweeps {a.sweeps}: wall {dt * 1e3:.1f} ms, sweep kernel "
-              f"{st['sweep_ms']:.1f} ms ({st['sweep_launches']} launches), {sites / (st['sweep_ms'] / 1e3):.3e} "
+              f"{st['sweep_ms']:.1f} ms ({st['sweep_launches']} launches), contraction {st['contract_ms']:.1f} ms, "
+              f"{sites / (st['sweep_ms'] / 1e3):.3e} "
               f"site-updates/s, kernel {inv.kernel_info()}", flush=True)
 
 
