@@ -290,9 +290,10 @@ __global__ void __launch_bounds__(32 * 2 * (BN / WN), 2) contract_tma_kernel(con
     constexpr int BOX = TmaTile<S>::kBoxElems, NBOX = TmaTile<S>::kBoxes;
     constexpr uint32_t kBoxBytes = 64 * 128;                    // 64 rows x 128 B
     constexpr uint32_t kStageBytes = 2 * NBOX * kBoxBytes;      // X and Y
-    extern __shared__ __align__(1024) unsigned char smem_raw[];
-    // 1024-B aligned base for the swizzled boxes; the mbarriers after the stages
-    unsigned char *base = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    extern __shared__ __align__(128) unsigned char smem_tma[];
+    // 1024-B aligned base for the swizzled boxes (1 KB of slack is allocated); the mbarriers
+    // and the stage counters after the stages
+    unsigned char *base = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_tma) + 1023) & ~uintptr_t(1023));
     const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(base));
     const uint32_t bars = sbase + KS * kStageBytes;
     // per stage: how many warps are done with it; the last one refills it (no CTA barrier)

@@ -33,9 +33,52 @@ __device__ __forceinline__ ZW2 ld_zw2(const ZW<double> *p) {
 
 // Eq. (4)/(5) fma chains of both chains from a staged block: entries padded by the
 // host to a multiple of KU with zero coefficients on a valid column (no predicate)
+#ifndef MCINV_V6_CHUNKS
+#define MCINV_V6_CHUNKS 1  // gather chunks of KU entries in flight at once (A/B knob)
+#endif
 template <int KU>
 __device__ __forceinline__ void row_sums2(const ZW<double> *zcol, const int *col, const ZW<double> *ab, int cnt,
                                           uint32_t zst, double (&az)[2], double (&aw)[2]) {
+    if constexpr (MCINV_V6_CHUNKS == 2) {
+        // two chunks in flight: the second one predicated on the row having it (rows are
+        // padded to KU entries, so a chunk is all there or absent); an absent chunk gathers
+        // the first chunk's lines again (L1 hits) and skips its fma
+        for (int e0 = 0; e0 < cnt; e0 += 2 * KU) {
+            const bool two = e0 + KU < cnt;
+            int j[2 * KU];
+            ZW2 v[2 * KU];
+            ZW<double> c[2 * KU];
+#pragma unroll
+            for (int q = 0; q < KU; ++q) {
+                j[q] = col[e0 + q];
+                j[KU + q] = two ? col[e0 + KU + q] : j[q];
+            }
+#pragma unroll
+            for (int q = 0; q < 2 * KU; ++q) v[q] = ld_zw2(zrow(zcol, j[q], zst));
+#pragma unroll
+            for (int q = 0; q < KU; ++q) {
+                c[q] = ab[e0 + q];
+                c[KU + q] = two ? ab[e0 + KU + q] : ZW<double>{0.0, 0.0};
+            }
+#pragma unroll
+            for (int q = 0; q < KU; ++q)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    az[h] = fma(c[q].z, v[q].v[h].z, az[h]);
+                    aw[h] = fma(c[q].w, v[q].v[h].w, aw[h]);
+                }
+            if (two) {
+#pragma unroll
+                for (int q = KU; q < 2 * KU; ++q)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        az[h] = fma(c[q].z, v[q].v[h].z, az[h]);
+                        aw[h] = fma(c[q].w, v[q].v[h].w, aw[h]);
+                    }
+            }
+        }
+        return;
+    }
     for (int e0 = 0; e0 < cnt; e0 += KU) {
         int j[KU];
         ZW2 v[KU];
