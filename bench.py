@@ -156,7 +156,15 @@ def _cpu_clocks() -> str:
         if ":" in line:
             k, v = line.split(":", 1)
             d[k.strip()] = v.strip()
-    return (f"{d.get('Model name', '?')}, {d.get('CPU(s)', '?')} CPUs, max {d.get('CPU max MHz', '?')} MHz, "
+    mhz = d.get("CPU max MHz")
+    if mhz is None:  # VMs often hide the range: the current clock from /proc/cpuinfo
+        try:
+            with open("/proc/cpuinfo") as f:
+                cur = [float(l.split(":", 1)[1]) for l in f if l.startswith("cpu MHz")]
+            mhz = f"{max(cur):.0f} (current, /proc/cpuinfo)" if cur else "?"
+        except (OSError, ValueError):
+            mhz = "?"
+    return (f"{d.get('Model name', '?')}, {d.get('CPU(s)', '?')} CPUs, max {mhz} MHz, "
             f"min {d.get('CPU min MHz', '?')} MHz")
 
 

@@ -50,7 +50,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
     with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 1)) as ex:
         results = list(ex.map(compile_one, SOURCES))
-    link = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", tmp] + [o for o, _, _ in results]
+    link = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", tmp] + [o for o, _, _ in results] + ["-lpthread"]
     lr = subprocess.run(link, capture_output=True, text=True)
     log = os.path.join(HERE, "build.log")
     with open(log, "w") as f:

@@ -14,6 +14,7 @@
 #include <vector>
 
 #include <cstdlib>
+#include <future>
 #include <map>
 #include <memory>
 #include <tuple>
@@ -768,24 +769,28 @@ LevelDev::Slots *get_slots(mcinv_ctx *ctx, LevelDev *lv, int R, int W, bool bloc
             cand.push_back(L);
             if (L >= 4 && (3 * L / 4) < L) cand.push_back(3 * L / 4);
         }
-        // (the slack is chosen on schedules without the similarity window -- cheap -- and the
-        // final order is then built once with it)
+        // (the slack is chosen on schedules without the similarity window -- cheap, and the
+        // candidates are scheduled concurrently on host threads -- and the final order is then
+        // built once with it)
+        std::vector<std::future<size_t>> sizes;
+        for (int L : cand)
+            sizes.push_back(std::async(std::launch::async, [&, L] {
+                return mcinv::schedule_slots(nrec, xrec, xcol, R, L, blocks ? ecap : 0, 0).size();
+            }));
         int chosen = 1;
         size_t best_size = 0;
-        bool found = false;
-        for (int L : cand) {
-            const std::vector<int> o = mcinv::schedule_slots(nrec, xrec, xcol, R, L, blocks ? ecap : 0, 0);
-            if ((double)o.size() <= (double)nrec * (1.0 + pad / 100.0)) {
-                chosen = L;
-                found = true;
+        for (size_t k = 0; k < cand.size(); ++k) {
+            const size_t sz = sizes[k].get();
+            if ((double)sz <= (double)nrec * (1.0 + pad / 100.0)) {
+                chosen = cand[k];
+                for (size_t q = k + 1; q < cand.size(); ++q) sizes[q].wait();
                 break;
             }
-            if (best_size == 0 || o.size() < best_size) {
-                best_size = o.size();
-                chosen = L;
+            if (best_size == 0 || sz < best_size) {
+                best_size = sz;
+                chosen = cand[k];
             }
         }
-        (void)found;
         order = mcinv::schedule_slots(nrec, xrec, xcol, R, chosen, blocks ? ecap : 0, sim);
     }
     for (int o : order) {
@@ -1023,7 +1028,10 @@ mcinv_status run_typed(mcinv_ctx *ctx, const mcinv_run_args *a, const Layout &L,
         if (!std::getenv("MCINV_THREADS")) threads3 = v6_threads();
         const int R = 64 >> L.lgC, W = threads3 / 32, ku = mcinv::sweep6_ku(threads3);
         const size_t counters = n > mcinv::kByteCounters ? ((size_t)n + 127) / 128 * 16 : ((size_t)n + 15) / 16 * 16;
-        const long budget = ((long)(220 * 1024) - (long)counters) / (2 * W) - 16 - 36 * R - 64;
+        // shared-memory budget of one CTA (MCINV_V6_SMEM_KB: smaller budgets let several CTAs share an SM)
+        long smem_budget = 220 * 1024;
+        if (const char *e = std::getenv("MCINV_V6_SMEM_KB")) smem_budget = std::atol(e) * 1024;
+        const long budget = (smem_budget - (long)counters) / (2 * W) - 16 - 36 * R - 64;
         int ecap = std::max(8, std::min<int>(block_entries() * R / 4, (int)(budget / 28)));
         if (const char *e = std::getenv("MCINV_BLOCK_ENTRIES")) ecap = std::atoi(e);
         // the cap counts unpadded entries: shrink it until the padded blocks fit

@@ -211,9 +211,18 @@ __global__ void __launch_bounds__(NT, 1) sweep5_kernel(const Sweep3Params<S> p) 
                         wait_ready(ready, p.err, 0);
                     }
                     __threadfence_block();  // acquire
+                    // w_i and the first gathers of z_j all in flight before the products
+                    constexpr int TU = 4;
+                    const S wt = ld_zw(zrow(zcol, col[0], zst)).w;
+                    S zj[TU];
+#pragma unroll
+                    for (int q = 0; q < TU; ++q) zj[q] = 1 + q < tc ? ld_zw(zrow(zcol, col[1 + q], zst)).z : zero_s<S>();
                     S qz = zero_s<S>();
-                    for (int e = 1; e < tc; ++e) qz = add_s(qz, mul_s(ab[e].z, ld_zw(zrow(zcol, col[e], zst)).z));
-                    trs = add_s(trs, zwc_s(qz, ld_zw(zrow(zcol, col[0], zst)).w));
+#pragma unroll
+                    for (int q = 0; q < TU; ++q)
+                        if (1 + q < tc) qz = add_s(qz, mul_s(ab[1 + q].z, zj[q]));
+                    for (int e = 1 + TU; e < tc; ++e) qz = add_s(qz, mul_s(ab[e].z, ld_zw(zrow(zcol, col[e], zst)).z));
+                    trs = add_s(trs, zwc_s(qz, wt));
                 }
                 // (then on through the warp's collective steps as an invalid row: no update,
                 // no publication, zero products)
