@@ -251,7 +251,11 @@ __global__ void __launch_bounds__(NT, 1) sweep6_kernel(const Sweep3Params<double
             if (valid) {
                 const int nlow = static_cast<int>(static_cast<unsigned>(rec.z) >> 16);
                 // every neighbour's line on its way into L2 while the noise runs
-                if (p.prefetch) {
+                if (p.prefetch == 1) {  // into L1 (the SM's own L1 sees its CTA's stores)
+                    for (int e0 = 0; e0 < cnt; e0 += KU)
+#pragma unroll
+                        for (int q = 0; q < KU; ++q) prefetch_l1(zrow(zcol, col[e0 + q], zst));
+                } else if (p.prefetch) {
                     for (int e0 = 0; e0 < cnt; e0 += KU)
 #pragma unroll
                         for (int q = 0; q < KU; ++q) prefetch_l2(zrow(zcol, col[e0 + q], zst));
