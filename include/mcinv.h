@@ -269,6 +269,17 @@ mcinv_status mcinv_debug_levels(mcinv_dtype dtype, int64_t n, const int64_t *row
                                 const void *values, const int64_t *q_row_ptr, const int32_t *q_col_idx,
                                 const void *q_values, unsigned outputs, int32_t *level, int64_t *info,
                                 int slot_R, int slot_L, int32_t *slots, int64_t slots_capacity);
+/* Host-only (no GPU needed): the dataflow kernels' warp-group schedule as staged in
+ * their TMA plan blocks, for R rows per group, W warps per CTA, entries padded to
+ * pad_ku (0: default), block entry cap ecap (0: default), with the v6 wait masks
+ * (wmask != 0) -- DESIGN.md §3. slot_x[t] = the row at slot t, -1 for padding, -2 - i
+ * for the trace item of row i (TRACE in outputs); masks[t] = bit e set when the row
+ * waits on its lower-neighbour entry e (< 32). *nslots receives the slot count
+ * (E_BUFFER if above capacity). For CPU tests of the schedule and the masks. */
+mcinv_status mcinv_debug_blocks(mcinv_dtype dtype, int64_t n, const int64_t *row_ptr, const int32_t *col_idx,
+                                const void *values, const int64_t *q_row_ptr, const int32_t *q_col_idx,
+                                const void *q_values, unsigned outputs, int R, int W, int pad_ku, int ecap, int wmask,
+                                int32_t *slot_x, uint32_t *masks, int64_t capacity, int64_t *nslots);
 /* Copy the state of chains [chain_begin, chain_begin+chains) (relative to the
  * last run's chain_begin) to host arrays z, w of shape [chains][n] (x2 doubles
  * for C128). Only those chains are copied (one strided copy). Synchronizes. */

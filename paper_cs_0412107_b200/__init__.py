@@ -91,6 +91,9 @@ SYMBOLS = {
     "mcinv_debug_levels": (ctypes.c_int, [ctypes.c_int, ctypes.c_int64] + [ctypes.c_void_p] * 6 +
                            [ctypes.c_uint, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
                             ctypes.c_void_p, ctypes.c_int64]),
+    "mcinv_debug_blocks": (ctypes.c_int, [ctypes.c_int, ctypes.c_int64] + [ctypes.c_void_p] * 6 +
+                           [ctypes.c_uint, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                            ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.POINTER(ctypes.c_int64)]),
     "mcinv_debug_get_state": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p,
                                              ctypes.c_void_p]),
     "mcinv_debug_set_state": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p,
@@ -174,6 +177,34 @@ def debug_levels(csr, outputs=("diag",), q=None, slot_R: int = 0, slot_L: int = 
     if slots is not None:
         d["slots"] = slots[:d["nslots"]].copy()
     return lev, d
+
+
+def debug_blocks(csr, outputs=("diag",), q=None, R: int = 8, W: int = 16, pad_ku: int = 0, ecap: int = 0,
+                 wmask: bool = True):
+    """Host-only dataflow schedule as staged in the TMA plan blocks (no GPU): (slot
+    rows, wait masks); rows -1 = padding, -2 - i = trace item of row i."""
+    cplx = np.iscomplexobj(csr.val)
+    rp = np.ascontiguousarray(csr.row_ptr, np.int64)
+    col = np.ascontiguousarray(csr.col, np.int32)
+    val = _doubles(csr.val, cplx)
+    args = [C128 if cplx else F64, csr.n, rp.ctypes.data, col.ctypes.data, val.ctypes.data]
+    keep = [rp, col, val]
+    if q is not None:
+        qa = [np.ascontiguousarray(q.row_ptr, np.int64), np.ascontiguousarray(q.col, np.int32), _doubles(q.val, cplx)]
+        keep += qa
+        args += [a.ctypes.data for a in qa]
+    else:
+        args += [None, None, None]
+    bits = 0
+    for o in outputs:
+        bits |= OUTPUTS[o]
+    cap = (csr.n + (csr.n if q is not None else 0)) * R + 64
+    x = np.zeros(cap, np.int32)
+    m = np.zeros(cap, np.uint32)
+    ns = ctypes.c_int64()
+    _check(load().mcinv_debug_blocks(*args, bits, R, W, pad_ku, ecap, int(wmask), x.ctypes.data, m.ctypes.data, cap,
+                                     ctypes.byref(ns)))
+    return x[:ns.value].copy(), m[:ns.value].copy()
 
 
 class Inverter:

@@ -75,6 +75,8 @@ struct LevelDev {
         // pattern slots), staged into shared memory by a TMA bulk copy
         DevBuf blob, gofs;
         int maxb = 0;
+        std::vector<int> h_x;           // host-only contexts (mcinv_debug_blocks): rec.x per slot
+        std::vector<unsigned> h_mask;   // ... and its wait mask (v6 blocks)
     };
     // (rows per warp group R, warps W, TMA blocks, entry padding, block entry cap) -> slot arrays
     std::map<std::tuple<int, int, int, int, int>, std::unique_ptr<Slots>> slots;
@@ -882,7 +884,12 @@ LevelDev::Slots *get_slots(mcinv_ctx *ctx, LevelDev *lv, int R, int W, bool bloc
                 reinterpret_cast<int4 *>(b + 16)[r] = make_int4(q.x, e, q.x != -1 ? q.z : 0, q.w);
                 reinterpret_cast<S *>(b + 16 + 16 * R)[2 * r] = dsg[2 * (g * R + r)];
                 reinterpret_cast<S *>(b + 16 + 16 * R)[2 * r + 1] = dsg[2 * (g * R + r) + 1];
-                if (wmask) reinterpret_cast<unsigned *>(b + off_wm)[r] = q.x >= 0 ? wait_mask(q) : 0u;
+                const unsigned wm_r = (wmask && q.x >= 0) ? wait_mask(q) : 0u;
+                if (wmask) reinterpret_cast<unsigned *>(b + off_wm)[r] = wm_r;
+                if (ctx->host_only) {
+                    sl->h_x.push_back(q.x);
+                    sl->h_mask.push_back(wm_r);
+                }
                 for (int t = 0; t < cnt; ++t) {
                     reinterpret_cast<int *>(b + off_col)[e + t] = xcol[q.y + t];
                     reinterpret_cast<ZW<S> *>(b + off_ab)[e + t] = hab[q.y + t];
@@ -1732,6 +1739,39 @@ mcinv_status mcinv_debug_levels(mcinv_dtype dtype, int64_t n, const int64_t *row
     info[4] = (int64_t)P.tq_row.size();
     info[5] = (int64_t)P.ent_col.size() - 8;  // without the kernel padding
     if (level) std::copy(P.level.begin(), P.level.end(), level);
+    return MCINV_OK;
+}
+
+mcinv_status mcinv_debug_blocks(mcinv_dtype dtype, int64_t n, const int64_t *row_ptr, const int32_t *col_idx,
+                                const void *values, const int64_t *q_row_ptr, const int32_t *q_col_idx,
+                                const void *q_values, unsigned outputs, int R, int W, int pad_ku, int ecap, int wmask,
+                                int32_t *slot_x, uint32_t *masks, int64_t capacity, int64_t *nslots) {
+    if (!nslots || R < 1 || 32 % R || W < 1) return MCINV_E_INVALID;
+    mcinv_ctx c;
+    mcinv_ctx *ctx = &c;
+    ctx->host_only = true;
+    ctx->dtype = dtype;
+    ctx->n = n;
+    if (dtype != MCINV_F64 && dtype != MCINV_C128) return MCINV_E_INVALID;
+    if (n < 1 || n >= (int64_t(1) << 31)) return MCINV_E_INVALID;
+    std::vector<std::vector<Entry>> rows;
+    TRY(read_csr(ctx, n, row_ptr, col_idx, (const double *)values, dtype == MCINV_C128, rows));
+    TRY(dtype == MCINV_C128 ? build_matrix<cd>(ctx, rows) : build_matrix<double>(ctx, rows));
+    TRY(default_pattern(ctx));
+    if (q_row_ptr) {
+        std::vector<std::vector<Entry>> qrows;
+        TRY(read_csr(ctx, n, q_row_ptr, q_col_idx, (const double *)q_values, dtype == MCINV_C128, qrows));
+        TRY(dtype == MCINV_C128 ? build_q<cd>(ctx, qrows) : build_q<double>(ctx, qrows));
+    }
+    LevelDev *lv = dtype == MCINV_C128 ? get_levels<cd>(ctx, outputs) : get_levels<double>(ctx, outputs);
+    if (!lv->error.empty()) return fail(ctx, MCINV_E_INVALID, lv->error);
+    LevelDev::Slots *sl = dtype == MCINV_C128 ? get_slots<cd>(ctx, lv, R, W, true, pad_ku, ecap, wmask != 0)
+                                               : get_slots<double>(ctx, lv, R, W, true, pad_ku, ecap, wmask != 0);
+    if (!sl) return fail(ctx, MCINV_E_INVALID, "slot schedule");
+    *nslots = (int64_t)sl->h_x.size();
+    if (*nslots > capacity) return fail(ctx, MCINV_E_BUFFER, "slots", *nslots);
+    if (slot_x) std::copy(sl->h_x.begin(), sl->h_x.end(), slot_x);
+    if (masks) std::copy(sl->h_mask.begin(), sl->h_mask.end(), masks);
     return MCINV_OK;
 }
 

@@ -162,3 +162,70 @@ def test_arrow_row_with_many_lower_neighbours(mc):
     placed = slots[slots >= 0]
     assert np.array_equal(np.sort(placed), np.arange(n))
     assert np.nonzero(slots == n - 1)[0][0] // 4 > np.max(np.nonzero((slots >= 0) & (slots < n - 1))[0]) // 4
+
+
+def _lower_lists(c):
+    nb = neighbours(c)
+    return [sorted(j for j in nb[i] if j < i) for i in range(c.n)]
+
+
+@pytest.mark.parametrize("make,R,W", [
+    (lambda: W.pedigree(600, seed=13), 8, 16),      # v6 on config 2's recipe (C = 8)
+    (lambda: W.pedigree(900, seed=17), 4, 8),
+    (lambda: W.lattice(8, 2, 0.2, seed=14), 2, 24),
+    (lambda: W.dense_config1(40, seed=16), 8, 16),  # every row depends on all earlier ones
+])
+def test_v6_wait_masks_cover_every_lower_neighbour(mc, make, R, W):
+    """The dataflow kernels' correctness rests on every lower neighbour j of a
+    row i being final when i runs. v6 waits only on the
+    neighbours in the host's wait mask; the others must be implied. Replay the
+    schedule: Guar(i) = the rows certainly complete once i's waits succeed =
+    for each waited j: {j} + Guar(j) (completion is transitive through the
+    counters' release/acquire), plus the rows of the previous group of the same
+    warp and their Guar (program order). Every lower neighbour must be in it."""
+    c = make()
+    x, m = mc.debug_blocks(c, ("diag", "pattern"), R=R, W=W)
+    low = _lower_lists(c)
+    assert np.array_equal(np.sort(x[x >= 0]), np.arange(c.n))
+    guar = {}
+    last_of_warp = {}
+    ngroups = x.size // R
+    dropped = 0
+    for g in range(ngroups):
+        rows = [(int(x[g * R + r]), int(m[g * R + r])) for r in range(R) if x[g * R + r] >= 0]
+        prev = last_of_warp.get(g % W, [])
+        for i, mask in rows:
+            G = set()
+            for p in prev:
+                G |= {p} | guar[p]
+            for e, j in enumerate(low[i]):
+                if e >= 32 or (mask >> e) & 1:
+                    assert j in guar, f"row {i} waits on {j}, not scheduled earlier"
+                    G |= {j} | guar[j]
+            for e, j in enumerate(low[i]):
+                assert j in G, f"row {i}: lower neighbour {j} neither waited for nor implied"
+                if e < 32 and not (mask >> e) & 1:
+                    dropped += 1
+            guar[i] = G
+        last_of_warp[g % W] = [i for i, _ in rows]
+    assert len(guar) == c.n
+    if R == 8 and c.n == 600:
+        assert dropped > 0  # the pedigree's linked parents: one wait per row implied
+
+
+def test_v5_trace_items_are_scheduled_after_their_rows(mc):
+    """v5's trace items (conj(w_i) sum_j Q_ij z_j) enter the schedule after
+    rows i and j of Q's row i: every trace item's slot group is
+    later than the groups of all those rows, and every row and item appears once."""
+    c = W.lattice(4, 3, 0.15, seed=81)
+    q = W.random_q(c.n, 82, 4)
+    R = 2
+    x, _ = mc.debug_blocks(c, ("diag", "trace"), q=q, R=R, W=24, wmask=False)
+    grp = np.arange(x.size) // R
+    row_grp = {int(v): int(gg) for v, gg in zip(x, grp) if v >= 0}
+    assert sorted(row_grp) == list(range(c.n))
+    items = [(-2 - int(v), int(gg)) for v, gg in zip(x, grp) if v <= -2]
+    assert sorted(i for i, _ in items) == list(range(c.n))
+    for i, gg in items:
+        deps = {i} | set(int(j) for j in q.col[q.row_ptr[i]:q.row_ptr[i + 1]])
+        assert all(row_grp[j] < gg for j in deps), i
