@@ -15,7 +15,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libmcinv.so")
-SOURCES = ["mcinv_host.cu", "levels.cu", "sweep.cu", "sweep3.cu", "sweep5.cu", "sweep6.cu", "contract.cu", "reduce.cu"]
+SOURCES = ["mcinv_host.cu", "levels.cu", "sweep.cu", "sweep3.cu", "sweep5.cu", "sweep6.cu", "contract.cu", "contract_ozaki.cu", "reduce.cu"]
 HEADERS = ["mcinv_internal.cuh", "noise.cuh", "scalar.cuh", "levels.h", "sweep_common.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

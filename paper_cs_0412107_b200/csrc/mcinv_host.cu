@@ -145,6 +145,7 @@ struct mcinv_ctx {
     char *ws = nullptr;
     cudaStream_t stream = nullptr;
     DevBuf tmp;  // staging for host-side results
+    DevBuf ozaki;  // K3 Ozaki scratch (int8 digit planes and exponents), MCINV_CONTRACT_OZAKI=1
     // instrumentation
     bool timing = false;
     int64_t launches = 0;
@@ -1191,12 +1192,32 @@ mcinv_status run_typed(mcinv_ctx *ctx, const mcinv_run_args *a, const Layout &L,
         if (total > 0) sweep(0, total, 0, a->outputs);
     } else {
         // burn-in in one launch, then T-sweep chunks each followed by the
-        // X Y^dagger contraction of its snapshots
+        // X Y^dagger contraction of its snapshots (MCINV_CONTRACT_OZAKI=1: the Ozaki scheme on
+        // the tcgen05 int8 tensor cores, contract_ozaki.cu)
+        bool ozaki = false;
+        if (const char *oz = std::getenv("MCINV_CONTRACT_OZAKI")) ozaki = std::atoi(oz) != 0;
+        if (ozaki) {
+            const size_t need = mcinv::contract_ozaki_scratch((int)n, L.T * a->group_size, ctx->dtype == MCINV_C128);
+            if (ctx->ozaki.bytes < need) {
+                ctx->ozaki.release();
+                if (dev_alloc(&ctx->ozaki.p, need) != cudaSuccess || cudaStreamSynchronize(0) != cudaSuccess) {
+                    cudaGetLastError();
+                    ctx->ozaki.p = nullptr;
+                    ozaki = false;
+                } else {
+                    ctx->ozaki.bytes = need;
+                }
+            }
+        }
         if (a->burn_in > 0) sweep(0, (int)a->burn_in, 0, a->outputs & ~(unsigned)MCINV_FULL);
         for (int s0 = (int)a->burn_in; s0 < total; s0 += L.T) {
             const int s1 = std::min(total, s0 + L.T);
             sweep(s0, s1, s0, a->outputs);
             timed(ctx, 1, st, [&] {
+                if (ozaki && launch_contract_ozaki<S>((const S *)(ws + L.snap_x), (const S *)(ws + L.snap_y),
+                                                      (double *)(ws + L.slot_full), (int)n, L.ld, (int)a->chains,
+                                                      a->group_size, s1 - s0, ctx->ozaki.p, ctx->ozaki.bytes, st))
+                    return;
                 launch_contract<S>((const S *)(ws + L.snap_x), (const S *)(ws + L.snap_y),
                                    (double *)(ws + L.slot_full), (int)n, L.ld, (int)a->chains, a->group_size,
                                    s1 - s0, st);

@@ -157,6 +157,13 @@ template <typename S>
 void launch_contract(const S *x, const S *y, double *acc, int n, int ld, int chains, int gs, int T,
                      cudaStream_t st);
 
+// K3 by the Ozaki scheme on tcgen05 int8 (contract_ozaki.cu): scratch bytes for an n x K chunk,
+// and the launch (false: not applicable, the DMMA kernel runs instead)
+size_t contract_ozaki_scratch(int n, int K, bool cplx);
+template <typename S>
+bool launch_contract_ozaki(const S *x, const S *y, double *acc, int n, int ld, int chains, int gs, int T,
+                           void *scratch, size_t scratch_bytes, cudaStream_t st);
+
 // slot layout [G * k][comps]: group g is the sum of sub-slots g*k .. g*k+k-1
 // s1 = sum of the group sums, m2 = their scatter about the mean of these groups (center ==
 // nullptr) or about center[c] / center_G (the global mean after an all-reduce; s1 untouched)

@@ -686,3 +686,21 @@ def test_config2_level3_chain_subset(mc, orc):
     res = compare_run(mc, orc, c, seed=run.seed, chains=s, burn_in=run.burn_in, cycles=run.cycles,
                       outputs=("diag", "pattern"), group_size=8)
     assert np.all(np.isfinite(res["diag"][0]))
+
+
+@pytest.mark.parametrize("cplx", [True, False])
+def test_contraction_ozaki_tcgen05(mc, orc, monkeypatch, cplx):
+    """K3 by the Ozaki scheme on the tcgen05 INT8 tensor cores (MCINV_CONTRACT_OZAKI=1:
+    exact int8 digit products accumulated in TMEM, fp64 recombination): full C^-1
+    estimates and states vs the oracle within the fp64 tolerances, ragged tiles (n not a
+    multiple of 128/64), several chunks (ragged last), group sizes 16 and 32."""
+    monkeypatch.setenv("MCINV_CONTRACT_OZAKI", "1")
+    if cplx:
+        c = W.lattice(5, 3, 0.15, seed=31)  # n = 125
+        compare_run(mc, orc, c, seed=9, chains=64, burn_in=2, cycles=5, outputs=("full", "diag"), group_size=16,
+                    snapshot_sweeps=3)
+        compare_run(mc, orc, W.lattice(12, 2, 0.2, seed=33), seed=10, chains=64, burn_in=2, cycles=4, outputs=("full",),
+                    group_size=32, snapshot_sweeps=2)
+    else:
+        compare_run(mc, orc, W.pedigree(150, seed=32), seed=11, chains=64, burn_in=1, cycles=6, outputs=("full",),
+                    group_size=16, snapshot_sweeps=4)
