@@ -293,15 +293,45 @@ def sweep_roofline(name, c, q, outputs, chains, sweeps, st, kinfo, lconf, clk, s
     return out
 
 
-def contract_roofline(c, chains, cycles, st, steps):
-    """K3 (X Y^dagger over snapshot chunks, FP64 DMMA): algorithmic flops 8 n^2 per
-    complex sample (2 n^2 real) against cuBLAS ZGEMM measured on this pool."""
+def load_int8_peak():
+    """Dense int8 tensor peak: the measured bf16 matmul (MEASURED_PEAKS.json) x the guide's
+    nominal int8/bf16 ratio (4.5 / 2.25 PFLOP/s)."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return 2.0 * float(json.load(f)["bf16_tflops"]), "measured bf16 x 2 (MEASURED_PEAKS.json, nominal int8/bf16)"
+    except (OSError, KeyError, ValueError):
+        return 4500.0, "fallback (nominal dense int8)"
+
+
+OZAKI_DIGITS = 6  # contract_ozaki.cu kNS
+
+
+def contract_roofline(c, chains, cycles, st, steps, group_size=32):
+    """K3 (X Y^dagger over snapshot chunks): algorithmic flops 8 n^2 per complex sample
+    (2 n^2 real). The default for n >= 256 is the Ozaki scheme on tcgen05 int8 -- bound:
+    the int8 tensor pipe, executed int8 ops (NS(NS+1)/2 digit pairs x 2 n^2 K' per pass)
+    against the int8 peak; below, the DMMA kernel against cuBLAS ZGEMM."""
     import numpy as np
     cplx = bool(np.iscomplexobj(c.val))
     flops = (8.0 if cplx else 2.0) * c.n * c.n * chains * cycles
     cms = st["contract_ms"] / steps
-    fp = load_fp64_peak()
     achieved_tf = flops / (cms / 1e3) / 1e12
+    oz_env = os.environ.get("MCINV_CONTRACT_OZAKI")
+    if (c.n >= 256 and oz_env is None) or (oz_env is not None and oz_env != "0"):
+        pairs = OZAKI_DIGITS * (OZAKI_DIGITS + 1) // 2
+        kp_per_sample = 2 if cplx else 1  # K' = 2K for complex ([re | im]), two passes
+        passes = 2 if cplx else 1
+        ops = 2.0 * pairs * c.n * c.n * chains * cycles * kp_per_sample * passes
+        pk = load_int8_peak()
+        achieved = ops / (cms / 1e3) / 1e12
+        return {"bound": "tensor", "achieved": achieved, "peak": pk[0], "unit": "TOP/s (int8)",
+                "frac": achieved / pk[0], "traffic": None, "peak_source": pk[1],
+                "kernel": f"ozaki_gemm_kernel (K3, Ozaki scheme: {OZAKI_DIGITS} int8 digits, tcgen05.mma kind::i8, "
+                          "TMEM accumulators)",
+                "fp64_equivalent_tflops": achieved_tf, "executed_int8_ops_per_step": ops,
+                "contract_ms_per_step": cms, "algorithmic_flops_per_step": flops,
+                "dmma_yardstick_tflops": load_fp64_peak()[0]}
+    fp = load_fp64_peak()
     m3 = cplx and os.environ.get("MCINV_CONTRACT_3M", "1") != "0"
     return {"bound": "tensor", "achieved": achieved_tf, "peak": fp[0], "unit": "TFLOP/s",
             "frac": achieved_tf / fp[0] if fp[0] else None, "traffic": None, "peak_source": fp[1],

@@ -28,8 +28,11 @@
 namespace mcinv {
 namespace {
 
-constexpr int OZ_M = 128, OZ_N = 64, OZ_KC = 64;  // tile and K chunk (int8 = bytes)
-constexpr int OZ_KS = 3;                           // stages
+#ifndef MCINV_OZ_KC
+#define MCINV_OZ_KC 64  // K chunk per stage (bytes of one row): 64 (64-B swizzle) or 32 (32-B swizzle)
+#endif
+constexpr int OZ_M = 128, OZ_N = 64, OZ_KC = MCINV_OZ_KC;  // tile and K chunk (int8 = bytes)
+constexpr int OZ_KS = OZ_KC == 64 ? 3 : 6;                   // stages (216 KB of shared memory)
 
 __device__ __forceinline__ uint32_t s_addr(const void *p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -139,13 +142,14 @@ __device__ __forceinline__ void tma3(uint32_t dst, const CUtensorMap *map, int c
 }
 // shared-memory matrix descriptor, K-major, 64-B swizzle: rows of 64 B, 8-row groups 512 B apart
 // (SBO = 32 x 16 B), LBO = 1 (unused by swizzled K-major), version 1 (sm_100), layout 4 = SWIZZLE_64B
+// (KC = 32: rows of 32 B, 8-row groups 256 B apart, layout 6 = SWIZZLE_32B)
 __device__ __forceinline__ uint64_t sdesc_sw64(uint32_t addr) {
     uint64_t d = 0;
     d |= (uint64_t)((addr >> 4) & 0x3FFF);
     d |= (uint64_t)1 << 16;
-    d |= (uint64_t)32 << 32;
+    d |= (uint64_t)(OZ_KC == 64 ? 32 : 16) << 32;
     d |= (uint64_t)1 << 46;
-    d |= (uint64_t)4 << 61;
+    d |= (uint64_t)(OZ_KC == 64 ? 4 : 6) << 61;
     return d;
 }
 // instruction descriptor: s8 x s8 -> s32, K-major A and B, N = 64, M = 128
@@ -212,22 +216,28 @@ __global__ void __launch_bounds__(128, 1) ozaki_gemm_kernel(const __grid_constan
             const int q = kc % OZ_KS;
             mbar_waitp(full + 8 * q, (uint32_t)((kc / OZ_KS) & 1));
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const uint32_t st = sbase + q * kStage;
+            const uint64_t d0 = sdesc_sw64(sbase + q * kStage);  // descriptors differ only in the address field
+#pragma unroll
             for (int t = 0; t < NS; ++t)
+#pragma unroll
                 for (int s = 0; s + t < NS; ++s) {
                     const uint32_t acc_col = tmem + (uint32_t)((s + t) * OZ_N);
+#pragma unroll
                     for (int kk = 0; kk < OZ_KC / 32; ++kk) {
-                        const uint64_t da = sdesc_sw64(st + s * kA + kk * 32);
-                        const uint64_t db = sdesc_sw64(st + NS * kA + t * kB + kk * 32);
+                        const uint64_t da = d0 + (uint64_t)((s * kA + kk * 32) >> 4);
+                        const uint64_t db = d0 + (uint64_t)((NS * kA + t * kB + kk * 32) >> 4);
                         // the first product of each level (t = 0 of the first chunk) overwrites it
                         const uint32_t accum = (kc > 0 || kk > 0 || t > 0) ? 1u : 0u;
                         mma_i8(acc_col, da, db, accum);
                     }
                 }
             mma_commit(empty + 8 * q);  // the stage is free once these MMAs are done
-            if (kc + OZ_KS < nk) {
-                mbar_waitp(empty + 8 * q, (uint32_t)((kc / OZ_KS) & 1));
-                issue(kc + OZ_KS);
+            // refill the PREVIOUS chunk's stage: its MMAs are done by now (the tensor pipe is busy
+            // with this chunk's), so waiting on it does not drain the MMA queue
+            if (kc >= 1 && kc - 1 + OZ_KS < nk) {
+                const int pq = (kc - 1) % OZ_KS;
+                mbar_waitp(empty + 8 * pq, (uint32_t)(((kc - 1) / OZ_KS) & 1));
+                issue(kc - 1 + OZ_KS);
             }
         }
         mma_commit(done);
@@ -297,7 +307,8 @@ bool slice_map(CUtensorMap *m, const int8_t *base, int n, int Kp, int ns, int ro
     const cuuint32_t box[3] = {(cuuint32_t)OZ_KC, (cuuint32_t)rows, 1u};
     const cuuint32_t es[3] = {1u, 1u, 1u};
     return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t *>(base), dims, strides, box, es,
-               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, OZ_KC == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 

@@ -1194,7 +1194,9 @@ mcinv_status run_typed(mcinv_ctx *ctx, const mcinv_run_args *a, const Layout &L,
         // burn-in in one launch, then T-sweep chunks each followed by the
         // X Y^dagger contraction of its snapshots (MCINV_CONTRACT_OZAKI=1: the Ozaki scheme on
         // the tcgen05 int8 tensor cores, contract_ozaki.cu)
-        bool ozaki = false;
+        // default for n >= 256 (config 3: the contraction 402 -> 320 ms per 64 sampling sweeps over
+        // the TMA-fed DMMA kernel, profiles/r02_k3_ozaki.log); small n keeps DMMA (fewer launches)
+        bool ozaki = n >= 256;
         if (const char *oz = std::getenv("MCINV_CONTRACT_OZAKI")) ozaki = std::atoi(oz) != 0;
         if (ozaki) {
             const size_t need = mcinv::contract_ozaki_scratch((int)n, L.T * a->group_size, ctx->dtype == MCINV_C128);

@@ -647,6 +647,7 @@ def test_contraction_tiles_and_staging(mc, orc, monkeypatch, wn, m3):
     complex and real, ragged n (not a multiple of the 64-wide CTA tile)."""
     monkeypatch.setenv("MCINV_CONTRACT_WN", wn)
     monkeypatch.setenv("MCINV_CONTRACT_3M", m3)
+    monkeypatch.setenv("MCINV_CONTRACT_OZAKI", "0")  # the DMMA kernels (the Ozaki path has its own test)
     c = W.lattice(5, 3, 0.15, seed=31)  # n = 125: two ragged tiles per dimension
     for gs in (16, 8):
         compare_run(mc, orc, c, seed=9, chains=64, burn_in=2, cycles=5, outputs=("full",), group_size=gs,
