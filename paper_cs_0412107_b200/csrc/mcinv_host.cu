@@ -536,12 +536,13 @@ Layout make_layout(const mcinv_ctx *ctx, const mcinv_run_args *a) {
     if (a->outputs & MCINV_FULL) {
         int T = a->snapshot_sweeps;
         if (T <= 0) {
-            // K = T * gs >= 1024 per contraction (the A_g tiles are read and written once per
-            // launch), at most 64 sweeps and 16 GB of snapshots, bounded by cycles
-            T = (int)std::max<int64_t>(1, 1024 / a->group_size);
+            // K = T * gs >= 2048 per contraction (the A_g tiles are read and written once per
+            // launch: the epilogue's share falls with K), at most 64 sweeps and 32 GB of
+            // snapshots, bounded by cycles (T = 128 on config 3: contraction -3%, twice the memory)
+            T = (int)std::max<int64_t>(1, 2048 / a->group_size);
             if (T > 64) T = 64;
             const int64_t per = 2 * n * (int64_t)L.ld * (int64_t)sz;
-            while (T > 1 && T * per > (int64_t(16) << 30)) T /= 2;
+            while (T > 1 && T * per > (int64_t(32) << 30)) T /= 2;
         }
         if (a->cycles > 0 && T > a->cycles) T = (int)a->cycles;
         L.T = std::max(T, 1);
@@ -1199,7 +1200,8 @@ mcinv_status run_typed(mcinv_ctx *ctx, const mcinv_run_args *a, const Layout &L,
         bool ozaki = n >= 256;
         if (const char *oz = std::getenv("MCINV_CONTRACT_OZAKI")) ozaki = std::atoi(oz) != 0;
         if (ozaki) {
-            const size_t need = mcinv::contract_ozaki_scratch((int)n, L.T * a->group_size, ctx->dtype == MCINV_C128);
+            const size_t need = mcinv::contract_ozaki_scratch((int)n, L.T * a->group_size, ctx->dtype == MCINV_C128,
+                                                                (int)(a->chains / a->group_size));
             if (ctx->ozaki.bytes < need) {
                 ctx->ozaki.release();
                 if (dev_alloc(&ctx->ozaki.p, need) != cudaSuccess || cudaStreamSynchronize(0) != cudaSuccess) {

@@ -159,7 +159,7 @@ void launch_contract(const S *x, const S *y, double *acc, int n, int ld, int cha
 
 // K3 by the Ozaki scheme on tcgen05 int8 (contract_ozaki.cu): scratch bytes for an n x K chunk,
 // and the launch (false: not applicable, the DMMA kernel runs instead)
-size_t contract_ozaki_scratch(int n, int K, bool cplx);
+size_t contract_ozaki_scratch(int n, int K, bool cplx, int groups);
 template <typename S>
 bool launch_contract_ozaki(const S *x, const S *y, double *acc, int n, int ld, int chains, int gs, int T,
                            void *scratch, size_t scratch_bytes, cudaStream_t st);
