@@ -484,16 +484,19 @@ def test_dirac_parity(mc, orc):
 
 
 @pytest.mark.slow
-def test_dirac18_trace_matches_paper(mc):
-    """The paper's Dirac case 1 (Tables 3/4: N = 18, K = 0.1, n = 419,904,
-    Q = I): the GPU estimate of tr(L^-1) agrees with the exact value
-    (closed form 413007.825; the paper prints 413007.84) within 4
-    standard errors (scalar rule, reading R14)."""
-    c = W.dirac(18)
+@pytest.mark.parametrize("N,printed", [(18, 413007.84), (20, 629489.14)])
+def test_dirac_trace_matches_paper(mc, N, printed):
+    """The paper's Dirac cases (K = 0.1, Q = I): Tables 3/4, N = 18 (n = 419,904;
+    exact value printed 413007.84, P:909) and Table 5, N = 20 (n = 640,000;
+    printed 629489.14). The GPU estimate of tr(L^-1) agrees with the
+    exact value (the closed form, itself pinned to the printed values in
+    tests/test_dirac.py) within 4 standard errors (scalar rule, reading R14)."""
+    c = W.dirac(N)
+    exact = W.dirac_trace_closed(N)
+    assert abs(exact - printed) < 0.02
     inv = mc.Inverter(c, q=W.identity_q(c.n))
-    inv.run(0x5EED0012, 2048, 30, 200, ("trace",), group_size=32)
+    inv.run(0x5EED0012 + (N - 18), 2048, 30, 200, ("trace",), group_size=32)
     est, se = inv.result("trace")
-    exact = W.dirac_trace_closed(18)
     r = (est.real - exact) / se.real
     assert abs(r) < 4, (est, se, exact)
     assert abs(est.imag) < 4 * se.imag + 1e-9
