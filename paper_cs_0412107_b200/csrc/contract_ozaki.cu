@@ -320,20 +320,87 @@ __device__ __forceinline__ void mma_commit(uint32_t bar) {
 }
 
 // ---------------------------------------------------------------- GEMM + epilogue
-// out: A_g (fp64, e doubles per element, stride e): out[(i n + j) e + part] += sum_L 2^(ei + fj - 7(L+2)) D_L[i][j]
-template <int NS, bool BULK>
+// 16 columns (block q) of the tile's value sum_L 2^(x - 7(L+2)) D_L, x = e_i + f_j, for this
+// thread's TMEM lane: levels 0-2 and 3-5 combine exactly in int64 (hi = (D0 2^7 + D1) 2^7 + D2 <
+// 2^46, lo likewise), so each element is fma(lo, 2^(x-49), hi 2^(x-28)): one rounding.
+template <int NS>
+__device__ __forceinline__ void level_values16(uint32_t lane_addr, int q, int ei, const int *eys, double (&v)[16]) {
+    static_assert(NS == 6, "the epilogue groups the levels 3 + 3");
+    uint32_t d[NS][16];
+#pragma unroll
+    for (int L = 0; L < NS; ++L)
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+            : "=r"(d[L][0]), "=r"(d[L][1]), "=r"(d[L][2]), "=r"(d[L][3]), "=r"(d[L][4]), "=r"(d[L][5]),
+              "=r"(d[L][6]), "=r"(d[L][7]), "=r"(d[L][8]), "=r"(d[L][9]), "=r"(d[L][10]), "=r"(d[L][11]),
+              "=r"(d[L][12]), "=r"(d[L][13]), "=r"(d[L][14]), "=r"(d[L][15])
+            : "r"(lane_addr + (uint32_t)(L * OZ_N + q * 16)));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int c = 0; c < 16; ++c) {
+        long long hi = 0, lo = 0;
+#pragma unroll
+        for (int L = 0; L < 3; ++L) {
+            hi = hi * 128 + static_cast<int32_t>(d[L][c]);
+            lo = lo * 128 + static_cast<int32_t>(d[L + 3][c]);
+        }
+        const int x = ei + eys[q * 16 + c];
+        if (x > -960 && x < 1000)  // 2^(x-28) and 2^(x-49) are normal doubles
+            v[c] = fma(static_cast<double>(lo), __longlong_as_double((long long)(x - 49 + 1023) << 52),
+                       static_cast<double>(hi) * __longlong_as_double((long long)(x - 28 + 1023) << 52));
+        else
+            v[c] = ldexp(fma(static_cast<double>(lo), 0x1p-21, static_cast<double>(hi)), x - 28);
+    }
+}
+
+// TMEM columns 384..511 (free: the NS = 6 levels use 0..383) hold the real part of a complex tile
+// as fp64 (two 32-bit columns per element) while the imaginary part's MMAs reuse the accumulators
+constexpr int kReCol = 6 * 64;
+__device__ __forceinline__ void tmem_st32(uint32_t addr, const uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+        "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(addr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+        "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
+        "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
+        "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+        : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t addr, uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,"
+        "%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+          "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+          "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+          "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(addr));
+}
+
+// out: A_g (fp64, e doubles per element): out[(i n + j) e + part] += sum_L 2^(ei + fj - 7(L+2)) D_L[i][j].
+// FUSED (complex, tiled digits): phase 0 contracts A = [Xr | Xi] (real part), phase 1 A2 = [Xi | -Xr]
+// (imaginary part) against the same B in one CTA: the real tile is parked in TMEM between them, and
+// one epilogue adds whole complex elements (16-byte accesses) into A_g.
+template <int NS, bool BULK, bool FUSED>
 __global__ void __launch_bounds__(256, 1) ozaki_gemm_kernel(const __grid_constant__ CUtensorMap ma,
                                                             const __grid_constant__ CUtensorMap mb,
-                                                            const int8_t *__restrict__ ga, const int8_t *__restrict__ gb,
+                                                            const int8_t *__restrict__ ga, const int8_t *__restrict__ ga2,
+                                                            const int8_t *__restrict__ gb,
                                                             const int *__restrict__ ex, const int *__restrict__ ey,
                                                             double *__restrict__ out, int n, int e, int part, int Kp) {
+    static_assert(!FUSED || BULK, "the fused complex kernel reads the tiled digits");
+    constexpr int PH = FUSED ? 2 : 1;
     constexpr uint32_t kA = OZ_M * OZ_KC, kB = OZ_N * OZ_KC;  // bytes of one slice tile
     constexpr uint32_t kStage = NS * (kA + kB);
     extern __shared__ __align__(128) unsigned char smo[];
     unsigned char *base = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smo) + 1023) & ~uintptr_t(1023));
     const uint32_t sbase = s_addr(base);
+    // after the ring: full[KS], empty[KS], done, re_full (phase 0 accumulated), re_free (real part
+    // parked, accumulators free), the TMEM address, f_j of the tile's columns
     const uint32_t full = sbase + OZ_KS * kStage, empty = full + 8 * OZ_KS, done = empty + 8 * OZ_KS;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(base + OZ_KS * kStage + 16 * OZ_KS + 8);
+    const uint32_t re_full = done + 8, re_free = done + 16;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(base + OZ_KS * kStage + 16 * OZ_KS + 24);
+    int *eys = reinterpret_cast<int *>(base + OZ_KS * kStage + 16 * OZ_KS + 32);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #ifdef MCINV_OZ_PROF
     long long ph_[8] = {0, 0, 0, 0, 0, 0, 0, 0}, prof_[4] = {0, 0, 0, 0};
@@ -347,29 +414,36 @@ __global__ void __launch_bounds__(256, 1) ozaki_gemm_kernel(const __grid_constan
             mbar_init1(empty + 8 * q);
         }
         mbar_init1(done);
+        mbar_init1(re_full);
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 4;" ::"r"(re_free) : "memory");  // one arrival per warp
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (warp == 0) {  // 512 TMEM columns: NS accumulators of N = 64 int32 columns
+    if (warp == 0) {  // 512 TMEM columns: NS accumulators of N = 64 int32 columns (+ the parked real part)
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(s_addr(tmem_slot))
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
+    if (threadIdx.x < OZ_N) eys[threadIdx.x] = j0 + (int)threadIdx.x < n ? ey[j0 + threadIdx.x] : 0;
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = *reinterpret_cast<volatile uint32_t *>(tmem_slot);
+    const int lq = warp & 3, ch = warp >> 2;  // TMEM lane quarter (warp % 4 by hardware), column half
+    const int r = lq * 32 + lane, i = i0 + r;
+    const uint32_t lane_addr = tmem + ((uint32_t)(lq * 32) << 16);
+    const int ei = i < n ? ex[i] : 0;
 
     // warp specialisation: warp 1 lane 0 streams the stages (producer), warp 0 lane 0 issues the
-    // MMAs; all eight warps run the epilogue
+    // MMAs; warps 4-7 park the real part (FUSED); all eight warps run the final epilogue
     if (warp == 1 && lane == 0) {
-        for (int kc = 0; kc < nk; ++kc) {
-            const int q = kc % OZ_KS;
+        for (int it = 0; it < PH * nk; ++it) {
+            const int ph = it >= nk, kc = it - ph * nk, q = it % OZ_KS;
             const uint32_t st = sbase + q * kStage;
             OZ_CLK(ta);
-            if (kc >= OZ_KS) mbar_waitp(empty + 8 * q, (uint32_t)(((kc / OZ_KS) - 1) & 1));  // chunk kc - KS done
+            if (it >= OZ_KS) mbar_waitp(empty + 8 * q, (uint32_t)(((it / OZ_KS) - 1) & 1));  // chunk it - KS done
             OZ_CLK(tb);
             mbar_expect(full + 8 * q, kStage);
             if constexpr (BULK) {  // [panel][chunk][slice][row][64]: one stage of A, one of B
-                bulk_g2s(st, ga + ((size_t)blockIdx.y * nk + kc) * (NS * kA), NS * kA, full + 8 * q);
+                bulk_g2s(st, (ph ? ga2 : ga) + ((size_t)blockIdx.y * nk + kc) * (NS * kA), NS * kA, full + 8 * q);
                 bulk_g2s(st + NS * kA, gb + ((size_t)blockIdx.x * nk + kc) * (NS * kB), NS * kB, full + 8 * q);
             } else {
                 for (int s = 0; s < NS; ++s) {
@@ -383,10 +457,14 @@ __global__ void __launch_bounds__(256, 1) ozaki_gemm_kernel(const __grid_constan
         }
     } else if (threadIdx.x == 0) {
         OZ_P(1);
-        for (int kc = 0; kc < nk; ++kc) {
-            const int q = kc % OZ_KS;
+        for (int it = 0; it < PH * nk; ++it) {
+            const int ph = it >= nk, kc = it - ph * nk, q = it % OZ_KS;
+            if (FUSED && ph == 1 && kc == 0) {  // the real part must be parked before its columns are reused
+                mbar_waitp(re_free, 0);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            }
             OZ_CLK(ta);
-            mbar_waitp(full + 8 * q, (uint32_t)((kc / OZ_KS) & 1));
+            mbar_waitp(full + 8 * q, (uint32_t)((it / OZ_KS) & 1));
             OZ_CLK(tb);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             const uint64_t d0 = sdesc_sw64(sbase + q * kStage);  // descriptors differ only in the address field
@@ -409,12 +487,32 @@ __global__ void __launch_bounds__(256, 1) ozaki_gemm_kernel(const __grid_constan
                         mma_i8(tmem + (uint32_t)((s + t0) * OZ_N), da, db, idesc_i8(m * OZ_N), accum);
                     }
             mma_commit(empty + 8 * q);  // the stage is free once these MMAs are done
+            if (FUSED && ph == 0 && kc == nk - 1) mma_commit(re_full);
             OZ_CLK(tc);
             OZ_ADD(0, ta, tb);
             OZ_ADD(1, tb, tc);
         }
         mma_commit(done);
         OZ_P(2);
+    } else if (FUSED && warp >= 4) {  // park the real part: 4 column blocks, fp64 as 2 x 32 bits
+        mbar_waitp(re_full, 0);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll 1
+        for (int q = 0; q < OZ_N / 16; ++q) {
+            double v[16];
+            level_values16<NS>(lane_addr, q, ei, eys, v);
+            uint32_t w[32];
+#pragma unroll
+            for (int c = 0; c < 16; ++c) {
+                w[2 * c] = __double2loint(v[c]);
+                w[2 * c + 1] = __double2hiint(v[c]);
+            }
+            tmem_st32(lane_addr + (uint32_t)(kReCol + 32 * q), w);
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(re_free) : "memory");
     }
 #ifdef MCINV_OZ_PROF
     if ((warp == 1 && lane == 0) || threadIdx.x == 0)
@@ -425,56 +523,60 @@ __global__ void __launch_bounds__(256, 1) ozaki_gemm_kernel(const __grid_constan
     mbar_waitp(done, 0);
     OZ_P(3);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    // epilogue: warp w reads TMEM lanes 32(w % 4).. = tile rows, columns 32(w / 4).., 16 columns of
-    // all NS levels at a time. Levels 0-2 and 3-5 combine exactly in int64 (hi = (D0 2^7 + D1) 2^7 + D2 < 2^46, lo
-    // likewise), so each element is fma(lo, 2^(x-49), hi 2^(x-28)) with x = e_i + f_j: one rounding.
-    // The scaled tile is staged in shared memory (the ring is free: every TMA was consumed and
-    // every MMA has completed) and then added into A_g: each warp takes 16 rows, their loads in
-    // flight at once.
-    static_assert(NS == 6, "the epilogue groups the levels 3 + 3");
-    const int lq = warp & 3, ch = warp >> 2;  // TMEM lane quarter (warp % 4 by hardware), column half
-    const int r = lq * 32 + lane, i = i0 + r;
-    const uint32_t lane_addr = tmem + ((uint32_t)(lq * 32) << 16);
-    constexpr int kLd = OZ_N + 1;  // odd stride in doubles: two lanes per bank pair at most
-    double *tile = reinterpret_cast<double *>(base);
-    int *eys = reinterpret_cast<int *>(tile + OZ_M * kLd);
-    if (threadIdx.x < OZ_N) eys[threadIdx.x] = j0 + (int)threadIdx.x < n ? ey[j0 + threadIdx.x] : 0;
-    const int ei = i < n ? ex[i] : 0;
-    __syncthreads();
+    // epilogue: warp w reads TMEM lanes 32(w % 4).. = tile rows, columns 32(w / 4).. (16 columns of
+    // all NS levels at a time). The scaled tile is staged in shared memory (the ring is free: every
+    // copy was consumed and every MMA has completed) and then added into A_g: each warp takes 16
+    // rows, their loads in flight at once.
     OZ_P(4);
+    if constexpr (FUSED) {
+        constexpr int kLd = OZ_N + 1;  // odd stride in 16-byte elements: conflict-free quarter-warps
+        double2 *tile = reinterpret_cast<double2 *>(base);
 #pragma unroll 1
-    for (int q = ch * (OZ_N / 32); q < (ch + 1) * (OZ_N / 32); ++q) {
-        uint32_t d[NS][16];
+        for (int q = ch * (OZ_N / 32); q < (ch + 1) * (OZ_N / 32); ++q) {
+            double im[16];
+            level_values16<NS>(lane_addr, q, ei, eys, im);
+            uint32_t w[32];
+            tmem_ld32(lane_addr + (uint32_t)(kReCol + 32 * q), w);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-        for (int L = 0; L < NS; ++L)
-            asm volatile(
-                "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-                : "=r"(d[L][0]), "=r"(d[L][1]), "=r"(d[L][2]), "=r"(d[L][3]), "=r"(d[L][4]), "=r"(d[L][5]),
-                  "=r"(d[L][6]), "=r"(d[L][7]), "=r"(d[L][8]), "=r"(d[L][9]), "=r"(d[L][10]), "=r"(d[L][11]),
-                  "=r"(d[L][12]), "=r"(d[L][13]), "=r"(d[L][14]), "=r"(d[L][15])
-                : "r"(lane_addr + (uint32_t)(L * OZ_N + q * 16)));
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-        for (int c = 0; c < 16; ++c) {
-            long long hi = 0, lo = 0;
-#pragma unroll
-            for (int L = 0; L < 3; ++L) {
-                hi = hi * 128 + static_cast<int32_t>(d[L][c]);
-                lo = lo * 128 + static_cast<int32_t>(d[L + 3][c]);
-            }
-            const int x = ei + eys[q * 16 + c];
-            double v;
-            if (x > -960 && x < 1000)  // 2^(x-28) and 2^(x-49) are normal doubles
-                v = fma(static_cast<double>(lo), __longlong_as_double((long long)(x - 49 + 1023) << 52),
-                        static_cast<double>(hi) * __longlong_as_double((long long)(x - 28 + 1023) << 52));
-            else
-                v = ldexp(fma(static_cast<double>(lo), 0x1p-21, static_cast<double>(hi)), x - 28);
-            tile[r * kLd + q * 16 + c] = v;
+            for (int c = 0; c < 16; ++c)
+                tile[r * kLd + q * 16 + c] = make_double2(__hiloint2double(w[2 * c + 1], w[2 * c]), im[c]);
         }
-    }
-    __syncthreads();
-    OZ_P(5);
-    {
+        __syncthreads();
+        OZ_P(5);
+        const int ja = j0 + lane, jb = j0 + lane + 32;
+        const bool oka = ja < n, okb = jb < n;
+#pragma unroll 1
+        for (int rb = warp * 16; rb < warp * 16 + 16; rb += 8) {
+            double2 va[8], vb[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const int ii = i0 + rb + k;
+                const double2 *row = reinterpret_cast<const double2 *>(out) + (int64_t)ii * n;
+                va[k] = (ii < n && oka) ? __ldcs(row + ja) : make_double2(0.0, 0.0);
+                vb[k] = (ii < n && okb) ? __ldcs(row + jb) : make_double2(0.0, 0.0);
+            }
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const int ii = i0 + rb + k;
+                double2 *row = reinterpret_cast<double2 *>(out) + (int64_t)ii * n;
+                const double2 ta = tile[(rb + k) * kLd + lane], tb = tile[(rb + k) * kLd + lane + 32];
+                if (ii < n && oka) __stcs(row + ja, make_double2(va[k].x + ta.x, va[k].y + ta.y));
+                if (ii < n && okb) __stcs(row + jb, make_double2(vb[k].x + tb.x, vb[k].y + tb.y));
+            }
+        }
+    } else {
+        constexpr int kLd = OZ_N + 1;  // odd stride in doubles: two lanes per bank pair at most
+        double *tile = reinterpret_cast<double *>(base);
+#pragma unroll 1
+        for (int q = ch * (OZ_N / 32); q < (ch + 1) * (OZ_N / 32); ++q) {
+            double v[16];
+            level_values16<NS>(lane_addr, q, ei, eys, v);
+#pragma unroll
+            for (int c = 0; c < 16; ++c) tile[r * kLd + q * 16 + c] = v[c];
+        }
+        __syncthreads();
+        OZ_P(5);
         const int ja = j0 + lane, jb = j0 + lane + 32;
         const bool oka = ja < n, okb = jb < n;
 #pragma unroll 1
@@ -587,8 +689,10 @@ bool launch_contract_ozaki(const S *x, const S *y, double *acc, int n, int ld, i
         if (!slice_map(&ma, A_of(0), n, Kp, kNS, OZ_M) || !slice_map(&mb, B_of(0), n, Kp, kNS, OZ_N)) return false;
         if (kC && !slice_map(&ma2, A2_of(0), n, Kp, kNS, OZ_M)) return false;
     }
-    const size_t smem = (size_t)OZ_KS * kNS * (OZ_M + OZ_N) * OZ_KC + 16 * OZ_KS + 16 + 1024;
-    auto kg = bulk ? ozaki_gemm_kernel<kNS, true> : ozaki_gemm_kernel<kNS, false>;
+    const size_t smem = (size_t)OZ_KS * kNS * (OZ_M + OZ_N) * OZ_KC + 16 * OZ_KS + 32 + OZ_N * sizeof(int) + 1024;
+    const bool fused = kC && bulk;  // complex: real and imaginary parts in one CTA
+    auto kg = fused ? ozaki_gemm_kernel<kNS, true, true>
+                    : (bulk ? ozaki_gemm_kernel<kNS, true, false> : ozaki_gemm_kernel<kNS, false, false>);
     if (cudaFuncSetAttribute(kg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return false;
     const dim3 grid((n + OZ_N - 1) / OZ_N, (n + OZ_M - 1) / OZ_M);
     const int e = kC ? 2 : 1;
@@ -608,8 +712,14 @@ bool launch_contract_ozaki(const S *x, const S *y, double *acc, int n, int ld, i
         }
         for (int b = 0; b < nb; ++b) {
             double *out = acc + (int64_t)(g0 + b) * n * n * e;
-            kg<<<grid, 256, smem, st>>>(ma, mb, A_of(b), B_of(b), ex_of(b), ey_of(b), out, n, e, 0, Kp);
-            if (kC) kg<<<grid, 256, smem, st>>>(ma2, mb, A2_of(b), B_of(b), ex_of(b), ey_of(b), out, n, e, 1, Kp);
+            if (fused) {
+                kg<<<grid, 256, smem, st>>>(ma, mb, A_of(b), A2_of(b), B_of(b), ex_of(b), ey_of(b), out, n, e, 0, Kp);
+            } else {
+                kg<<<grid, 256, smem, st>>>(ma, mb, A_of(b), nullptr, B_of(b), ex_of(b), ey_of(b), out, n, e, 0, Kp);
+                if (kC)
+                    kg<<<grid, 256, smem, st>>>(ma2, mb, A2_of(b), nullptr, B_of(b), ex_of(b), ey_of(b), out, n, e, 1,
+                                                Kp);
+            }
         }
     }
 #ifdef MCINV_OZ_PROF
