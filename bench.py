@@ -329,6 +329,8 @@ def contract_roofline(c, chains, cycles, st, steps, group_size=32):
                 "kernel": f"ozaki_gemm_kernel (K3, Ozaki scheme: {OZAKI_DIGITS} int8 digits, tcgen05.mma kind::i8, "
                           "TMEM accumulators)",
                 "fp64_equivalent_tflops": achieved_tf, "executed_int8_ops_per_step": ops,
+                "note": "contract_ms includes the digit slicing (about 9% of it); the UMMA microbenchmark "
+                        "(tools/micro/umma_bench.cu) sustains 4.76 int8 POP/s at N >= 128",
                 "contract_ms_per_step": cms, "algorithmic_flops_per_step": flops,
                 "dmma_yardstick_tflops": load_fp64_peak()[0]}
     fp = load_fp64_peak()
