@@ -708,3 +708,29 @@ def test_contraction_ozaki_tcgen05(mc, orc, monkeypatch, cplx):
     else:
         compare_run(mc, orc, W.pedigree(150, seed=32), seed=11, chains=64, burn_in=1, cycles=6, outputs=("full",),
                     group_size=16, snapshot_sweeps=4)
+
+
+@pytest.mark.parametrize("ozaki", ["1", "0"])
+@pytest.mark.parametrize("cplx", [True, False])
+def test_contraction_wide_row_scales(mc, orc, monkeypatch, cplx, ozaki):
+    """Reading R26's bound is relative to each row's and column's own scale (2^e_i, 2^f_j):
+    C' = S C S with S = diag(10^U(-4, 4)) spreads the rows of X and Y -- and the entries
+    of C'^-1 = S^-1 C^-1 S^-1 -- over 16 orders of magnitude (Gauss-Seidel is invariant
+    under the scaling: its iteration matrix is similar to C's). The unscaled estimate
+    S est S must match the oracle's within 1e-10, i.e. every element to 1e-10 of its own
+    row/column scale, for the Ozaki kernel and for the DMMA kernel."""
+    monkeypatch.setenv("MCINV_CONTRACT_OZAKI", ozaki)
+    base = W.lattice(5, 3, 0.15, seed=31) if cplx else W.pedigree(150, seed=32)
+    s = 10.0 ** np.random.default_rng(77).uniform(-4.0, 4.0, base.n)
+    rows = np.repeat(np.arange(base.n), np.diff(base.row_ptr))
+    c = W.CSR(base.n, base.row_ptr, base.col, base.val * s[rows] * s[base.col])
+    seed, chains, burn, cycles, gs = 12, 64, 2, 5, 16
+    inv = mc.Inverter(c)
+    inv.run(seed, chains, burn, cycles, ("full",), group_size=gs, snapshot_sweeps=3)
+    eg, _ = inv.result("full")
+    inv.close()
+    r = orc.Matrix(c).run(seed, chains, burn, cycles, ("full",))
+    eo, _ = orc.estimate(r["full"], cycles, group_size=gs)
+    assert np.max(np.abs(eo)) / np.min(np.abs(np.diag(eo))) > 1e10  # the spread is real
+    u = s[:, None] * s[None, :]
+    est_match(u * eg, u * eo, what="unscaled full")
