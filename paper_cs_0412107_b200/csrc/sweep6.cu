@@ -327,10 +327,15 @@ namespace {
 #ifndef MCINV_V6_KU768
 #define MCINV_V6_KU768 2
 #endif
+// gathers in flight per thread at 512 threads; config 2: KU 4 2.53e10, 5 2.61e10, 6 2.65e10,
+// 7 2.47e10, 8 2.41e10 site-updates/s (profiles/r02_v6_ku512.log)
+#ifndef MCINV_V6_KU512
+#define MCINV_V6_KU512 6
+#endif
 template <int NT, int LGC, int LGP, bool BITS>
 cudaError_t launch6b(const Sweep3Params<double> &p, int threads, cudaStream_t st) {
-    // gathers in flight: 64 registers at 1024 threads, 85 at 768, 128 at 512
-    constexpr int KU = NT > 768 ? 2 : NT > 512 ? MCINV_V6_KU768 : 4;
+    // gathers in flight: 64 registers at 1024 threads, 85 at 768, 128 at 512 (KU = 6: 128 registers, no spill)
+    constexpr int KU = NT > 768 ? 2 : NT > 512 ? MCINV_V6_KU768 : MCINV_V6_KU512;
     if (threads > NT) return cudaErrorInvalidConfiguration;
     const int blocks = (p.chains + (1 << LGC) - 1) >> LGC;
     const size_t smem = sweep6_smem(p.n, threads, p.maxb);
@@ -381,7 +386,7 @@ size_t sweep6_smem(int n, int threads, int maxb) {
     return 16 * W + 2 * W * (size_t)maxb + counters;
 }
 
-int sweep6_ku(int threads) { return threads > 768 ? 2 : threads > 512 ? MCINV_V6_KU768 : 4; }
+int sweep6_ku(int threads) { return threads > 768 ? 2 : threads > 512 ? MCINV_V6_KU768 : MCINV_V6_KU512; }
 
 cudaError_t launch_sweep6(const Sweep3Params<double> &p, int threads, cudaStream_t st) {
     switch (p.lgC) {
