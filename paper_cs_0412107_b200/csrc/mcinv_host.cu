@@ -708,7 +708,7 @@ template <typename S>
 LevelDev::Slots *get_slots(mcinv_ctx *ctx, LevelDev *lv, int R, int W, bool blocks, int pad_ku = 0, int ecap = 0,
                            bool wmask = false) {
     if (ecap <= 0) ecap = block_entries();
-    const int KU = pad_ku > 0 ? pad_ku : (sizeof(S) == sizeof(double) ? 4 : 2);
+    const int KU = pad_ku > 0 ? pad_ku : (sizeof(S) == sizeof(double) ? MCINV_V5_KUR : MCINV_V5_KUC);
     const auto key = std::make_tuple(R, W, (blocks ? 1 : 0) | (wmask ? 2 : 0), KU, ecap);
     auto it = lv->slots.find(key);
     if (it != lv->slots.end()) return it->second.get();

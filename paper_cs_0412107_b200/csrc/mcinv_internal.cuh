@@ -5,6 +5,15 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+// v5 gather unroll (entries in flight per thread): real / complex; the host pads every row's
+// block entries to a multiple of it
+#ifndef MCINV_V5_KUR
+#define MCINV_V5_KUR 4
+#endif
+#ifndef MCINV_V5_KUC
+#define MCINV_V5_KUC 2
+#endif
+
 namespace mcinv {
 
 // Complex double, interleaved (re, im) as in the ABI.

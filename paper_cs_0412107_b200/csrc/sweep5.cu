@@ -327,7 +327,7 @@ namespace {
 template <typename S, int LGC, int LGP, bool BITS>
 cudaError_t launch5b(const Sweep3Params<S> &p, int threads, cudaStream_t st) {
     constexpr bool kReal = ScalarTraits<S>::kDoubles == 1;
-    constexpr int NT = kReal ? 1024 : 768, KU = kReal ? 4 : 2;
+    constexpr int NT = kReal ? 1024 : 768, KU = kReal ? MCINV_V5_KUR : MCINV_V5_KUC;
     if (threads > NT) return cudaErrorInvalidConfiguration;
     const int blocks = (p.chains + (1 << LGC) - 1) >> LGC;
     size_t smem = sweep5_smem(p.n, threads, p.maxb);
