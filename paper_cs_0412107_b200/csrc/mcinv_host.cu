@@ -750,9 +750,10 @@ LevelDev::Slots *get_slots(mcinv_ctx *ctx, LevelDev *lv, int R, int W, bool bloc
     // slot order: the list schedule (levels.h schedule_slots) with a slack of L = W groups
     // (the warps of a CTA); MCINV_SLOT_ORDER=level keeps plain level order (each level padded)
     const char *so = std::getenv("MCINV_SLOT_ORDER");
-    // similarity window of the list schedule (levels.h): 32 measured best on config 2 (+3%)
+    // similarity window of the list schedule (levels.h): 64 measured best on config 2 (32: -2%,
+    // 0: -4%; configs 3 and 5 unchanged; profiles/r02_schedule_knobs.log)
     const char *se = std::getenv("MCINV_SIMILAR");
-    const int sim = se ? std::atoi(se) : 32;
+    const int sim = se ? std::atoi(se) : 64;
     std::vector<int> order;
     if (so && !std::strcmp(so, "level")) {
         for (int l = 0; l < lv->D; ++l) {
@@ -1752,7 +1753,7 @@ mcinv_status mcinv_debug_levels(mcinv_dtype dtype, int64_t n, const int64_t *row
             rec[o] = make_int4(i, beg, (int)((unsigned)cnt | (unsigned)nlow << 16), -1);
         }
         const char *se = std::getenv("MCINV_SIMILAR");
-        const std::vector<int> order = mcinv::schedule_slots(n, rec, P.ent_col, slot_R, slot_L, 0, se ? std::atoi(se) : 32);
+        const std::vector<int> order = mcinv::schedule_slots(n, rec, P.ent_col, slot_R, slot_L, 0, se ? std::atoi(se) : 64);
         if ((int64_t)order.size() > slots_capacity) return fail(ctx, MCINV_E_BUFFER, "slots", (int64_t)order.size());
         for (size_t t = 0; t < order.size(); ++t) info_slots[t] = order[t] < 0 ? -1 : P.ord_row[order[t]];
         info[6] = (int64_t)order.size();
