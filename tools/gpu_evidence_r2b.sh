@@ -17,6 +17,6 @@ cap() {  # tag kernel-regex run_one args...
   ncu -i /tmp/$tag.ncu-rep --page raw --csv > gpurun_out/${tag}_raw.csv 2>/dev/null
   ncu -i /tmp/$tag.ncu-rep > gpurun_out/${tag}_details.txt 2>/dev/null
 }
-cap ev_k3oz ozaki_gemm --config 3 --sweeps 66 --burn 2 --outputs full
-cap ev_k3sl ozaki_slice --config 3 --sweeps 66 --burn 2 --outputs full
+#cap ev_k3oz ozaki_gemm --config 3 --sweeps 66 --burn 2 --outputs full
+#cap ev_k3sl ozaki_slice --config 3 --sweeps 66 --burn 2 --outputs full
 du -sh gpurun_out
