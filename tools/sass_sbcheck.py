@@ -1,0 +1,66 @@
+"""Find scoreboard sharing between shared-memory loads and global loads in a kernel's SASS:
+an instruction that waits on scoreboard k where, since the last shared load (LDS) that wrote
+k, a global load (LDG) also wrote k -- the wait then lasts a global round trip although the
+consumer only needs the shared value (the v6 finding, K1). Prints each such place.
+
+    cuobjdump -sass libmcinv.so > k.sass; python tools/sass_sbcheck.py k.sass [kernel-substring]
+"""
+import re
+import sys
+
+
+def parse(lines):
+    i, out = 0, []
+    while i < len(lines) - 1:
+        m = re.match(r'\s*/\*([0-9a-f]{4,})\*/\s+(.*?);\s*/\* 0x([0-9a-f]{16}) \*/', lines[i])
+        if m:
+            m2 = re.match(r'\s*/\* 0x([0-9a-f]{16}) \*/', lines[i + 1])
+            c = int(m2.group(1), 16) >> 41
+            out.append((int(m.group(1), 16), m.group(2).strip(), (c >> 5) & 7, (c >> 11) & 0x3f))
+            i += 2
+            continue
+        i += 1
+    return out
+
+
+def main():
+    text = open(sys.argv[1]).read().split("Function : ")
+    want = sys.argv[2] if len(sys.argv) > 2 else ""
+    for blk in text[1:]:
+        name = blk.split("\n", 1)[0].strip()
+        if want not in name:
+            continue
+        ins = parse(blk.splitlines())
+        last = {}  # sb -> [(kind, dest registers)] written since the last wait on it
+        hits = 0
+
+        def regs(txt):
+            return set(int(r) for r in re.findall(r"\bR(\d+)\b", txt))
+
+        for addr, op, wb, wm in ins:
+            body = re.sub(r"^@!?U?P\d+\s+", "", op)
+            mnem = body.split()[0]
+            operands = body[len(mnem):]
+            for k in range(6):
+                if wm >> k & 1:
+                    pend = last.get(k, [])
+                    kinds = [p[0] for p in pend]
+                    if "LDS" in kinds and "LDG" in kinds[kinds.index("LDS"):]:
+                        # a false dependency when the waiting instruction reads none of the
+                        # global loads' destinations
+                        src = regs(operands.split(",", 1)[1] if "," in operands else "")
+                        gdst = set().union(*[p[1] for p in pend if p[0] == "LDG"])
+                        if not (src & gdst):
+                            hits += 1
+                            if hits <= 8:
+                                print(f"  {addr:05x} {op[:60]} waits sb{k}: shared value behind a global load")
+                    last[k] = []
+            if wb != 7:
+                kind = "LDG" if mnem.startswith("LDG") else ("LDS" if mnem.startswith("LDS") else "other")
+                dst = operands.split("desc")[0] if kind == "LDG" else operands.split(",")[0]
+                last.setdefault(wb, []).append((kind, regs(dst)))
+        print(f"{name[:90]}: {hits} shared/global scoreboard waits")
+
+
+if __name__ == "__main__":
+    main()
