@@ -1151,6 +1151,9 @@ mcinv_status run_typed(mcinv_ctx *ctx, const mcinv_run_args *a, const Layout &L,
             // 220-sweep runs: config 2 2.02 -> 2.06e10, config 3 3.00 -> 3.26e10), upper
             // neighbours only into L2 (2) or L1 (1), none (0) -- profiles/r01_prefetch.log
             q3.prefetch = 3;
+            // v6: the later gather chunks' lines with an L1 prefetch (+8: +1% on config 2,
+            // profiles/r02_v6_stage.log)
+            if (v6) q3.prefetch |= 8;
         }
         // v3 (level kernel): the same prefetch for real C (config 4: 3.82 -> 4.02e10), not for
         // complex (config 5: 1.36 -> 1.34e10)

@@ -34,7 +34,8 @@ __device__ __forceinline__ ZW2 ld_zw2(const ZW<double> *p) {
 
 // diagnostic ablations (timing only, results wrong; never in the product build):
 // bit 1 skip the dependency waits, bit 2 gather every neighbour from the row's own line,
-// bit 4 skip the sweep-end barrier, bit 8 skip the accumulation
+// bit 4 skip the sweep-end barrier, bit 8 skip the accumulation, bit 16 later chunks re-gather
+// the first entry's line (an L1 hit: the cost of a chunk without its round trip)
 #ifndef MCINV_ABL
 #define MCINV_ABL 0
 #endif
@@ -46,9 +47,6 @@ __device__ __forceinline__ ZW2 ld_zw2(const ZW<double> *p) {
 #endif
 #ifndef MCINV_V6_EARLY
 #define MCINV_V6_EARLY 1  // first chunk's gather addresses computed before the noise (0: after the waits)
-#endif
-#ifndef MCINV_V6_CHUNKS
-#define MCINV_V6_CHUNKS 1  // gather chunks of KU entries in flight at once (A/B knob)
 #endif
 #ifndef MCINV_TRACE
 #define MCINV_TRACE 0
@@ -70,46 +68,6 @@ template <int KU>
 __device__ __forceinline__ void row_sums2(const ZW<double> *zcol, const int *col, const ZW<double> *ab, int cnt,
                                           uint32_t zst, double (&az)[2], double (&aw)[2], const ZW<double> *const *a0,
                                           long long *trc = nullptr) {
-    if constexpr (MCINV_V6_CHUNKS == 2) {
-        // two chunks in flight: the second one predicated on the row having it (rows are
-        // padded to KU entries, so a chunk is all there or absent); an absent chunk gathers
-        // the first chunk's lines again (L1 hits) and skips its fma
-        for (int e0 = 0; e0 < cnt; e0 += 2 * KU) {
-            const bool two = e0 + KU < cnt;
-            int j[2 * KU];
-            ZW2 v[2 * KU];
-            ZW<double> c[2 * KU];
-#pragma unroll
-            for (int q = 0; q < KU; ++q) {
-                j[q] = col[e0 + q];
-                j[KU + q] = two ? col[e0 + KU + q] : j[q];
-            }
-#pragma unroll
-            for (int q = 0; q < 2 * KU; ++q) v[q] = ld_zw2(zrow(zcol, j[q], zst));
-#pragma unroll
-            for (int q = 0; q < KU; ++q) {
-                c[q] = ab[e0 + q];
-                c[KU + q] = two ? ab[e0 + KU + q] : ZW<double>{0.0, 0.0};
-            }
-#pragma unroll
-            for (int q = 0; q < KU; ++q)
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    az[h] = fma(c[q].z, v[q].v[h].z, az[h]);
-                    aw[h] = fma(c[q].w, v[q].v[h].w, aw[h]);
-                }
-            if (two) {
-#pragma unroll
-                for (int q = KU; q < 2 * KU; ++q)
-#pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        az[h] = fma(c[q].z, v[q].v[h].z, az[h]);
-                        aw[h] = fma(c[q].w, v[q].v[h].w, aw[h]);
-                    }
-            }
-        }
-        return;
-    }
     int first = 0;
     if (a0 && cnt > 0) {
         // the first chunk from the precomputed addresses (peeled: a shared loop body would
@@ -158,7 +116,7 @@ __device__ __forceinline__ void row_sums2(const ZW<double> *zcol, const int *col
         const ZW<double> *a[KU];
 #pragma unroll
         for (int q = 0; q < KU; ++q) {
-            a[q] = zrow(zcol, j[q], zst);
+            a[q] = ((MCINV_ABL & 16) && a0) ? a0[0] : zrow(zcol, j[q], zst);
         }
 #pragma unroll
         for (int q = 0; q < KU; ++q) {
@@ -456,7 +414,12 @@ __global__ void __launch_bounds__(NT, 1) sweep6_kernel(const Sweep3Params<double
                         if (p.prefetch >= 2) prefetch_l2(a0[q]);
                     }
                 }
-                if (p.prefetch >= 2) {
+                if (p.prefetch & 8) {
+                    // the later chunks' lines with an L1 prefetch (measured +1%, profiles/r02_v6_stage.log)
+                    for (int e0 = KU; e0 < cnt; e0 += KU)
+#pragma unroll
+                        for (int q = 0; q < KU; ++q) prefetch_l1(zrow(zcol, col[e0 + q], zst));
+                } else if (p.prefetch >= 2) {
                     for (int e0 = KU; e0 < cnt; e0 += KU)
 #pragma unroll
                         for (int q = 0; q < KU; ++q) prefetch_l2(zrow(zcol, col[e0 + q], zst));
