@@ -1,7 +1,7 @@
 """Find scoreboard sharing between shared-memory loads and global loads in a kernel's SASS:
-an instruction that waits on scoreboard k where, since the last shared load (LDS) that wrote
-k, a global load (LDG) also wrote k -- the wait then lasts a global round trip although the
-consumer only needs the shared value (the v6 finding, K1). Prints each such place.
+an instruction that waits on scoreboard k for the result of a load (shared or global) although a
+global load issued after it also holds k -- the wait then lasts that later load's round trip
+(the v6 finding: column reads behind the chunk's first gathers, K1). Prints each such place.
 
     cuobjdump -sass libmcinv.so > k.sass; python tools/sass_sbcheck.py k.sass [kernel-substring]
 """
@@ -44,16 +44,16 @@ def main():
             for k in range(6):
                 if wm >> k & 1:
                     pend = last.get(k, [])
-                    kinds = [p[0] for p in pend]
-                    if "LDS" in kinds and "LDG" in kinds[kinds.index("LDS"):]:
-                        # a false dependency when the waiting instruction reads none of the
-                        # global loads' destinations
-                        src = regs(operands.split(",", 1)[1] if "," in operands else "")
-                        gdst = set().union(*[p[1] for p in pend if p[0] == "LDG"])
-                        if not (src & gdst):
+                    src = regs(operands.split(",", 1)[1] if "," in operands else operands)
+                    need = [n for n, p in enumerate(pend) if p[1] & src]
+                    if need:
+                        # a false dependency: the value comes from an earlier load, but a global
+                        # load issued after it on the same scoreboard must return first
+                        later = [p for p in pend[need[-1] + 1:] if p[0] == "LDG"]
+                        if later:
                             hits += 1
                             if hits <= 8:
-                                print(f"  {addr:05x} {op[:60]} waits sb{k}: shared value behind a global load")
+                                print(f"  {addr:05x} {op[:60]} waits sb{k}: {pend[need[-1]][0]} value behind a later global load")
                     last[k] = []
             if wb != 7:
                 kind = "LDG" if mnem.startswith("LDG") else ("LDS" if mnem.startswith("LDS") else "other")
