@@ -80,3 +80,24 @@ def test_product_never_imports_oracle():
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt, f
                 assert "oracle.h" not in txt and "liboracle" not in txt, f
+
+
+def test_v6_gathers_do_not_wait_behind_global_loads(lib):
+    """Regression guard for the late-round-2 finding ("K1 v6, late r2"): ptxas put
+    the column reads of a gather chunk on the scoreboard of the chunk's first global loads, so
+    the fifth address waited a whole round trip. The config-2 kernel (C = 8, 512 threads) must
+    have no instruction that waits for a load's result behind a later global load on the same
+    scoreboard (tools/sass_sbcheck.py, run on the built library's SASS)."""
+    import importlib.util
+    import os
+    from paper_cs_0412107_b200 import build
+    sass = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", build.SO], capture_output=True,
+                          text=True).stdout
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    spec = importlib.util.spec_from_file_location("sbcheck", os.path.join(root, "tools", "sass_sbcheck.py"))
+    sb = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(sb)
+    blocks = [b for b in sass.split("Function : ")[1:]
+              if b.startswith("_ZN5mcinv13sweep6_kernelILi6ELi512ELi3ELi2ELb0ELb1E")]
+    assert len(blocks) == 1
+    assert sb.false_waits(blocks[0]) == []

@@ -23,6 +23,35 @@ def parse(lines):
     return out
 
 
+def false_waits(blk):
+    """(address, instruction, scoreboard, kind) of every wait in one function's SASS that
+    needs an earlier load's result while a later global load holds the same scoreboard."""
+    ins = parse(blk.splitlines())
+    out = []
+    last = {}
+
+    def regs(txt):
+        return set(int(r) for r in re.findall(r"\bR(\d+)\b", txt))
+
+    for addr, op, wb, wm in ins:
+        body = re.sub(r"^@!?U?P\d+\s+", "", op)
+        mnem = body.split()[0]
+        operands = body[len(mnem):]
+        for k in range(6):
+            if wm >> k & 1:
+                pend = last.get(k, [])
+                src = regs(operands.split(",", 1)[1] if "," in operands else operands)
+                need = [n for n, p in enumerate(pend) if p[1] & src]
+                if need and [p for p in pend[need[-1] + 1:] if p[0] == "LDG"]:
+                    out.append((addr, op, k, pend[need[-1]][0]))
+                last[k] = []
+        if wb != 7:
+            kind = "LDG" if mnem.startswith("LDG") else ("LDS" if mnem.startswith("LDS") else "other")
+            dst = operands.split("desc")[0] if kind == "LDG" else operands.split(",")[0]
+            last.setdefault(wb, []).append((kind, regs(dst)))
+    return out
+
+
 def main():
     text = open(sys.argv[1]).read().split("Function : ")
     want = sys.argv[2] if len(sys.argv) > 2 else ""
