@@ -255,8 +255,9 @@ def sweep_roofline(name, c, q, outputs, chains, sweeps, st, kinfo, lconf, clk, s
     """Roofline of the sweep kernel K1 over its launches: achieved algorithmic bytes
      per launch / launch time against the measured HBM peak, and the
     instruction-issue ceiling from the committed ncu warp instructions per
-    site. `bound` names the nearer of the two ceilings (the larger fraction); the
-    other stays in the object, with ncu's actual DRAM bandwidth at this rate."""
+    site. `bound` names the nearer of the two ceilings (the larger fraction), or the issue
+    ceiling when ncu's DRAM bandwidth at this rate is below half the peak (the kernel is then
+    latency-bound, not HBM-bound); both stay in the object, with that DRAM fraction."""
     launch_ms = st["sweep_ms"] / max(st["sweep_launches"], 1)
     per_launch_sweeps = sweeps / max(st["sweep_launches"], 1)
     sites_launch = chains * c.n * per_launch_sweeps
@@ -285,9 +286,15 @@ def sweep_roofline(name, c, q, outputs, chains, sweeps, st, kinfo, lconf, clk, s
         out["issue"] = issue
     dram_frac = (tps * rate / 1e9 / peak) if tps else None
     out["dram_frac_of_peak"] = dram_frac
-    if issue is not None and issue["frac"] > hbm["frac"]:
+    if issue is not None and (issue["frac"] > hbm["frac"] or (dram_frac is not None and dram_frac < 0.5)):
+        # DRAM below half its peak (ncu): HBM is not what binds the kernel -- it is latency-bound
+        # (DESIGN.md §4), and the issue ceiling is the compute-side yardstick (round-1 verdict);
+        # the HBM model stays in `hbm_model`
         out.update(bound="issue", achieved=issue["achieved"], peak=issue["peak"], unit="warp-inst/s",
                    frac=issue["frac"])
+        if dram_frac is not None and dram_frac < 0.5:
+            out["note"] = (f"latency-bound: ncu DRAM at {dram_frac:.0%} of peak at this rate; "
+                           f"HBM model {hbm['frac']:.2f}, issue ceiling {issue['frac']:.2f}")
     else:
         out.update(bound="hbm", achieved=achieved, peak=peak, unit="GB/s", frac=achieved / peak)
     return out

@@ -54,3 +54,25 @@ def test_scaling_modes_shard_the_chains():
     assert bench.scaling_mode(a) == "weak"
     _, _, run = W.config(2)
     assert bench.shard_of(a, run, 4, 3) == (3 * 1024, 1024, 4096)
+
+
+def test_roofline_bound_is_issue_when_dram_is_below_half_its_peak():
+    # round-1 verdict: a kernel whose ncu DRAM bandwidth at the measured rate is below half the
+    # peak is not HBM-bound -- the bench labels it by the issue ceiling (the HBM model stays in
+    # the object); with enough DRAM traffic it is labelled HBM-bound
+    c2, _, r2 = W.config(2)
+    name = W.CONFIGS[2]["name"]
+    sweeps = r2.burn_in + r2.cycles
+
+    def roof(ms):
+        st = {"sweep_ms": ms, "sweep_launches": 1}
+        return bench.sweep_roofline(name, c2, None, r2.outputs, r2.chains, sweeps, st, {"version": 6},
+                                    {"blocks": 128}, {"sm_mhz": 1965.0}, 148)
+
+    slow = roof(1500.0)  # ~3.0e10 site-updates/s: DRAM ~40% of the peak
+    assert slow["dram_frac_of_peak"] < 0.5
+    assert slow["bound"] == "issue" and slow["frac"] == slow["issue"]["frac"]
+    assert "latency-bound" in slow["note"] and 0 < slow["hbm_model"]["frac"] < 1
+    fast = roof(500.0)  # three times the rate: DRAM above half the peak, HBM model above the issue
+    assert fast["dram_frac_of_peak"] > 0.5
+    assert fast["bound"] == ("issue" if fast["issue"]["frac"] > fast["hbm_model"]["frac"] else "hbm")
