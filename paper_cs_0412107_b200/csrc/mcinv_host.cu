@@ -7,6 +7,7 @@
 // workspace and enqueues kernels on the caller's stream.
 #include <algorithm>
 #include <complex>
+#include <chrono>
 #include <cstdio>
 #include <cstring>
 #include <new>
@@ -586,6 +587,19 @@ Layout make_layout(const mcinv_ctx *ctx, const mcinv_run_args *a) {
 }
 
 
+// MCINV_HOST_TIMING=1: host planning phases to stderr (e2e diagnostics)
+struct HostTimer {
+    bool on = std::getenv("MCINV_HOST_TIMING") != nullptr;
+    std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+    void mark(const char *what) {
+        if (!on) return;
+        const auto now = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[mcinv host] %-28s %8.2f ms\n", what,
+                     std::chrono::duration<double, std::milli>(now - t).count());
+        t = now;
+    }
+};
+
 template <typename S>
 LevelDev *get_levels(mcinv_ctx *ctx, unsigned outputs) {
     const unsigned key = outputs & (MCINV_PATTERN | MCINV_TRACE);
@@ -608,7 +622,9 @@ LevelDev *get_levels(mcinv_ctx *ctx, unsigned outputs) {
     in.q_col = &ctx->h_q_col;
     in.q_val = &ctx->h_q_val;
     mcinv::LevelPlan &P = ld->host;
+    HostTimer ht;
     ld->error = mcinv::build_levels(in, P);
+    ht.mark("level plan");
     if (ld->error.empty()) {
         ld->D = P.D;
         ld->max_rows = P.max_rows;
@@ -747,6 +763,7 @@ LevelDev::Slots *get_slots(mcinv_ctx *ctx, LevelDev *lv, int R, int W, bool bloc
     }
     const int64_t nrec = (int64_t)xrec.size();
     const S *hd = reinterpret_cast<const S *>(xdsg.data());
+    HostTimer ht;
     // slot order: the list schedule (levels.h schedule_slots) with a slack of L = W groups
     // (the warps of a CTA); MCINV_SLOT_ORDER=level keeps plain level order (each level padded)
     const char *so = std::getenv("MCINV_SLOT_ORDER");
@@ -796,8 +813,10 @@ LevelDev::Slots *get_slots(mcinv_ctx *ctx, LevelDev *lv, int R, int W, bool bloc
                 chosen = cand[k];
             }
         }
+        ht.mark("slack candidates");
         order = mcinv::schedule_slots(nrec, xrec, xcol, R, chosen, blocks ? ecap : 0, sim);
     }
+    ht.mark("list schedule");
     for (int o : order) {
         if (o < 0) {
             rec.push_back(make_int4(-1, 0, 0, -1));
@@ -912,7 +931,9 @@ LevelDev::Slots *get_slots(mcinv_ctx *ctx, LevelDev *lv, int R, int W, bool bloc
             sl->maxb = std::max(sl->maxb, (int)bytes);
             gofs[g + 1] = (int64_t)blob.size();
         }
+        ht.mark("blocks + wait masks");
         if (upload(ctx, sl->blob, blob) != MCINV_OK || upload(ctx, sl->gofs, gofs) != MCINV_OK) return nullptr;
+        ht.mark("upload");
     }
     LevelDev::Slots *raw = sl.get();
     lv->slots[key] = std::move(sl);
