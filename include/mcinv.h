@@ -231,17 +231,19 @@ mcinv_status mcinv_set_timing(mcinv_ctx *ctx, int enable);
 mcinv_status mcinv_stats(mcinv_ctx *ctx, int64_t *launches, double *sweep_ms, int64_t *sweep_launches,
                          double *contract_ms, int64_t *contract_launches);
 
-/* Which sweep kernel the last mcinv_run used: 5 = dataflow kernel with
- * TMA-staged plan blocks (sweep5.cu, the default where it applies), 4 = the
- * same reading its plan through L1, 3 = level-scheduled kernel (C > 32 chains
- * per CTA, trace, more than 200k rows), 1 = row-by-row kernel (sweep.cu, one
- * thread per chain; the simple reference kernel). chains_per_warp = C, the
- * chains of one CTA (for 4/5 also the lanes of one row within a warp);
- * steps_per_sweep = levels D of the row DAG. MCINV_KERNEL=v1|v3|v4|v5 in the
+/* Which sweep kernel the last mcinv_run used: 6 = dataflow kernel with
+ * TMA-staged plan blocks and the two chains of a Box-Muller pair per thread
+ * (sweep6.cu; the default for real C with n <= 200k and no trace), 5 = the
+ * dataflow kernel with one chain per thread (sweep5.cu; complex C, trace runs,
+ * one chain per CTA), 4 = the same reading its plan through L1, 3 =
+ * level-scheduled kernel (C > 32 chains per CTA, deferred pattern pairs, more
+ * than 200k rows), 1 = row-by-row kernel (sweep.cu, one thread per chain; the
+ * simple reference kernel). chains_per_warp = C, the chains of one CTA;
+ * steps_per_sweep = levels D of the row DAG. MCINV_KERNEL=v1|v3|v4|v5|v6 in the
  * environment forces one (MCINV_E_INVALID if it does not apply). */
 mcinv_status mcinv_kernel_info(const mcinv_ctx *ctx, int *version, int *chains_per_warp, int64_t *steps_per_sweep);
 /* Launch layout of the last run's sweep kernel (the level and dataflow kernels):
- * threads per CTA, chains per thread K (1 or 2) and CTAs; 0 threads/blocks for
+ * threads per CTA, chains per thread K (1 or 2; 2 for v6) and CTAs; 0 threads/blocks for
  * the row-by-row kernel. For tests and the bench line. */
 mcinv_status mcinv_launch_config(const mcinv_ctx *ctx, int *threads, int *chains_per_thread, int *blocks);
 
